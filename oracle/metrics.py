@@ -1,0 +1,161 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+The paper's accuracy metric and its post hoc reconstruction, on CPU.
+
+* Eq. 5 (§4.3): total average L2 = (1/p) sum_i ||b_i - m_i||.
+  The printed sum runs i = 0..p while dividing by p; reading R9 takes
+  i = 1..p (p terms).
+* Eq. 6: Accuracy% = (C - L) / C * 100, C = cell side
+  (reading R10: C = extent / (N - 1), min over axes; the paper's printed
+  accuracy cells are (C - L)/C*100 truncated to 0.1 — pinned in
+  tests/golden/paper_tables.json).
+* Max-L2 folds: greatest max over intervals; average of
+  per-interval maxima.
+* Post hoc reconstruction (§3.2): Delaunay triangulation over the
+  start locations of valid basis flows of the own and adjacent blocks, then
+  barycentric interpolation of the end positions.  Reading R12: Qhull with
+  joggle (QJ) over spatial tiles of the hole bands.
+* Eq. 2 (§3.3): linear interpolation through a reconstructed hole
+  equals interpolation between its valid neighbours — used as the hole-fill
+  cross-check (grid_fill_1d).
+"""
+from __future__ import annotations
+
+import math
+from typing import Dict, Iterable, List, Tuple
+
+import numpy as np
+
+
+def total_avg_l2(b: np.ndarray, m: np.ndarray) -> float:
+    """Eq. 5 with i = 1..p (reading R9)."""
+    b = np.asarray(b, dtype=np.float64)
+    m = np.asarray(m, dtype=np.float64)
+    if b.shape != m.shape:
+        raise ValueError("length mismatch")
+    p = b.shape[0]
+    if p == 0:
+        raise ValueError("no particles")
+    return float(np.sqrt(((b - m) ** 2).sum(axis=1)).sum()) / p
+
+
+def accuracy_pct(L: float, C: float) -> float:
+    """Eq. 6: (C - L) / C * 100."""
+    if not C > 0:
+        raise ValueError("cell side must be positive")
+    return (C - L) / C * 100.0
+
+
+def paper_printed_accuracy(L: float, C: float) -> float:
+    """How the paper prints Eq. 6: truncated (floored) to one decimal
+    (reading R10; reproduces 33 of 35 printed cells)."""
+    return math.floor(accuracy_pct(L, C) * 10.0 + 1e-9) / 10.0
+
+
+def cell_side(grid) -> float:
+    """C = extent / (N - 1) per axis = h_a; min over axes (reading R10)."""
+    return float(min(grid.spacing[a] for a in range(grid.dim)))
+
+
+def max_l2_stats(per_interval_max: Iterable[float]) -> Tuple[float, float]:
+    """(greatest maximum, average maximum) over intervals."""
+    vals = [float(v) for v in per_interval_max]
+    if not vals:
+        raise ValueError("no intervals")
+    return max(vals), sum(vals) / len(vals)
+
+
+def grid_fill_1d(f: np.ndarray, valid: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """Eq. 1 / Eq. 2 along a lattice line: fill each invalid sample by linear
+    interpolation between its nearest valid neighbours (Eq. 1), then evaluate
+    the piecewise-linear interpolant at x.  Eq. 2 says this equals direct
+    interpolation between the valid neighbours."""
+    f = np.asarray(f, dtype=np.float64).copy()
+    valid = np.asarray(valid, dtype=bool)
+    idx = np.arange(f.size)
+    vi = idx[valid]
+    for i in idx[~valid]:
+        left = vi[vi < i]
+        right = vi[vi > i]
+        if left.size == 0 or right.size == 0:
+            raise ValueError("unfillable hole")
+        x0, x2 = left[-1], right[0]
+        f[i] = (i - x0) / (x2 - x0) * f[x2] + (x2 - i) / (x2 - x0) * f[x0]
+    return np.interp(x, idx.astype(np.float64), f)
+
+
+def barycentric_interpolate(points: np.ndarray, values: np.ndarray, queries: np.ndarray,
+                            joggle: bool = True):
+    """Delaunay over `points`, barycentric interpolation of `values`
+    at `queries`.  Returns (interpolated [m, k], inside mask [m])."""
+    from scipy.spatial import Delaunay
+    points = np.asarray(points, dtype=np.float64)
+    queries = np.asarray(queries, dtype=np.float64)
+    values = np.asarray(values, dtype=np.float64)
+    dim = points.shape[1]
+    tri = Delaunay(points, qhull_options="QJ" if joggle else None)
+    simp = tri.find_simplex(queries)
+    inside = simp >= 0
+    out = np.full((queries.shape[0], values.shape[1]), np.nan)
+    if inside.any():
+        s = simp[inside]
+        T = tri.transform[s]                       # [m, dim+1, dim]
+        r = queries[inside] - T[:, dim]
+        lam = np.einsum("mij,mj->mi", T[:, :dim], r)
+        lam = np.concatenate([lam, 1.0 - lam.sum(axis=1, keepdims=True)], axis=1)
+        verts = tri.simplices[s]                   # [m, dim+1]
+        out[inside] = np.einsum("mv,mvk->mk", lam, values[verts])
+    return out, inside
+
+
+def reconstruct_holes(g_seeds: np.ndarray, start: np.ndarray, end: np.ndarray,
+                      valid: np.ndarray, hole: np.ndarray, stride: int,
+                      margin: int = 4, tile: int = 16):
+    """Reconstruct end positions for `hole` seeds from the valid basis flows
+    around them (own + adjacent blocks: with the global seed set the union is
+    the same).  Spatial tiles of `tile` lattice steps, each
+    triangulating the valid seeds within `margin` lattice steps of the tile.
+    Returns (recon [n, dim] with NaN where not reconstructed, inside mask)."""
+    g = np.asarray(g_seeds) // stride
+    dim = start.shape[1]
+    recon = np.full(end.shape, np.nan)
+    inside = np.zeros(g.shape[0], dtype=bool)
+    hidx = np.nonzero(hole)[0]
+    if hidx.size == 0:
+        return recon, inside
+    tkey = g[hidx, :dim] // tile
+    uniq, inv = np.unique(tkey, axis=0, return_inverse=True)
+    vidx = np.nonzero(valid)[0]
+    gv = g[vidx, :dim]
+    for t in range(uniq.shape[0]):
+        hsel = hidx[inv.ravel() == t]
+        lo = uniq[t] * tile - margin
+        hi = (uniq[t] + 1) * tile + margin
+        m = np.all((gv >= lo) & (gv < hi), axis=1)
+        pts = vidx[m]
+        if pts.size < dim + 1:
+            continue
+        vals, ins = barycentric_interpolate(start[pts], end[pts], start[hsel])
+        recon[hsel] = vals
+        inside[hsel] = ins
+    return recon, inside
+
+
+def agreement(grid, g_seeds, start, bto_end, bto_status, comm_end, comm_status, stride):
+    """BTO-vs-comm flow-map agreement for one interval (§4.3):
+    over seeds valid in the comm flow map, b = BTO end if valid, else its
+    reconstruction; L = Eq. 5, accuracy = Eq. 6.  Seeds whose reconstruction
+    falls outside the hull are excluded and counted."""
+    comm_ok = np.asarray(comm_status) == 0
+    bto_ok = np.asarray(bto_status) == 0
+    hole = comm_ok & ~bto_ok
+    recon, inside = reconstruct_holes(g_seeds, start, bto_end, bto_ok, hole, stride)
+    b = np.where(bto_ok[:, None], bto_end, recon)
+    use = comm_ok & (bto_ok | inside)
+    diff = np.linalg.norm(b[use] - comm_end[use], axis=1)
+    L = float(diff.mean()) if diff.size else 0.0
+    C = cell_side(grid)
+    return dict(L=L, max_l2=float(diff.max()) if diff.size else 0.0,
+                accuracy=accuracy_pct(L, C), C=C, compared=int(use.sum()),
+                holes=int(hole.sum()), excluded=int((hole & ~inside).sum()),
+                discarded=int((~bto_ok).sum()), seeded=int(bto_ok.size))
