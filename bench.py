@@ -1,0 +1,450 @@
+#!/usr/bin/env python
+"""Benchmark: in situ Lagrangian flow-map extraction (arXiv 2004.02003) on B200.
+
+Metric (BASELINE.json): particle-steps/s at 1/2/4/8 B200 (BTO vs comm), % of
+the memory roofline, flow-map agreement %.
+
+Workload: C5 — ABC flow, 128^3 nodes per GPU (weak scaling, layouts (1,1,1),
+(2,1,1), (2,2,1), (2,2,2)), one seed per node (2,097,152 particles per GPU),
+interval 25.  A "step" is one interval: lag_seed + 25 x lag_advect_cycle +
+lag_extract (every §8(a) row).  value = particle-steps of all ranks / max-over-
+ranks device time of the step (CUDA events on the launching stream).  L2 is
+flushed (256 MB write) before every cycle, outside the timed events.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lag|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "particle-steps/s at 1/2/4/8 B200 (BTO vs comm); % of mem roofline; flow-map agree %"
+UNIT = "particle-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="lag", choices=["lag", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--no-comm", action="store_true", help="skip the comm-baseline arm")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--warm-l2", action="store_true", help="do not flush L2 between cycles")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (torch.distributed only for process groups)
+
+def dist_setup(n_gpus):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def broadcast_bytes(b, world, rank):
+    if world == 1:
+        return b
+    import torch.distributed as dist
+    obj = [b if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if r[4 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# the product arm
+
+class Arm:
+    """One block of the weak-scaling layout on this rank, driven through the
+    C ABI binding (paper_2004_02003_b200)."""
+
+    def __init__(self, cfg, rank, world, mode, nccl_id=None, host=False):
+        import torch
+        import lag_inputs as L
+        import paper_2004_02003_b200 as P
+        self.P = P
+        self.cfg = cfg
+        g = cfg["grid"]
+        self.block = L.decompose(g, cfg["layout"])[rank]
+        self.ghost = 1 if mode == P.LAG_COMM else 0
+        self.interval = cfg["interval"]
+        self.stream = torch.cuda.current_stream()
+        lo = [self.block.lo[a] - self.ghost if a < g.dim else 0 for a in range(3)]
+        ext = L.block_slice_extent(g, self.block, self.ghost)
+        hi = [lo[a] + ext[a] for a in range(3)]
+        # one interval's slices, generated on the device (fp64 -> fp32), untimed
+        self.slices = [L.field_at_nodes(cfg["field"], g, k * cfg["dt"], lo=lo, hi=hi,
+                                        device="cuda", backend="torch").contiguous()
+                       for k in range(self.interval + 1)]
+        self.slice_bytes = self.slices[0].numel() * 4
+        if host:
+            self.slices = [s.cpu().pin_memory() for s in self.slices]
+        pc = P.make_config(g.dim, g.nodes, g.origin, g.spacing, self.block.lo, self.block.hi,
+                           mode=mode, ghost=self.ghost, device=torch.cuda.current_device(),
+                           rank=rank, nranks=world if mode == P.LAG_COMM else 1,
+                           layout=cfg["layout"] if mode == P.LAG_COMM else (1, 1, 1),
+                           nccl_id=nccl_id, stream=self.stream.cuda_stream)
+        self.ctx = P.Context(pc)
+        self.n = self.ctx.seed(cfg["stride"])
+        dev = "cpu" if host else "cuda"
+        kw = dict(pin_memory=True) if host else {}
+        self.start = torch.empty((self.n, g.dim), dtype=torch.float64, device=dev, **kw)
+        self.end = torch.empty_like(self.start)
+        self.status = torch.empty((self.n,), dtype=torch.uint8, device=dev, **kw)
+
+
+def run_arm(arm, steps, flush, timed=True):
+    """Run `steps` intervals; returns per-piece event times (ms) and the
+    particle-steps done (from the library's device counters)."""
+    import torch
+    P = arm.P
+    s = arm.stream
+    t_adv, t_other, psteps = [], [], 0
+    st0 = arm.ctx.stats()["particle_steps"]
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if flush is not None:
+            flush.zero_()
+        e0.record(s)
+        arm.ctx.seed(arm.cfg["stride"])
+        e1.record(s)
+        pieces = [(e0, e1)]
+        advs = []
+        for c in range(arm.interval):
+            if flush is not None:
+                flush.zero_()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(s)
+            arm.ctx.advect(arm.slices[c], arm.slices[c + 1], arm.cfg["dt"])
+            a1.record(s)
+            advs.append((a0, a1))
+        if flush is not None:
+            flush.zero_()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(s)
+        arm.ctx.extract(arm.start, arm.end, arm.status, flags=P.LAG_NO_RESEED)
+        x1.record(s)
+        pieces.append((x0, x1))
+        torch.cuda.synchronize()
+        t_adv.append(sum(a.elapsed_time(b) for a, b in advs))
+        t_other.append(sum(a.elapsed_time(b) for a, b in pieces))
+    psteps = arm.ctx.stats()["particle_steps"] - st0
+    return t_adv, t_other, psteps
+
+
+def run_e2e(cfg, rank, world, steps, warmup):
+    """Same metric through the public C ABI with HOST buffers: pinned host
+    slices staged by the library (H2D inside the timed region) and the flow
+    map returned into pinned host arrays (D2H inside the timed region)."""
+    import torch
+    import paper_2004_02003_b200 as P
+    arm = Arm(cfg, rank, world, P.LAG_BTO, host=True)
+    h2d = arm.slice_bytes * (arm.interval + 1)
+    d2h = arm.start.numel() * 8 + arm.end.numel() * 8 + arm.status.numel()
+    times, ps = [], 0
+    for it in range(warmup + steps):
+        st0 = arm.ctx.stats()["particle_steps"]
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        arm.ctx.seed(cfg["stride"])
+        for c in range(arm.interval):
+            arm.ctx.advect(arm.slices[c], arm.slices[c + 1], cfg["dt"])
+        arm.ctx.extract(arm.start, arm.end, arm.status, flags=P.LAG_NO_RESEED)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        dt = allreduce_max(dt, world)
+        if it >= warmup:
+            times.append(dt)
+            ps += arm.ctx.stats()["particle_steps"] - st0
+    arm.ctx.close()
+    total_ps = allreduce_sum(ps, world)
+    return {"value": total_ps / sum(times), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * sum(times) / len(times),
+            "timing": "wall clock around synchronize, max over ranks"}
+
+
+def measured_peak():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config):
+    p = os.path.join(ROOT, "profiles", "advect_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(config)
+    except Exception:
+        return None
+
+
+def cpu_baseline(cfg, seconds_target=12.0):
+    """The fp64 oracle as it stands, on the host cores, on a bounded sample of
+    the same workload: a strided subset of the block's seeds advanced over the
+    first cycles of the interval."""
+    import lag_inputs as L
+    import oracle
+    g = cfg["grid"]
+    block = L.decompose(g, cfg["layout"])[0]
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    seeds = oracle.seeds(g, block.lo, block.hi, cfg["stride"])
+    ncyc = 5
+    sl = [L.field_at_nodes(cfg["field"], g, k * cfg["dt"]) for k in range(ncyc + 1)]
+    # calibrate on a small sample, then size for ~seconds_target
+    n0 = min(20000, seeds.shape[0])
+    it = oracle.Interval(g, block.lo, block.hi, cfg["stride"], g_seeds=seeds[:: max(1, seeds.shape[0] // n0)][:n0])
+    t0 = time.perf_counter()
+    it.cycle(sl[0], sl[1], cfg["dt"])
+    per = (time.perf_counter() - t0) / it.n
+    n = int(min(seeds.shape[0], max(n0, seconds_target / (per * ncyc))))
+    pick = seeds[:: max(1, seeds.shape[0] // n)][:n]
+    it = oracle.Interval(g, block.lo, block.hi, cfg["stride"], g_seeds=pick)
+    t0 = time.perf_counter()
+    for c in range(ncyc):
+        it.cycle(sl[c], sl[c + 1], cfg["dt"])
+    el = time.perf_counter() - t0
+    return {"value": it.n * ncyc / el, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]),
+            "kind": "oracle",
+            "sample": f"{it.n} of {seeds.shape[0]} seeds (strided) of the {cfg['name']} block, "
+                      f"{ncyc} cycles, fp64 C oracle with OpenMP; {el:.1f} s"}
+
+
+def reference_arm(args):
+    """--impl reference: the oracle on the host cores as the reference arm."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import lag_inputs as L
+    cfg = L.make_config(args.config, nranks=1)
+    vals = []
+    for _ in range(max(1, args.steps)):
+        vals.append(cpu_baseline(cfg, seconds_target=max(2.0, 60.0 / max(1, args.steps + args.warmup))))
+    v = statistics.median(x["value"] for x in vals)
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{cfg['name']} ABC 128^3 block, stride 1, interval 25 (bounded sample)"},
+           "cpu_baseline": {"kind": "oracle", "cores": vals[0]["cores"], "sample": vals[0]["sample"],
+                            "value": v},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    import torch
+    import lag_inputs as L
+    import paper_2004_02003_b200 as P
+    rank, world, local = dist_setup(args.gpus)
+    cfg = L.make_config(args.config, nranks=world)
+    flush = None if args.warm_l2 else torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    # ---------------- BTO (the paper's method): headline ----------------
+    arm = Arm(cfg, rank, world, P.LAG_BTO)
+    run_arm(arm, args.warmup, flush)
+    launches0 = arm.ctx.launches()
+    clk = ClockSampler(local)
+    clk.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    t_adv, t_other, psteps = run_arm(arm, args.steps, flush)
+    barrier(world)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    clocks = clk.stop()
+    launches = arm.ctx.launches() - launches0
+    dev_ms = sum(t_adv) + sum(t_other)
+    adv_ms = sum(t_adv)
+    dev_ms_max = allreduce_max(dev_ms, world)
+    adv_ms_max = allreduce_max(adv_ms, world)
+    total_ps = allreduce_sum(psteps, world)
+    value = total_ps / (dev_ms_max / 1e3)
+    # roofline of the dominant kernel (advect): algorithmic bytes per launch =
+    # 32 B x active particles (float4 read + write) + both slices read once
+    # (stride 1 touches every node) — DESIGN.md §roofline
+    cycles = args.steps * arm.interval
+    alg_bytes = 32.0 * psteps + cycles * 2.0 * arm.slice_bytes
+    achieved = alg_bytes / (adv_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    st = arm.ctx.stats()
+    n_per_rank = arm.n
+    arm.ctx.close()
+    del arm
+
+    # ---------------- comm baseline (Lagrangian-MPI analogue) ----------------
+    comm = None
+    if not args.no_comm:
+        nid = broadcast_bytes(P.lag_nccl_unique_id() if rank == 0 else None, world, rank) if world > 1 else None
+        carm = Arm(cfg, rank, world, P.LAG_COMM, nccl_id=nid)
+        run_arm(carm, args.warmup, flush)
+        barrier(world)
+        c_adv, c_other, c_ps = run_arm(carm, args.steps, flush)
+        c_ms = allreduce_max(sum(c_adv) + sum(c_other), world)
+        c_total = allreduce_sum(c_ps, world)
+        cst = carm.ctx.stats()
+        comm = {"value": c_total / (c_ms / 1e3), "unit": UNIT,
+                "ms_per_step": c_ms / args.steps,
+                "ms_per_cycle": allreduce_max(sum(c_adv), world) / cycles,
+                "bto_speedup": (c_ms / dev_ms_max),
+                "sent_last_interval": int(cst["sent"]), "received_last_interval": int(cst["received"]),
+                "exchange": "NCCL grouped send/recv per cycle: halo (G=1, faces+edges+corners) + particle slots"}
+        carm.ctx.close()
+        del carm
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(cfg, rank, world, max(2, args.steps // 2), 1)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg['name']}: ABC flow 128^3 nodes per GPU, 1 seed/node "
+                                   f"({n_per_rank} particles/GPU), interval {cfg['interval']}, BTO",
+                       "layout": list(cfg["layout"]), "global_nodes": list(cfg["grid"].nodes),
+                       "particles_per_gpu": n_per_rank, "cycles_per_step": arm_interval(cfg),
+                       "step": "lag_seed + interval x lag_advect_cycle + lag_extract",
+                       "l2": "warm (no flush)" if args.warm_l2 else
+                             "flushed (256 MB write) before every cycle, outside the timed events",
+                       "wall_s_timed_region": wall,
+                       "ms_per_cycle": adv_ms_max / cycles,
+                       "discarded_last_interval": int(st["term_boundary"] + st["exit_domain"]),
+                       "parallelism": f"dp{world} (one block per GPU, no collective)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(cfg["name"]),
+                         "kernel": "advect_kernel<3,true>", "peak_source": peak_src,
+                         "alg_bytes_per_launch": alg_bytes / cycles},
+            "comm": comm,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def arm_interval(cfg):
+    return cfg["interval"]
+
+
+if __name__ == "__main__":
+    main()

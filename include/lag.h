@@ -1,0 +1,201 @@
+/*
+ * lag.h — C ABI of liblag, the B200-native in situ Lagrangian flow-map
+ * extraction hot path of arXiv 2004.02003 (Sane, Childs, Bujack:
+ * "Scalable in situ Lagrangian flow map extraction: demonstrating the
+ * viability of a communication-free model").
+ *
+ * Citations: P:nnn = the paper text line nnn.
+ *
+ * What the library computes, per rank block (one context per block):
+ *   - lag_seed:  uniform seeding of basis-flow particles on the grid nodes
+ *                (§2.3: "particles are seeded along a uniform grid";
+ *                data reduction 1:X, X = stride^dim).
+ *   - lag_advect_cycle: one RK4 step of every active particle per simulation
+ *                cycle (§3.1, §2.2) through the velocity field,
+ *                multilinear in space on the uniform grid and linear in time
+ *                between the cycle's two slices v_t and v_{t+1}; particles
+ *                leaving the block are terminated in place (BTO, P:190-196
+ *                §3.1) or handed to the owning rank (COMM, the paper's
+ *                Lagrangian-MPI baseline after Agranovsky et al., P:153,
+ *                P:206-208).  Particle management (validity tracking and
+ *                compaction so invalid particles are not launched) is
+ *                fused into the same kernel.
+ *   - lag_extract: at the end of an interval ("write cycle")
+ *                returns the basis flows (start, end, validity) in the block's
+ *                seed order, after returning particles to their origin rank in
+ *                COMM mode, and reseeds for the next interval.
+ *
+ * Conventions
+ *   - Every call returns lag_status: 0 = LAG_OK, negative = error.  No C++
+ *     exception or abort crosses the ABI.  lag_last_error() gives a message.
+ *   - Grid: nodes n in [0, N_a), position x(n) = origin + n * spacing.
+ *     Domain Omega = prod_a [origin_a, origin_a + (N_a - 1) spacing_a], closed.
+ *   - Block: owned nodes [block_lo, block_hi) per axis, half-open; a block
+ *     whose block_hi == N owns the closed upper face.  Rank = x-fastest block
+ *     index in `layout`.
+ *   - Velocity slice arrays (borrowed, read-only in BTO mode): fp32, AoS
+ *     (vx, vy[, vz]) per node, x fastest, dense rows.  Extent per axis =
+ *     (min(block_hi + 1, N) - block_lo) + 2 * ghost nodes: the owned nodes,
+ *     the neighbour's first (shared) node plane when block_hi < N, and `ghost`
+ *     layers on every side (allocated even at global faces, never read there).
+ *     Element (0,0,0) is global node block_lo - ghost.
+ *   - Pointers passed to lag_advect_cycle / lag_extract may be device pointers
+ *     (used in place, stream-ordered on cfg.stream) or host pointers (the
+ *     library stages them through device buffers with cudaMemcpyAsync; this is
+ *     the end-to-end path).
+ *   - Not thread-safe per context.  Several contexts may share a device.
+ */
+#ifndef LAG_H
+#define LAG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LAG_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define LAG_API __attribute__((visibility("default")))
+#else
+#define LAG_API
+#endif
+
+typedef struct lag_ctx_s* lag_ctx;
+
+typedef enum {
+    LAG_OK = 0,
+    LAG_EINVAL = -1,      /* bad argument / configuration                      */
+    LAG_ESTATE = -2,      /* call out of order (advect before seed, ...)       */
+    LAG_EEMPTY = -3,      /* the block holds no seed at this stride            */
+    LAG_ENOMEM = -4,      /* device allocation failed                          */
+    LAG_ECUDA = -5,       /* CUDA runtime error                                */
+    LAG_ENCCL = -6,       /* NCCL error (COMM mode)                            */
+    LAG_EOVERFLOW = -7,   /* latched: an exchange slot or the particle list overflowed */
+    LAG_EGHOST = -8,      /* latched: a stage sample fell outside the ghost layers (CFL >= 1) */
+    LAG_ENONFINITE = -9   /* latched: non-finite velocity reached a particle   */
+} lag_status;
+
+typedef enum { LAG_BTO = 0, LAG_COMM = 1 } lag_mode;
+
+/* Per-basis-flow status returned by lag_extract. */
+typedef enum {
+    LAG_VALID = 0,          /* stayed in the block (BTO) / domain (COMM) for the whole interval */
+    LAG_TERM_BOUNDARY = 1,  /* BTO: a stage sample or the update left the block; end = pre-step position */
+    LAG_EXIT_DOMAIN = 2     /* a stage sample or the update left the global domain; end = pre-step position */
+} lag_flow_status;
+
+/* lag_extract flags */
+#define LAG_NO_RESEED 1u    /* do not reseed after extracting */
+
+typedef struct {
+    int32_t dim;                 /* 2 or 3                                                */
+    int32_t mode;                /* lag_mode                                              */
+    int64_t global_nodes[3];     /* N_a >= 2 on used axes; unused axis = 1                */
+    double  origin[3];           /* o_a, finite                                           */
+    double  spacing[3];          /* h_a > 0, finite                                       */
+    int64_t block_lo[3];         /* owned node range [lo, hi), 0 <= lo < hi <= N          */
+    int64_t block_hi[3];
+    int32_t ghost;               /* G ghost node layers per side in the slice arrays;
+                                    COMM requires G >= 1; BTO reads none                  */
+    int32_t device;              /* CUDA device ordinal                                   */
+    int32_t rank;                /* COMM: this block's rank (x-fastest in layout)         */
+    int32_t nranks;              /* COMM: number of ranks = prod(layout)                  */
+    int32_t layout[3];           /* COMM: blocks per axis                                 */
+    int32_t pad_;
+    const void* nccl_id;         /* COMM: 128-byte ncclUniqueId shared by all ranks (from
+                                    lag_nccl_unique_id on one rank); NULL for BTO         */
+    void*   stream;              /* cudaStream_t the library enqueues on (borrowed);
+                                    NULL = the legacy default stream                     */
+} lag_config;
+
+typedef struct {
+    int64_t seeded;          /* seeds placed at the last lag_seed                           */
+    int64_t active;          /* particles currently advancing on this rank                  */
+    int64_t term_boundary;   /* this interval: BTO terminations at the block boundary       */
+    int64_t exit_domain;     /* this interval: global-domain exits                          */
+    int64_t sent;            /* this interval: particles handed to other ranks (COMM)       */
+    int64_t received;        /* this interval: particles received from other ranks (COMM)   */
+    int64_t particle_steps;  /* cumulative RK4 particle-steps since lag_init                */
+    int64_t cycles;          /* cumulative lag_advect_cycle calls since lag_init            */
+    int32_t device_error;    /* latched async condition as a lag_status (0 = none)          */
+    int32_t pad_;
+} lag_stats_t;
+
+/*
+ * lag_init — validate the configuration, allocate every device buffer the
+ * context needs (particle list, exchange slots, staging) and, in COMM mode,
+ * join the NCCL communicator.  Collective in COMM mode (all ranks must call).
+ * Errors: LAG_EINVAL (dims, spacing, bounds, layout, ghost, packed seed-node
+ * width > 32 bits), LAG_ECUDA, LAG_ENCCL, LAG_ENOMEM.  *out is NULL on error.
+ */
+LAG_API lag_status lag_init(const lag_config* cfg, lag_ctx* out);
+
+/*
+ * lag_seed — start a new interval: place one particle on every global lattice
+ * node g with g_a = 0 (mod stride) and block_lo_a <= g_a < block_hi_a (x-fastest
+ * seed order), discarding any previous particles (reading R4 in
+ * DESIGN.md).  *n_seeds_out = number of seeds.
+ * Errors: LAG_EINVAL (stride < 1), LAG_EEMPTY (no lattice node in the block).
+ */
+LAG_API lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out);
+
+/*
+ * lag_advect_cycle — advance every active particle by one RK4 step of size dt
+ * (physical time units) through v(x, t) = (1 - a) Tri(v_t, x) + a Tri(v_t1, x),
+ * a = 0, 1/2, 1/2, 1 for the four stages.
+ * BTO: no communication, no host synchronisation; particles with any stage
+ * sample or updated position outside the block terminate at their pre-step
+ * position (status LAG_TERM_BOUNDARY).  COMM (collective): fills the ghost
+ * layers of v_t1 (and of v_t unless it is the previous call's v_t1) from the
+ * neighbours, advances, and hands particles whose updated position lies in
+ * another block to its owner.  In COMM mode the ghost layers of the slice
+ * arrays are written; interior nodes never are.
+ * v_t, v_t1: slice arrays (see Conventions), device or host memory.
+ * Errors: LAG_ESTATE (no lag_seed), LAG_EINVAL (dt <= 0 or non-finite, NULL
+ * slice), LAG_ECUDA, LAG_ENCCL.  Async conditions are latched (see lag_stats).
+ */
+LAG_API lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, double dt);
+
+/*
+ * lag_extract — end of interval (write cycle).  COMM: first returns every
+ * particle to its origin rank (collective).  Writes, for each of the n seeds
+ * of the last lag_seed in seed order: start[i][dim] = x(g_i), end[i][dim] =
+ * o + (g_i + d_i) h in fp64, status[i] = lag_flow_status.  Any of start, end,
+ * status may be NULL (skipped); each may be a host or device pointer with
+ * room for `capacity` entries.  Synchronises the stream and reports latched
+ * asynchronous errors (LAG_EOVERFLOW, LAG_EGHOST, LAG_ENONFINITE) after
+ * writing the outputs.  Then reseeds with the same stride unless
+ * flags & LAG_NO_RESEED.
+ * Errors: LAG_ESTATE (no lag_seed), LAG_EINVAL (capacity < n).
+ */
+LAG_API lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8_t* status,
+                       int64_t capacity, int64_t* n_out, uint32_t flags);
+
+/* lag_stats — synchronise the stream and report counters (see lag_stats_t). */
+LAG_API lag_status lag_stats(lag_ctx ctx, lag_stats_t* out);
+
+/* lag_destroy — free every resource of the context (NULL is a no-op). */
+LAG_API lag_status lag_destroy(lag_ctx ctx);
+
+/* lag_last_error — message of the last failing call on ctx (ctx may be NULL
+ * for lag_init failures; thread-local).  Never NULL. */
+LAG_API const char* lag_last_error(lag_ctx ctx);
+
+/* lag_nccl_unique_id — write a fresh 128-byte ncclUniqueId into out (call on
+ * one rank, broadcast to the others, pass as lag_config.nccl_id). */
+LAG_API lag_status lag_nccl_unique_id(void* out, int64_t out_bytes);
+
+/* lag_kernel_launches — number of kernels the context has launched since
+ * lag_init (instrumentation for the benchmark's gpu_launches claim). */
+LAG_API int64_t lag_kernel_launches(lag_ctx ctx);
+
+/* lag_abi_version — LAG_ABI_VERSION the library was built with. */
+LAG_API int32_t lag_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LAG_H */

@@ -65,7 +65,8 @@ def _load():
         _lib.orc_cycle.argtypes = [P(_Grid), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
                                    ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
-                                   ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]
+                                   ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         _lib.orc_rk4_free.argtypes = [P(_Grid), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
                                       ctypes.c_int64, ctypes.c_void_p]
     return _lib
@@ -147,7 +148,8 @@ class Interval:
     domain (block := Omega), which is what the exchange baseline computes
     (reading R7)."""
 
-    def __init__(self, grid, lo, hi, stride: int, mode: int = BTO, g_seeds=None):
+    def __init__(self, grid, lo, hi, stride: int, mode: int = BTO, g_seeds=None,
+                 faces=None):
         self.grid = grid
         self.mode = mode
         self.lo = np.array(lo, dtype=np.int64)
@@ -164,6 +166,12 @@ class Interval:
         self.status = np.zeros(n, dtype=np.uint8)
         self.term_cycle = np.full(n, -1, dtype=np.int32)
         self.cycle_index = 0
+        # excuse-band instrumentation: faces = (lo, hi) of the block whose
+        # boundary decides the flags (defaults to this block)
+        flo, fhi = faces if faces is not None else (lo, hi)
+        self.flo = np.array(flo, dtype=np.int64)
+        self.fhi = np.array(fhi, dtype=np.int64)
+        self.min_face = np.full(n, np.inf)
 
     @property
     def n(self) -> int:
@@ -176,7 +184,8 @@ class Interval:
                       int(self.mode), _ptr(V0), _ptr(V1), float(dt), self.n,
                       _ptr(self.pos), _ptr(self.status), _ptr(self.term_cycle),
                       int(self.cycle_index),
-                      _ptr(touched) if touched is not None else None)
+                      _ptr(touched) if touched is not None else None,
+                      _ptr(self.flo), _ptr(self.fhi), _ptr(self.min_face))
         self.cycle_index += 1
 
     def active(self) -> int:
@@ -184,10 +193,10 @@ class Interval:
 
 
 def run_interval(grid, lo, hi, stride, slices: Iterable, dt: float, mode: int = BTO,
-                 g_seeds=None) -> Interval:
+                 g_seeds=None, faces=None) -> Interval:
     """Drive one interval given an iterable of consecutive global slices
     V_c, V_{c+1}, ... (len = cycles + 1)."""
-    it = Interval(grid, lo, hi, stride, mode, g_seeds)
+    it = Interval(grid, lo, hi, stride, mode, g_seeds, faces)
     prev = None
     for V in slices:
         if prev is not None:

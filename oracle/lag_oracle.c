@@ -136,6 +136,22 @@ static int in_block(const orc_grid* g, const int64_t* lo, const int64_t* hi, con
     return 1;
 }
 
+/* Smallest distance, in cell units of its axis, from q to any block face or
+ * global face (the flag-parity excuse band, reading R14). */
+static double face_distance(const orc_grid* g, const int64_t* flo, const int64_t* fhi, const double* q)
+{
+    double best = INFINITY;
+    for (int a = 0; a < g->dim; ++a) {
+        double u = (q[a] - g->o[a]) / g->h[a];
+        double faces[4] = {0.0, (double)(g->N[a] - 1), (double)flo[a], (double)fhi[a]};
+        for (int k = 0; k < 4; ++k) {
+            double dd = fabs(u - faces[k]);
+            if (dd < best) best = dd;
+        }
+    }
+    return best;
+}
+
 /* Sample test of one RK4 stage point / updated position.
  * Returns ORC_VALID, ORC_EXIT_DOMAIN or ORC_TERM_BOUNDARY (BTO only). */
 static int classify(const orc_grid* g, const int64_t* lo, const int64_t* hi, int mode, const double* q)
@@ -164,7 +180,7 @@ static const double RK_B[4]     = {1.0, 2.0, 2.0, 1.0};
  */
 static int rk4_step(const orc_grid* g, const int64_t* lo, const int64_t* hi, int mode,
                     int check, const float* V0, const float* V1, double dt, double* x,
-                    uint8_t* touched)
+                    uint8_t* touched, const int64_t* flo, const int64_t* fhi, double* mind)
 {
     const int d = g->dim;
     double k[4][3];
@@ -172,6 +188,10 @@ static int rk4_step(const orc_grid* g, const int64_t* lo, const int64_t* hi, int
     for (int s = 0; s < 4; ++s) {
         double q[3] = {0.0, 0.0, 0.0};
         for (int a = 0; a < d; ++a) q[a] = x[a] + RK_BETA[s] * dt * kprev[a];
+        if (mind && s > 0) {
+            double fd = face_distance(g, flo, fhi, q);
+            if (fd < *mind) *mind = fd;
+        }
         if (check) {
             int outcome = classify(g, lo, hi, mode, q);
             if (outcome != ORC_VALID) return outcome;
@@ -196,6 +216,10 @@ static int rk4_step(const orc_grid* g, const int64_t* lo, const int64_t* hi, int
         for (int s = 0; s < 4; ++s) sum += RK_B[s] * k[s][a];
         xn[a] = x[a] + dt / 6.0 * sum;
     }
+    if (mind) {
+        double fd = face_distance(g, flo, fhi, xn);
+        if (fd < *mind) *mind = fd;
+    }
     if (check) {
         int outcome = classify(g, lo, hi, mode, xn);
         if (outcome != ORC_VALID) return outcome;
@@ -213,7 +237,7 @@ static int rk4_step(const orc_grid* g, const int64_t* lo, const int64_t* hi, int
 void orc_cycle(const orc_grid* g, const int64_t* lo, const int64_t* hi, int32_t mode,
                const float* V0, const float* V1, double dt, int64_t n,
                double* pos, uint8_t* status, int32_t* term_cycle, int32_t cycle,
-               uint8_t* touched)
+               uint8_t* touched, const int64_t* flo, const int64_t* fhi, double* min_face)
 {
     const int d = g->dim;
 #pragma omp parallel for schedule(static)
@@ -221,7 +245,8 @@ void orc_cycle(const orc_grid* g, const int64_t* lo, const int64_t* hi, int32_t 
         if (status[p] != ORC_VALID) continue;
         double x[3] = {0.0, 0.0, 0.0};
         for (int a = 0; a < d; ++a) x[a] = pos[p * d + a];
-        int outcome = rk4_step(g, lo, hi, mode, 1, V0, V1, dt, x, touched);
+        int outcome = rk4_step(g, lo, hi, mode, 1, V0, V1, dt, x, touched, flo, fhi,
+                               min_face ? &min_face[p] : NULL);
         if (outcome == ORC_VALID) {
             for (int a = 0; a < d; ++a) pos[p * d + a] = x[a];
         } else {
@@ -240,7 +265,7 @@ void orc_rk4_free(const orc_grid* g, const float* V0, const float* V1, double dt
     for (int64_t p = 0; p < n; ++p) {
         double x[3] = {0.0, 0.0, 0.0};
         for (int a = 0; a < d; ++a) x[a] = pos[p * d + a];
-        rk4_step(g, NULL, NULL, ORC_COMM, 0, V0, V1, dt, x, NULL);
+        rk4_step(g, NULL, NULL, ORC_COMM, 0, V0, V1, dt, x, NULL, NULL, NULL, NULL);
         for (int a = 0; a < d; ++a) pos[p * d + a] = x[a];
     }
 }

@@ -1,0 +1,470 @@
+// lag_api.cu — C ABI of liblag (include/lag.h): validation, device memory,
+// launches.  Kernels: lag_kernels.cuh.  COMM exchange: lag_comm.cu.
+//
+// The product path has no CPU fallback: every step of the hot path runs in
+// the kernels below; host code only validates, allocates and enqueues.
+#include "lag.h"
+#include "lag_internal.h"
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+using namespace lag;
+
+static thread_local std::string g_init_error = "no error";
+
+int lag_set_error(lag_ctx_s* ctx, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->msg = buf; else g_init_error = buf;
+    return 0;
+}
+
+#define CK(call)                                                                   \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess) {                                                   \
+            lag_set_error(ctx, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                          __FILE__, __LINE__);                                     \
+            return e_ == cudaErrorMemoryAllocation ? LAG_ENOMEM : LAG_ECUDA;      \
+        }                                                                          \
+    } while (0)
+
+static int bits_for(int64_t n) {       // bits to hold values 0..n-1 (>= 1)
+    int b = 1;
+    while ((int64_t(1) << b) < n) ++b;
+    return b;
+}
+
+template <typename T>
+static lag_status dmalloc(lag_ctx_s* ctx, T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+    if (e != cudaSuccess) {
+        lag_set_error(ctx, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+        return LAG_ENOMEM;
+    }
+    return LAG_OK;
+}
+
+static void dfree(void* p) { if (p) cudaFree(p); }
+
+// ---------------------------------------------------------------------------
+
+extern "C" int32_t lag_abi_version(void) { return LAG_ABI_VERSION; }
+
+extern "C" const char* lag_last_error(lag_ctx ctx) {
+    return ctx ? ctx->msg.c_str() : g_init_error.c_str();
+}
+
+extern "C" int64_t lag_kernel_launches(lag_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+static lag_status validate(const lag_config* c) {
+    lag_ctx_s* ctx = nullptr;
+    if (!c) { lag_set_error(ctx, "cfg is NULL"); return LAG_EINVAL; }
+    if (c->dim != 2 && c->dim != 3) { lag_set_error(ctx, "dim must be 2 or 3 (got %d)", c->dim); return LAG_EINVAL; }
+    if (c->mode != LAG_BTO && c->mode != LAG_COMM) { lag_set_error(ctx, "mode must be LAG_BTO or LAG_COMM"); return LAG_EINVAL; }
+    int64_t total_bits = 0;
+    for (int a = 0; a < 3; ++a) {
+        const bool used = a < c->dim;
+        const int64_t N = c->global_nodes[a];
+        if (used) {
+            if (N < 2 || N > (int64_t(1) << 30)) { lag_set_error(ctx, "global_nodes[%d] = %lld must be in [2, 2^30]", a, (long long)N); return LAG_EINVAL; }
+            if (!(c->spacing[a] > 0.0) || !std::isfinite(c->spacing[a])) { lag_set_error(ctx, "spacing[%d] must be finite and > 0", a); return LAG_EINVAL; }
+            if (!std::isfinite(c->origin[a])) { lag_set_error(ctx, "origin[%d] must be finite", a); return LAG_EINVAL; }
+            if (!(0 <= c->block_lo[a] && c->block_lo[a] < c->block_hi[a] && c->block_hi[a] <= N)) {
+                lag_set_error(ctx, "block [%lld, %lld) on axis %d must satisfy 0 <= lo < hi <= N = %lld", (long long)c->block_lo[a], (long long)c->block_hi[a], a, (long long)N);
+                return LAG_EINVAL;
+            }
+            total_bits += bits_for(N);
+        } else if (N != 1 || c->block_lo[a] != 0 || c->block_hi[a] != 1) {
+            lag_set_error(ctx, "unused axis %d must have global_nodes = 1 and block [0, 1)", a);
+            return LAG_EINVAL;
+        }
+    }
+    if (total_bits > 32 || (c->dim == 3 && bits_for(c->global_nodes[0]) + bits_for(c->global_nodes[1]) >= 32)) {
+        lag_set_error(ctx, "grid too large: the packed seed node needs %lld > 32 bits", (long long)total_bits);
+        return LAG_EINVAL;
+    }
+    if (c->ghost < 0 || c->ghost > 8) { lag_set_error(ctx, "ghost must be in [0, 8]"); return LAG_EINVAL; }
+    if (c->mode == LAG_COMM) {
+        if (c->ghost < 1) { lag_set_error(ctx, "COMM mode needs ghost >= 1"); return LAG_EINVAL; }
+        int64_t prod = 1;
+        for (int a = 0; a < 3; ++a) {
+            if (c->layout[a] < 1 || (a >= c->dim && c->layout[a] != 1)) { lag_set_error(ctx, "bad layout"); return LAG_EINVAL; }
+            prod *= c->layout[a];
+        }
+        if (prod != c->nranks || c->rank < 0 || c->rank >= c->nranks) { lag_set_error(ctx, "rank/nranks/layout mismatch"); return LAG_EINVAL; }
+        if (c->nranks > 1 && !c->nccl_id) { lag_set_error(ctx, "COMM mode with nranks > 1 needs nccl_id"); return LAG_EINVAL; }
+    }
+    // slice extent must fit 32-bit element offsets
+    int64_t nodes = 1;
+    for (int a = 0; a < c->dim; ++a)
+        nodes *= (std::min(c->block_hi[a] + 1, c->global_nodes[a]) - c->block_lo[a] + 2 * c->ghost);
+    if (nodes * c->dim >= (int64_t(1) << 31)) { lag_set_error(ctx, "block slice too large for 32-bit offsets"); return LAG_EINVAL; }
+    return LAG_OK;
+}
+
+extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
+    if (out) *out = nullptr;
+    lag_ctx_s* ctx = nullptr;
+    if (!out) { lag_set_error(ctx, "out is NULL"); return LAG_EINVAL; }
+    lag_status st = validate(cfg);
+    if (st != LAG_OK) return st;
+
+    ctx = new (std::nothrow) lag_ctx_s();
+    if (!ctx) { lag_set_error(nullptr, "out of host memory"); return LAG_ENOMEM; }
+    ctx->cfg = *cfg;
+    ctx->stream = (cudaStream_t)cfg->stream;
+    {
+        cudaError_t e = cudaSetDevice(cfg->device);
+        if (e != cudaSuccess) {
+            lag_set_error(nullptr, "cudaSetDevice(%d): %s", cfg->device, cudaGetErrorString(e));
+            delete ctx;
+            return LAG_ECUDA;
+        }
+    }
+    const int D = cfg->dim;
+    for (int a = 0; a < 3; ++a) {
+        const bool used = a < D;
+        ctx->ext[a] = used ? (int)(std::min(cfg->block_hi[a] + 1, cfg->global_nodes[a]) - cfg->block_lo[a] + 2 * cfg->ghost) : 1;
+        ctx->base[a] = used ? (int)(cfg->block_lo[a] - cfg->ghost) : 0;
+    }
+    ctx->bits[0] = bits_for(cfg->global_nodes[0]);
+    ctx->bits[1] = bits_for(cfg->global_nodes[1]);
+    ctx->bits[2] = D == 3 ? bits_for(cfg->global_nodes[2]) : 0;
+    ctx->slice_floats = (int64_t)ctx->ext[0] * ctx->ext[1] * ctx->ext[2] * D;
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+    ctx->num_sms = dev_sms;
+
+    // max seeds at stride 1 bounds every later seeding
+    int64_t owned = 1;
+    for (int a = 0; a < D; ++a) owned *= (cfg->block_hi[a] - cfg->block_lo[a]);
+    ctx->max_seeds = owned;
+    // COMM: particles migrate in; keep room for 2x the owned nodes (+ tail tiles)
+    ctx->cap = cfg->mode == LAG_COMM ? 2 * owned + 64 * kTile : owned;
+    ctx->cap_tiles = (ctx->cap + kTile - 1) / kTile;
+
+    auto fail = [&](lag_status s) {
+        std::string m = ctx->msg;
+        lag_destroy(ctx);
+        g_init_error = m;
+        return s;
+    };
+    if ((st = dmalloc(ctx, &ctx->state, (size_t)ctx->cap_tiles * kTile)) != LAG_OK) return fail(st);
+    if ((st = dmalloc(ctx, &ctx->tile_count, (size_t)ctx->cap_tiles)) != LAG_OK) return fail(st);
+    if ((st = dmalloc(ctx, &ctx->dead_rec, (size_t)ctx->cap)) != LAG_OK) return fail(st);
+    if ((st = dmalloc(ctx, &ctx->dead_info, (size_t)ctx->cap)) != LAG_OK) return fail(st);
+    if ((st = dmalloc(ctx, &ctx->words, (size_t)kWords)) != LAG_OK) return fail(st);
+    if ((st = dmalloc(ctx, &ctx->counters, (size_t)CNT_N)) != LAG_OK) return fail(st);
+    if ((st = dmalloc(ctx, &ctx->out_start, (size_t)owned * D)) != LAG_OK) return fail(st);
+    if ((st = dmalloc(ctx, &ctx->out_end, (size_t)owned * D)) != LAG_OK) return fail(st);
+    if ((st = dmalloc(ctx, &ctx->out_status, (size_t)owned)) != LAG_OK) return fail(st);
+    {
+        cudaError_t e = cudaMemsetAsync(ctx->counters, 0, CNT_N * sizeof(unsigned long long), ctx->stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(ctx->words, 0, kWords * sizeof(uint32_t), ctx->stream);
+        if (e != cudaSuccess) { lag_set_error(ctx, "memset: %s", cudaGetErrorString(e)); return fail(LAG_ECUDA); }
+    }
+    if (cfg->mode == LAG_COMM) {
+        st = lag_comm_init(ctx);
+        if (st != LAG_OK) return fail(st);
+    }
+    // occupancy-sized persistent grid for the advect kernel
+    int occ = 1;
+    if (D == 3)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<3, true> : advect_kernel<3, false>, kThreads, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<2, true> : advect_kernel<2, false>, kThreads, 0);
+    ctx->advect_blocks_per_sm = occ > 0 ? occ : 1;
+    *out = ctx;
+    return LAG_OK;
+}
+
+extern "C" lag_status lag_destroy(lag_ctx ctx) {
+    if (!ctx) return LAG_OK;
+    cudaSetDevice(ctx->cfg.device);
+    if (ctx->stream_synced_needed) cudaStreamSynchronize(ctx->stream);
+    lag_comm_destroy(ctx);
+    dfree(ctx->state); dfree(ctx->tile_count); dfree(ctx->dead_rec); dfree(ctx->dead_info);
+    dfree(ctx->words); dfree(ctx->counters); dfree(ctx->out_start); dfree(ctx->out_end);
+    dfree(ctx->out_status); dfree(ctx->stage[0]); dfree(ctx->stage[1]);
+    delete ctx;
+    return LAG_OK;
+}
+
+// ---------------------------------------------------------------------------
+
+lag_status lag_reset_interval(lag_ctx_s* ctx) {
+    // device words: [W_DEAD] dead count, [W_ERR] error bits, [W_NTILES] tile count (COMM)
+    CK(cudaMemsetAsync(ctx->words, 0, kWords * sizeof(uint32_t), ctx->stream));
+    CK(cudaMemsetAsync(ctx->counters + CNT_TERM, 0, 4 * sizeof(unsigned long long), ctx->stream));
+    return LAG_OK;
+}
+
+extern "C" lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out) {
+    if (n_seeds_out) *n_seeds_out = 0;
+    if (!ctx) { lag_set_error(nullptr, "ctx is NULL"); return LAG_EINVAL; }
+    if (stride < 1) { lag_set_error(ctx, "stride must be >= 1 (got %d)", stride); return LAG_EINVAL; }
+    CK(cudaSetDevice(ctx->cfg.device));
+    const int D = ctx->cfg.dim;
+    int64_t n = 1;
+    for (int a = 0; a < 3; ++a) {
+        if (a < D) {
+            const int64_t lo = ctx->cfg.block_lo[a], hi = ctx->cfg.block_hi[a];
+            const int64_t first = ((lo + stride - 1) / stride) * stride;
+            const int64_t cnt = first < hi ? (hi - first + stride - 1) / stride : 0;
+            ctx->first[a] = (int)first;
+            ctx->ns[a] = (int)cnt;
+        } else {
+            ctx->first[a] = 0;
+            ctx->ns[a] = 1;
+        }
+        n *= ctx->ns[a];
+    }
+    if (n == 0) {
+        ctx->seeded = false;
+        lag_set_error(ctx, "no lattice node of stride %d in the block", stride);
+        return LAG_EEMPTY;
+    }
+    lag_status st = lag_reset_interval(ctx);
+    if (st != LAG_OK) return st;
+    ctx->stride = stride;
+    ctx->n_seeds = n;
+    ctx->n_tiles = (int)((n + kTile - 1) / kTile);
+    if (ctx->cfg.mode == LAG_COMM) {
+        // tail tiles past the seeds are empty; n_tiles lives on the device (appends)
+        CK(cudaMemsetAsync(ctx->tile_count, 0, (size_t)ctx->cap_tiles, ctx->stream));
+        st = lag_comm_reset(ctx);
+        if (st != LAG_OK) return st;
+    }
+    SeedArgs sa{};
+    sa.state = ctx->state; sa.tile_count = ctx->tile_count; sa.n = n; sa.stride = stride;
+    for (int a = 0; a < 3; ++a) { sa.first[a] = ctx->first[a]; sa.ns[a] = ctx->ns[a]; }
+    sa.bx = ctx->bits[0]; sa.by = ctx->bits[1];
+    const int64_t total = (int64_t)ctx->n_tiles * kTile;
+    seed_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(sa);
+    ++ctx->launches;
+    CK(cudaGetLastError());
+    ctx->seeded = true;
+    ctx->cycles_in_interval = 0;
+    ctx->active_host = n;
+    ctx->last_v1 = nullptr;
+    if (n_seeds_out) *n_seeds_out = n;
+    return LAG_OK;
+}
+
+// Device-resident velocity for a caller pointer: device memory is used in
+// place; host memory is copied into one of two staging buffers (end-to-end
+// path).  A host pointer already staged (the previous call's v_t1 passed as
+// this call's v_t) is reused: host slices must not change between those calls.
+static lag_status resolve_slice(lag_ctx_s* ctx, void* p, int avoid, float** out, int* slot_out) {
+    *slot_out = -1;
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) { cudaGetLastError(); at.type = cudaMemoryTypeUnregistered; }
+    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+        if (at.type == cudaMemoryTypeDevice && at.device != ctx->cfg.device) {
+            lag_set_error(ctx, "slice pointer lives on device %d, context on %d", at.device, ctx->cfg.device);
+            return LAG_EINVAL;
+        }
+        *out = (float*)p;
+        return LAG_OK;
+    }
+    for (int s = 0; s < 2; ++s)
+        if (ctx->stage[s] && ctx->stage_src[s] == p && s != avoid) {
+            *out = ctx->stage[s]; *slot_out = s;
+            return LAG_OK;
+        }
+    const int s = avoid == 0 ? 1 : 0;
+    if (!ctx->stage[s]) {
+        lag_status st = dmalloc(ctx, &ctx->stage[s], (size_t)ctx->slice_floats);
+        if (st != LAG_OK) return st;
+    }
+    CK(cudaMemcpyAsync(ctx->stage[s], p, (size_t)ctx->slice_floats * sizeof(float),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    ctx->stage_src[s] = p;
+    *out = ctx->stage[s]; *slot_out = s;
+    return LAG_OK;
+}
+
+extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, double dt) {
+    if (!ctx) { lag_set_error(nullptr, "ctx is NULL"); return LAG_EINVAL; }
+    if (!ctx->seeded) { lag_set_error(ctx, "lag_advect_cycle before lag_seed"); return LAG_ESTATE; }
+    if (!v_t || !v_t1) { lag_set_error(ctx, "velocity slice pointer is NULL"); return LAG_EINVAL; }
+    if (!(dt > 0.0) || !std::isfinite(dt)) { lag_set_error(ctx, "dt must be finite and > 0"); return LAG_EINVAL; }
+    CK(cudaSetDevice(ctx->cfg.device));
+    float* d0 = nullptr;
+    float* d1 = nullptr;
+    lag_status st;
+    int s0 = -1, s1 = -1;
+    if ((st = resolve_slice(ctx, v_t, -1, &d0, &s0)) != LAG_OK) return st;
+    if ((st = resolve_slice(ctx, v_t1, s0, &d1, &s1)) != LAG_OK) return st;
+    const int D = ctx->cfg.dim;
+    if (ctx->cfg.mode == LAG_COMM) {
+        st = lag_comm_pre_advect(ctx, d0, d1, v_t == ctx->last_v1);
+        if (st != LAG_OK) return st;
+    }
+    AdvectArgs a{};
+    a.v0 = d0; a.v1 = d1;
+    a.state = ctx->state; a.tile_count = ctx->tile_count;
+    a.n_tiles_dev = ctx->cfg.mode == LAG_COMM ? (const int32_t*)(ctx->words + W_NTILES) : nullptr;
+    a.n_tiles = ctx->n_tiles;
+    for (int ax = 0; ax < 3; ++ax) {
+        a.N[ax] = (int)ctx->cfg.global_nodes[ax];
+        a.lo[ax] = (int)ctx->cfg.block_lo[ax];
+        a.hi[ax] = (int)ctx->cfg.block_hi[ax];
+        a.base[ax] = ctx->base[ax];
+        a.cmax[ax] = ctx->ext[ax] - 2;
+        const double dth = ax < D ? dt / ctx->cfg.spacing[ax] : 0.0;
+        a.hdth[ax] = (float)(0.5 * dth);
+        a.qdth[ax] = (float)(0.25 * dth);
+        a.sdth[ax] = (float)(dth / 6.0);
+    }
+    a.sx = ctx->ext[0];
+    a.sxy = ctx->ext[0] * ctx->ext[1];
+    a.bx = ctx->bits[0]; a.by = ctx->bits[1];
+    a.mx = (1u << ctx->bits[0]) - 1u; a.my = (1u << ctx->bits[1]) - 1u;
+    a.dead_rec = ctx->dead_rec; a.dead_info = ctx->dead_info;
+    a.dead_count = ctx->words + W_DEAD; a.dead_cap = (uint32_t)ctx->cap;
+    a.counters = ctx->counters; a.err = ctx->words + W_ERR;
+    a.cycle = ctx->cycles_in_interval;
+    if (ctx->cfg.mode == LAG_COMM) lag_comm_fill_args(ctx, &a);
+
+    const int tiles = ctx->cfg.mode == LAG_COMM ? ctx->cap_tiles : ctx->n_tiles;
+    const int warps_per_block = kThreads / 32;
+    int blocks = (tiles + warps_per_block - 1) / warps_per_block;
+    const int max_blocks = ctx->num_sms * ctx->advect_blocks_per_sm;
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (blocks < 1) blocks = 1;
+    if (D == 3) {
+        if (ctx->cfg.mode == LAG_BTO) advect_kernel<3, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
+        else advect_kernel<3, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
+    } else {
+        if (ctx->cfg.mode == LAG_BTO) advect_kernel<2, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
+        else advect_kernel<2, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
+    }
+    ++ctx->launches;
+    CK(cudaGetLastError());
+    if (ctx->cfg.mode == LAG_COMM) {
+        st = lag_comm_post_advect(ctx);
+        if (st != LAG_OK) return st;
+    }
+    ctx->last_v1 = v_t1;
+    ++ctx->cycles_in_interval;
+    ++ctx->cycles_total;
+    return LAG_OK;
+}
+
+static lag_status latched(lag_ctx_s* ctx, uint32_t err) {
+    if (err & ERR_OVERFLOW) { lag_set_error(ctx, "latched: exchange slot or particle list overflow"); return LAG_EOVERFLOW; }
+    if (err & ERR_GHOST) { lag_set_error(ctx, "latched: a stage sample left the ghost layers (CFL >= 1?)"); return LAG_EGHOST; }
+    if (err & ERR_NONFINITE) { lag_set_error(ctx, "latched: non-finite velocity reached a particle"); return LAG_ENONFINITE; }
+    return LAG_OK;
+}
+
+static lag_status copy_out(lag_ctx_s* ctx, void* dst, const void* src, size_t bytes) {
+    if (!dst || bytes == 0) return LAG_OK;
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+    return LAG_OK;
+}
+
+extern "C" lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8_t* status,
+                                  int64_t capacity, int64_t* n_out, uint32_t flags) {
+    if (n_out) *n_out = 0;
+    if (!ctx) { lag_set_error(nullptr, "ctx is NULL"); return LAG_EINVAL; }
+    if (!ctx->seeded) { lag_set_error(ctx, "lag_extract before lag_seed"); return LAG_ESTATE; }
+    if (capacity < ctx->n_seeds && (start || end || status)) {
+        lag_set_error(ctx, "capacity %lld < %lld seeds", (long long)capacity, (long long)ctx->n_seeds);
+        return LAG_EINVAL;
+    }
+    CK(cudaSetDevice(ctx->cfg.device));
+    lag_status st;
+    if (ctx->cfg.mode == LAG_COMM) {
+        st = lag_comm_return_to_origin(ctx);      // collective; leaves only own-origin records
+        if (st != LAG_OK) return st;
+    }
+    const int D = ctx->cfg.dim;
+    uint32_t n_dead = 0;
+    CK(cudaMemcpyAsync(&ctx->host_words[0], ctx->words, kWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    n_dead = ctx->host_words[W_DEAD];
+    if (n_dead > (uint32_t)ctx->cap) n_dead = (uint32_t)ctx->cap;
+    const int n_tiles = ctx->cfg.mode == LAG_COMM ? (int)ctx->host_words[W_NTILES] : ctx->n_tiles;
+
+    ExtractArgs e{};
+    e.state = ctx->state; e.tile_count = ctx->tile_count; e.n_tiles = n_tiles;
+    e.dead_rec = ctx->dead_rec; e.dead_info = ctx->dead_info; e.n_dead = n_dead;
+    e.n = ctx->n_seeds; e.dim = D; e.stride = ctx->stride;
+    for (int a = 0; a < 3; ++a) {
+        e.first[a] = ctx->first[a]; e.ns[a] = ctx->ns[a];
+        e.o[a] = ctx->cfg.origin[a]; e.h[a] = ctx->cfg.spacing[a];
+    }
+    e.bx = ctx->bits[0]; e.by = ctx->bits[1];
+    e.mx = (1u << ctx->bits[0]) - 1u; e.my = (1u << ctx->bits[1]) - 1u;
+    for (int a = 0; a < 3; ++a) { e.lo[a] = (int)ctx->cfg.block_lo[a]; e.hi[a] = (int)ctx->cfg.block_hi[a]; }
+    e.ret = nullptr; e.n_ret = 0;
+    if (ctx->cfg.mode == LAG_COMM) {
+        int64_t stride_f4 = 2;
+        lag_comm_returned(ctx, &e.ret, &stride_f4, &e.n_ret);
+    }
+    e.start = ctx->out_start; e.end = ctx->out_end; e.status = ctx->out_status;
+    const unsigned nb_seed = (unsigned)((ctx->n_seeds + 255) / 256);
+    extract_start_kernel<<<nb_seed, 256, 0, ctx->stream>>>(e);
+    ++ctx->launches;
+    if (n_tiles > 0) {
+        extract_live_kernel<<<(unsigned)(((int64_t)n_tiles * kTile + 255) / 256), 256, 0, ctx->stream>>>(e);
+        ++ctx->launches;
+    }
+    if (n_dead > 0) {
+        extract_dead_kernel<<<(n_dead + 255) / 256, 256, 0, ctx->stream>>>(e);
+        ++ctx->launches;
+    }
+    if (e.n_ret > 0) {
+        extract_returned_kernel<<<(e.n_ret + 255) / 256, 256, 0, ctx->stream>>>(e);
+        ++ctx->launches;
+    }
+    CK(cudaGetLastError());
+    const size_t n = (size_t)ctx->n_seeds;
+    if ((st = copy_out(ctx, start, ctx->out_start, n * D * sizeof(double))) != LAG_OK) return st;
+    if ((st = copy_out(ctx, end, ctx->out_end, n * D * sizeof(double))) != LAG_OK) return st;
+    if ((st = copy_out(ctx, status, ctx->out_status, n)) != LAG_OK) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (n_out) *n_out = ctx->n_seeds;
+    const lag_status err = latched(ctx, ctx->host_words[W_ERR]);
+    if (!(flags & LAG_NO_RESEED)) {
+        st = lag_seed(ctx, ctx->stride, nullptr);
+        if (st != LAG_OK) return st;
+    } else {
+        ctx->seeded = true;   // outputs stay valid; advect continues the interval
+    }
+    return err;
+}
+
+extern "C" lag_status lag_stats(lag_ctx ctx, lag_stats_t* out) {
+    if (!ctx || !out) { lag_set_error(ctx, "NULL argument"); return LAG_EINVAL; }
+    CK(cudaSetDevice(ctx->cfg.device));
+    unsigned long long c[CNT_N];
+    CK(cudaMemcpyAsync(c, ctx->counters, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&ctx->host_words[0], ctx->words, kWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::memset(out, 0, sizeof(*out));
+    out->seeded = ctx->seeded ? ctx->n_seeds : 0;
+    out->term_boundary = (int64_t)c[CNT_TERM];
+    out->exit_domain = (int64_t)c[CNT_EXIT];
+    out->sent = (int64_t)c[CNT_SENT];
+    out->received = (int64_t)c[CNT_RECV];
+    out->particle_steps = (int64_t)c[CNT_STEPS];
+    out->cycles = ctx->cycles_total;
+    out->active = out->seeded + out->received - out->sent - out->term_boundary - out->exit_domain;
+    out->device_error = (int32_t)latched(ctx, ctx->host_words[W_ERR]);
+    return LAG_OK;
+}

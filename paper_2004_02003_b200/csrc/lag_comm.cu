@@ -1,0 +1,636 @@
+// lag_comm.cu — COMM mode: the paper's communicating baseline (Lagrangian-MPI
+// after Agranovsky et al., §2.3, §3.1) on NCCL over NVLink.
+//
+// Per lag_advect_cycle (one NCCL group per cycle, no host synchronisation):
+//   1. halo_pack    : the parts of my slice interior my neighbours need as
+//                     ghost layers (faces, edges, corners: all 3^d - 1 offsets
+//                     go direct — NVSwitch gives every peer full bandwidth)
+//   2. NCCL group   : halo boxes + the particle slots filled by the previous
+//                     cycle's advect (messages sent in cycle c are advanced by
+//                     the receiver from cycle c+1 on)
+//   3. halo_unpack  : write the received ghost layers of v_t1 (and v_t)
+//   4. append       : received particles -> new tiles at the end of the list
+//   5. advect       : (lag_api.cu) writes leaving particles to per-offset slots
+// Slots are fixed-capacity [header | cap records] so NCCL sizes are known on
+// the host; overflow is latched as LAG_EOVERFLOW.
+// lag_extract first flushes pending particles, then returns every particle
+// to its origin rank ("each compute node returns its particles to
+// their originating nodes"; untimed write cycle).
+#include "lag_internal.h"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+using namespace lag;
+
+#define CKC(call)                                                                  \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess) {                                                   \
+            lag_set_error(ctx, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                          __FILE__, __LINE__);                                     \
+            return LAG_ECUDA;                                                      \
+        }                                                                          \
+    } while (0)
+#define CKN(call)                                                                  \
+    do {                                                                           \
+        ncclResult_t r_ = (call);                                                  \
+        if (r_ != ncclSuccess) {                                                   \
+            lag_set_error(ctx, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_),    \
+                          __FILE__, __LINE__);                                     \
+            return LAG_ENCCL;                                                      \
+        }                                                                          \
+    } while (0)
+
+namespace lag {
+
+constexpr int kMaxOff = 27;
+constexpr int kMaxCuts = 65;
+
+struct Box {            // local slice coordinates
+    int x0, y0, z0, nx, ny, nz;
+    int64_t off;        // float offset in the pack buffer
+    int slice;          // 0 = v_t, 1 = v_t1
+};
+
+struct RouteRec {       // return-to-origin record (32 B)
+    float4 rec;
+    uint32_t info;      // (status << 24) | cycle ; 0 = valid
+    uint32_t pad[3];
+};
+
+struct Peer {
+    int rank;
+    int off;                    // neighbour offset index (0..3^d-1)
+    int back;                   // the offset index of me as seen from the peer
+    int send_box, recv_box;     // indices into the box tables
+    int64_t halo_floats_send, halo_floats_recv;
+    uint32_t cap_send, cap_recv;   // particle slot capacities (records)
+    float4* recv_slot;             // [1 + cap_recv]
+};
+
+struct Comm {
+    ncclComm_t nccl = nullptr;
+    int me[3] = {0, 0, 0};
+    std::vector<int64_t> blocks;        // nranks * 6 (lo[3], hi[3])
+    std::vector<Peer> peers;
+    std::vector<Box> send_boxes, recv_boxes;    // per peer, one slice
+    Box* d_send_boxes = nullptr;                // [2 * npeers]: v1 boxes then v0 boxes
+    Box* d_recv_boxes = nullptr;
+    float* halo_send = nullptr;                 // 2 slices worth
+    float* halo_recv = nullptr;
+    int64_t halo_send_floats = 0, halo_recv_floats = 0;   // one slice
+    // outgoing particle slots: per offset [header | cap]
+    float4* slots = nullptr;
+    int32_t slot_base[kMaxOff] = {0};
+    int32_t slot_capv[kMaxOff] = {0};
+    int64_t slot_total = 0;
+    float4* recv_slots = nullptr;
+    int64_t recv_total = 0;
+    bool pending = false;
+    // routing
+    int32_t cuts[3][kMaxCuts] = {{0}};
+    int ncuts[3] = {0, 0, 0};
+    int32_t* d_cuts = nullptr;
+    uint32_t* d_route_count = nullptr;  // [nranks]
+    RouteRec* route = nullptr;          // [cap]
+    RouteRec* route_recv = nullptr;     // [cap]
+    uint32_t* d_route_pos = nullptr;
+    int64_t route_cap = 0;
+    uint32_t n_returned = 0;
+};
+
+// ---------------------------------------------------------------------------
+// kernels
+
+struct BoxArgs {
+    const float* v0;
+    float* v1;           // v_t1 (written by unpack)
+    float* v0w;          // v_t  (written by unpack when its ghosts are stale)
+    const Box* boxes;
+    int nbox;
+    float* buf;
+    int sx, sxy, dim;
+    int64_t total;       // floats over all boxes
+};
+
+__device__ __forceinline__ int find_box(const Box* b, int nbox, int64_t i) {
+    int k = 0;
+    while (k + 1 < nbox && b[k + 1].off <= i) ++k;
+    return k;
+}
+
+__global__ void halo_pack_kernel(BoxArgs a) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = find_box(a.boxes, a.nbox, i);
+        const Box b = a.boxes[k];
+        const int64_t j = i - b.off;
+        const int comp = (int)(j % a.dim);
+        const int64_t node = j / a.dim;
+        const int x = (int)(node % b.nx), y = (int)((node / b.nx) % b.ny), z = (int)(node / ((int64_t)b.nx * b.ny));
+        const float* src = b.slice ? a.v1 : a.v0;
+        a.buf[i] = src[(int64_t)a.dim * ((b.x0 + x) + (int64_t)a.sx * (b.y0 + y) + (int64_t)a.sxy * (b.z0 + z)) + comp];
+    }
+}
+
+__global__ void halo_unpack_kernel(BoxArgs a) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = find_box(a.boxes, a.nbox, i);
+        const Box b = a.boxes[k];
+        const int64_t j = i - b.off;
+        const int comp = (int)(j % a.dim);
+        const int64_t node = j / a.dim;
+        const int x = (int)(node % b.nx), y = (int)((node / b.nx) % b.ny), z = (int)(node / ((int64_t)b.nx * b.ny));
+        float* dst = b.slice ? a.v1 : a.v0w;
+        dst[(int64_t)a.dim * ((b.x0 + x) + (int64_t)a.sx * (b.y0 + y) + (int64_t)a.sxy * (b.z0 + z)) + comp] = a.buf[i];
+    }
+}
+
+struct AppendArgs {
+    float4* state;
+    uint8_t* tile_count;
+    uint32_t* words;
+    unsigned long long* counters;
+    int cap_tiles;
+    int npeers;
+    const float4* recv[kMaxOff];
+    uint32_t cap[kMaxOff];
+    float4* slots;                  // outgoing slots: headers reset here
+    int32_t slot_base[kMaxOff];
+    int noff;
+};
+
+// single block: received particles become new tiles at the end of the list
+__global__ void __launch_bounds__(1024) append_kernel(AppendArgs a) {
+    __shared__ uint32_t pre[kMaxOff + 1];
+    __shared__ uint32_t old_tiles;
+    if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int p = 0; p < a.npeers; ++p) {
+            pre[p] = s;
+            uint32_t c = *reinterpret_cast<const uint32_t*>(a.recv[p]);
+            if (c > a.cap[p]) { c = a.cap[p]; atomicOr(a.words + W_ERR, ERR_OVERFLOW); }
+            s += c;
+        }
+        pre[a.npeers] = s;
+        old_tiles = a.words[W_NTILES];
+    }
+    __syncthreads();
+    uint32_t total = pre[a.npeers];
+    const uint32_t room = (uint32_t)(a.cap_tiles - (int)old_tiles) * kTile;
+    if (total > room) {
+        if (threadIdx.x == 0) atomicOr(a.words + W_ERR, ERR_OVERFLOW);
+        total = room;
+    }
+    for (uint32_t j = threadIdx.x; j < total; j += blockDim.x) {
+        int p = 0;
+        while (p + 1 < a.npeers && pre[p + 1] <= j) ++p;
+        a.state[(size_t)old_tiles * kTile + j] = a.recv[p][1 + (j - pre[p])];
+    }
+    const uint32_t new_tiles = (total + kTile - 1) / kTile;
+    for (uint32_t t = threadIdx.x; t < new_tiles; t += blockDim.x) {
+        const uint32_t rem = total - t * kTile;
+        a.tile_count[old_tiles + t] = (uint8_t)(rem >= (uint32_t)kTile ? kTile : rem);
+    }
+    if (threadIdx.x < (unsigned)a.noff)
+        *reinterpret_cast<uint32_t*>(a.slots + a.slot_base[threadIdx.x]) = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a.words[W_NTILES] = old_tiles + new_tiles;
+        if (total) atomicAdd(&a.counters[CNT_RECV], (unsigned long long)total);
+    }
+}
+
+struct RouteArgs {
+    const float4* state;
+    const uint8_t* tile_count;
+    const uint32_t* words;
+    const float4* dead_rec;
+    const uint32_t* dead_info;
+    uint32_t dead_cap;
+    const int32_t* cuts;        // [3][kMaxCuts]
+    int ncuts0, ncuts1, ncuts2;
+    int lay0, lay1;
+    uint32_t bx, by, mx, my;
+    int me;
+    uint32_t* count;            // [nranks]
+    uint32_t* pos;              // [nranks] running positions (pass 2)
+    const uint32_t* seg;        // [nranks] segment starts (pass 2)
+    RouteRec* out;
+    int pass;
+};
+
+__device__ __forceinline__ int origin_rank(const RouteArgs& a, uint32_t w) {
+    const int g[3] = {(int)(w & a.mx), (int)((w >> a.bx) & a.my), (int)(w >> (a.bx + a.by))};
+    const int nc[3] = {a.ncuts0, a.ncuts1, a.ncuts2};
+    int c[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        int k = 0;
+        while (k + 1 < nc[ax] - 1 && a.cuts[ax * kMaxCuts + k + 1] <= g[ax]) ++k;
+        c[ax] = k;
+    }
+    return c[0] + a.lay0 * (c[1] + a.lay1 * c[2]);
+}
+
+__global__ void route_kernel(RouteArgs a) {
+    const int64_t n_live = (int64_t)a.words[W_NTILES] * kTile;
+    uint32_t n_dead = a.words[W_DEAD];
+    if (n_dead > a.dead_cap) n_dead = a.dead_cap;
+    const int64_t total = n_live + n_dead;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float4 r;
+        uint32_t info;
+        if (i < n_live) {
+            if ((int)(i % kTile) >= a.tile_count[i / kTile]) continue;
+            r = a.state[i];
+            info = 0u;
+        } else {
+            r = a.dead_rec[i - n_live];
+            info = a.dead_info[i - n_live];
+        }
+        const int o = origin_rank(a, __float_as_uint(r.w));
+        if (o == a.me) continue;
+        if (a.pass == 0) {
+            atomicAdd(&a.count[o], 1u);
+        } else {
+            const uint32_t p = a.seg[o] + atomicAdd(&a.pos[o], 1u);
+            RouteRec rr;
+            rr.rec = r; rr.info = info; rr.pad[0] = rr.pad[1] = rr.pad[2] = 0;
+            a.out[p] = rr;
+        }
+    }
+}
+
+}  // namespace lag
+
+// ---------------------------------------------------------------------------
+// host side
+
+static int off_index(const int o[3]) { return (o[0] + 1) + 3 * ((o[1] + 1) + 3 * (o[2] + 1)); }
+
+lag_status lag_comm_init(lag_ctx_s* ctx) {
+    const lag_config& c = ctx->cfg;
+    Comm* cm = new Comm();
+    ctx->comm = cm;
+    const int D = c.dim;
+    const int G = c.ghost;
+    cm->me[0] = c.rank % c.layout[0];
+    cm->me[1] = (c.rank / c.layout[0]) % c.layout[1];
+    cm->me[2] = c.rank / (c.layout[0] * c.layout[1]);
+    cm->blocks.assign((size_t)c.nranks * 6, 0);
+    int64_t mine[6] = {c.block_lo[0], c.block_lo[1], c.block_lo[2], c.block_hi[0], c.block_hi[1], c.block_hi[2]};
+    if (c.nranks > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, c.nccl_id, sizeof(id));
+        CKN(ncclCommInitRank(&cm->nccl, c.nranks, id, c.rank));
+        int64_t* d = nullptr;
+        CKC(cudaMalloc(&d, sizeof(int64_t) * 6 * (c.nranks + 1)));
+        CKC(cudaMemcpyAsync(d, mine, sizeof(mine), cudaMemcpyHostToDevice, ctx->stream));
+        CKN(ncclAllGather(d, d + 6, 6, ncclInt64, cm->nccl, ctx->stream));
+        CKC(cudaMemcpyAsync(cm->blocks.data(), d + 6, sizeof(int64_t) * 6 * c.nranks, cudaMemcpyDeviceToHost, ctx->stream));
+        CKC(cudaStreamSynchronize(ctx->stream));
+        cudaFree(d);
+    } else {
+        std::copy(mine, mine + 6, cm->blocks.begin());
+    }
+    // per-axis cut points (block lo values along each axis, plus N)
+    for (int ax = 0; ax < 3; ++ax) {
+        std::vector<int32_t> v;
+        for (int r = 0; r < c.nranks; ++r) v.push_back((int32_t)cm->blocks[(size_t)r * 6 + ax]);
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        if ((int)v.size() != c.layout[ax] || (int)v.size() + 1 > kMaxCuts) {
+            lag_set_error(ctx, "blocks do not form the declared layout on axis %d", ax);
+            return LAG_EINVAL;
+        }
+        v.push_back((int32_t)c.global_nodes[ax]);
+        cm->ncuts[ax] = (int)v.size();
+        for (size_t k = 0; k < v.size(); ++k) cm->cuts[ax][k] = v[k];
+    }
+    // neighbours, halo boxes, slot capacities
+    auto top = [&](const int64_t* b, int ax) { return std::min(b[3 + ax] + 1, c.global_nodes[ax]); };
+    const int64_t* my = mine;
+    int64_t send_off = 0, recv_off = 0, slot_off = 0;
+    for (int oz = (D == 3 ? -1 : 0); oz <= (D == 3 ? 1 : 0); ++oz)
+        for (int oy = -1; oy <= 1; ++oy)
+            for (int ox = -1; ox <= 1; ++ox) {
+                const int o[3] = {ox, oy, oz};
+                const int k = off_index(o);
+                // particle slot capacity by neighbour kind: faces get a full face of nodes
+                int64_t cap = 64;
+                {
+                    int nz = 0;
+                    int64_t area = 1;
+                    for (int ax = 0; ax < D; ++ax) {
+                        if (o[ax] == 0) area *= (my[3 + ax] - my[ax]);
+                        else ++nz;
+                    }
+                    if (ox == 0 && oy == 0 && oz == 0) cap = 0;
+                    else if (nz == 1) cap = area + 1024;
+                    else if (nz == 2 && D == 3) cap = area + 256;
+                    else cap = 64 + (D == 2 ? area : 0);
+                }
+                cm->slot_base[k] = (int32_t)slot_off;
+                cm->slot_capv[k] = (int32_t)cap;
+                slot_off += cap + 1;
+                if (ox == 0 && oy == 0 && oz == 0) continue;
+                int nbc[3];
+                bool ok = true;
+                for (int ax = 0; ax < 3; ++ax) {
+                    nbc[ax] = cm->me[ax] + o[ax];
+                    if (nbc[ax] < 0 || nbc[ax] >= c.layout[ax]) ok = false;
+                }
+                if (!ok) continue;
+                const int nr = nbc[0] + c.layout[0] * (nbc[1] + c.layout[1] * nbc[2]);
+                const int64_t* nb = &cm->blocks[(size_t)nr * 6];
+                Box rb{}, sb{};
+                int64_t rlo[3], rn[3], slo[3], sn[3];
+                for (int ax = 0; ax < 3; ++ax) {
+                    if (ax >= D) { rlo[ax] = 0; rn[ax] = 1; slo[ax] = 0; sn[ax] = 1; continue; }
+                    // my ghost region filled by this neighbour
+                    if (o[ax] < 0) { rlo[ax] = my[ax] - G; rn[ax] = G; }
+                    else if (o[ax] == 0) { rlo[ax] = my[ax]; rn[ax] = top(my, ax) - my[ax]; }
+                    else { rlo[ax] = top(my, ax); rn[ax] = G; }
+                    // the neighbour's ghost region (offset -o) that I fill
+                    if (-o[ax] < 0) { slo[ax] = nb[ax] - G; sn[ax] = G; }
+                    else if (o[ax] == 0) { slo[ax] = nb[ax]; sn[ax] = top(nb, ax) - nb[ax]; }
+                    else { slo[ax] = top(nb, ax); sn[ax] = G; }
+                    if (slo[ax] < my[ax] || slo[ax] + sn[ax] > top(my, ax)) {
+                        lag_set_error(ctx, "block too thin for %d ghost layers on axis %d", G, ax);
+                        return LAG_EINVAL;
+                    }
+                }
+                auto local = [&](const int64_t* lo3, const int64_t* n3, int64_t off) {
+                    Box b{};
+                    b.x0 = (int)(lo3[0] - ctx->base[0]); b.y0 = (int)(lo3[1] - ctx->base[1]); b.z0 = (int)(lo3[2] - ctx->base[2]);
+                    b.nx = (int)n3[0]; b.ny = (int)n3[1]; b.nz = (int)n3[2];
+                    b.off = off; b.slice = 1;
+                    return b;
+                };
+                sb = local(slo, sn, send_off);
+                rb = local(rlo, rn, recv_off);
+                Peer p{};
+                p.rank = nr;
+                p.off = k;
+                const int ob[3] = {-o[0], -o[1], -o[2]};
+                p.back = off_index(ob);
+                p.send_box = (int)cm->send_boxes.size();
+                p.recv_box = (int)cm->recv_boxes.size();
+                p.halo_floats_send = sn[0] * sn[1] * sn[2] * D;
+                p.halo_floats_recv = rn[0] * rn[1] * rn[2] * D;
+                send_off += p.halo_floats_send;
+                recv_off += p.halo_floats_recv;
+                cm->send_boxes.push_back(sb);
+                cm->recv_boxes.push_back(rb);
+                cm->peers.push_back(p);
+            }
+    cm->halo_send_floats = send_off;
+    cm->halo_recv_floats = recv_off;
+    cm->slot_total = slot_off;
+    // the receive capacity from a peer = the peer's send capacity toward me:
+    // the same formula evaluated with the peer's block
+    for (Peer& p : cm->peers) {
+        const int64_t* nb = &cm->blocks[(size_t)p.rank * 6];
+        int o[3] = {0, 0, 0};
+        {
+            int k = p.back;
+            o[0] = k % 3 - 1; o[1] = (k / 3) % 3 - 1; o[2] = k / 9 - 1;
+        }
+        int nz = 0;
+        int64_t area = 1;
+        for (int ax = 0; ax < D; ++ax) {
+            if (o[ax] == 0) area *= (nb[3 + ax] - nb[ax]);
+            else ++nz;
+        }
+        int64_t cap = nz == 1 ? area + 1024 : ((nz == 2 && D == 3) ? area + 256 : 64 + (D == 2 ? area : 0));
+        p.cap_send = (uint32_t)cm->slot_capv[p.off];
+        p.cap_recv = (uint32_t)cap;
+        cm->recv_total += cap + 1;
+    }
+    // device buffers
+    const size_t np = cm->peers.size();
+    std::vector<Box> sb2(cm->send_boxes), rb2(cm->recv_boxes);
+    for (size_t i = 0; i < np; ++i) {   // v0 copies of the boxes follow the v1 ones
+        Box b = cm->send_boxes[i]; b.slice = 0; b.off += send_off; sb2.push_back(b);
+        Box r = cm->recv_boxes[i]; r.slice = 0; r.off += recv_off; rb2.push_back(r);
+    }
+    CKC(cudaMalloc(&cm->d_send_boxes, sizeof(Box) * std::max<size_t>(1, sb2.size())));
+    CKC(cudaMalloc(&cm->d_recv_boxes, sizeof(Box) * std::max<size_t>(1, rb2.size())));
+    if (!sb2.empty()) {
+        CKC(cudaMemcpy(cm->d_send_boxes, sb2.data(), sizeof(Box) * sb2.size(), cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(cm->d_recv_boxes, rb2.data(), sizeof(Box) * rb2.size(), cudaMemcpyHostToDevice));
+    }
+    CKC(cudaMalloc(&cm->halo_send, sizeof(float) * std::max<int64_t>(1, 2 * send_off)));
+    CKC(cudaMalloc(&cm->halo_recv, sizeof(float) * std::max<int64_t>(1, 2 * recv_off)));
+    CKC(cudaMalloc(&cm->slots, sizeof(float4) * std::max<int64_t>(1, cm->slot_total)));
+    CKC(cudaMemset(cm->slots, 0, sizeof(float4) * std::max<int64_t>(1, cm->slot_total)));
+    CKC(cudaMalloc(&cm->recv_slots, sizeof(float4) * std::max<int64_t>(1, cm->recv_total)));
+    {
+        int64_t off = 0;
+        for (Peer& p : cm->peers) { p.recv_slot = cm->recv_slots + off; off += p.cap_recv + 1; }
+    }
+    CKC(cudaMalloc(&cm->d_cuts, sizeof(int32_t) * 3 * kMaxCuts));
+    CKC(cudaMemcpy(cm->d_cuts, cm->cuts, sizeof(int32_t) * 3 * kMaxCuts, cudaMemcpyHostToDevice));
+    CKC(cudaMalloc(&cm->d_route_count, sizeof(uint32_t) * 2 * std::max(1, c.nranks)));
+    cm->d_route_pos = cm->d_route_count + c.nranks;
+    cm->route_cap = ctx->cap;
+    CKC(cudaMalloc(&cm->route, sizeof(RouteRec) * std::max<int64_t>(1, cm->route_cap)));
+    CKC(cudaMalloc(&cm->route_recv, sizeof(RouteRec) * std::max<int64_t>(1, cm->route_cap)));
+    return LAG_OK;
+}
+
+void lag_comm_destroy(lag_ctx_s* ctx) {
+    Comm* cm = ctx->comm;
+    if (!cm) return;
+    if (cm->nccl) ncclCommDestroy(cm->nccl);
+    cudaFree(cm->d_send_boxes); cudaFree(cm->d_recv_boxes);
+    cudaFree(cm->halo_send); cudaFree(cm->halo_recv);
+    cudaFree(cm->slots); cudaFree(cm->recv_slots); cudaFree(cm->d_cuts);
+    cudaFree(cm->d_route_count); cudaFree(cm->route); cudaFree(cm->route_recv);
+    delete cm;
+    ctx->comm = nullptr;
+}
+
+lag_status lag_comm_reset(lag_ctx_s* ctx) {
+    Comm* cm = ctx->comm;
+    // W_NTILES = seed tiles; empty outgoing slots; nothing pending
+    const uint32_t nt = (uint32_t)ctx->n_tiles;
+    CKC(cudaMemcpyAsync(ctx->words + W_NTILES, &nt, sizeof(nt), cudaMemcpyHostToDevice, ctx->stream));
+    CKC(cudaStreamSynchronize(ctx->stream));   // nt is a host stack variable
+    CKC(cudaMemsetAsync(cm->slots, 0, sizeof(float4) * std::max<int64_t>(1, cm->slot_total), ctx->stream));
+    cm->pending = false;
+    cm->n_returned = 0;
+    return LAG_OK;
+}
+
+static lag_status launch_append(lag_ctx_s* ctx) {
+    Comm* cm = ctx->comm;
+    AppendArgs a{};
+    a.state = ctx->state; a.tile_count = ctx->tile_count; a.words = ctx->words;
+    a.counters = ctx->counters; a.cap_tiles = ctx->cap_tiles;
+    a.npeers = (int)cm->peers.size();
+    for (size_t i = 0; i < cm->peers.size(); ++i) { a.recv[i] = cm->peers[i].recv_slot; a.cap[i] = cm->peers[i].cap_recv; }
+    a.slots = cm->slots;
+    a.noff = ctx->cfg.dim == 3 ? 27 : 9;
+    for (int k = 0; k < kMaxOff; ++k) a.slot_base[k] = cm->slot_base[k];
+    append_kernel<<<1, 1024, 0, ctx->stream>>>(a);
+    ++ctx->launches;
+    CKC(cudaGetLastError());
+    return LAG_OK;
+}
+
+// One NCCL group: optional halo boxes (v1 [+ v0]) and the pending particle slots.
+static lag_status exchange(lag_ctx_s* ctx, float* v0, float* v1, bool halo, bool halo_v0) {
+    Comm* cm = ctx->comm;
+    const int D = ctx->cfg.dim;
+    const size_t np = cm->peers.size();
+    if (np == 0) return LAG_OK;
+    const int nbox = halo ? (int)(halo_v0 ? 2 * np : np) : 0;
+    const int64_t sfl = halo ? (halo_v0 ? 2 : 1) * cm->halo_send_floats : 0;
+    const int64_t rfl = halo ? (halo_v0 ? 2 : 1) * cm->halo_recv_floats : 0;
+    if (halo && sfl > 0) {
+        BoxArgs b{};
+        b.v0 = v0; b.v1 = v1; b.v0w = v0; b.boxes = cm->d_send_boxes; b.nbox = nbox;
+        b.buf = cm->halo_send; b.sx = ctx->ext[0]; b.sxy = ctx->ext[0] * ctx->ext[1]; b.dim = D; b.total = sfl;
+        const int blocks = (int)std::min<int64_t>((sfl + 255) / 256, (int64_t)ctx->num_sms * 8);
+        halo_pack_kernel<<<blocks, 256, 0, ctx->stream>>>(b);
+        ++ctx->launches;
+        CKC(cudaGetLastError());
+    }
+    CKN(ncclGroupStart());
+    for (const Peer& p : cm->peers) {
+        if (halo) {
+            const Box& s = cm->send_boxes[(size_t)p.send_box];
+            const Box& r = cm->recv_boxes[(size_t)p.recv_box];
+            CKN(ncclSend(cm->halo_send + s.off, p.halo_floats_send, ncclFloat32, p.rank, cm->nccl, ctx->stream));
+            CKN(ncclRecv(cm->halo_recv + r.off, p.halo_floats_recv, ncclFloat32, p.rank, cm->nccl, ctx->stream));
+            if (halo_v0) {
+                CKN(ncclSend(cm->halo_send + cm->halo_send_floats + s.off, p.halo_floats_send, ncclFloat32, p.rank, cm->nccl, ctx->stream));
+                CKN(ncclRecv(cm->halo_recv + cm->halo_recv_floats + r.off, p.halo_floats_recv, ncclFloat32, p.rank, cm->nccl, ctx->stream));
+            }
+        }
+        // particle slot toward this peer: header + cap records (float4 = 4 floats)
+        CKN(ncclSend(cm->slots + cm->slot_base[p.off], (size_t)(p.cap_send + 1) * 4, ncclFloat32, p.rank, cm->nccl, ctx->stream));
+        CKN(ncclRecv(p.recv_slot, (size_t)(p.cap_recv + 1) * 4, ncclFloat32, p.rank, cm->nccl, ctx->stream));
+    }
+    CKN(ncclGroupEnd());
+    if (halo && rfl > 0) {
+        BoxArgs b{};
+        b.v0 = v0; b.v1 = v1; b.v0w = v0; b.boxes = cm->d_recv_boxes; b.nbox = nbox;
+        b.buf = cm->halo_recv; b.sx = ctx->ext[0]; b.sxy = ctx->ext[0] * ctx->ext[1]; b.dim = D; b.total = rfl;
+        const int blocks = (int)std::min<int64_t>((rfl + 255) / 256, (int64_t)ctx->num_sms * 8);
+        halo_unpack_kernel<<<blocks, 256, 0, ctx->stream>>>(b);
+        ++ctx->launches;
+        CKC(cudaGetLastError());
+    }
+    return launch_append(ctx);
+}
+
+lag_status lag_comm_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool v0_is_prev_v1) {
+    Comm* cm = ctx->comm;
+    if (cm->peers.empty()) return LAG_OK;
+    lag_status st = exchange(ctx, v0, v1, true, !v0_is_prev_v1);
+    cm->pending = false;
+    return st;
+}
+
+void lag_comm_fill_args(lag_ctx_s* ctx, AdvectArgs* a) {
+    Comm* cm = ctx->comm;
+    a->slot_rec = cm->slots;
+    for (int k = 0; k < kMaxOff; ++k) { a->slot_base[k] = cm->slot_base[k]; a->slot_capv[k] = cm->slot_capv[k]; }
+}
+
+lag_status lag_comm_post_advect(lag_ctx_s* ctx) {
+    ctx->comm->pending = !ctx->comm->peers.empty();
+    return LAG_OK;
+}
+
+// Write cycle: flush pending hand-offs, then route every record whose seed
+// belongs to another rank back to it (exact sizes; untimed, host syncs allowed).
+lag_status lag_comm_return_to_origin(lag_ctx_s* ctx) {
+    Comm* cm = ctx->comm;
+    const lag_config& c = ctx->cfg;
+    cm->n_returned = 0;
+    if (c.nranks == 1) return LAG_OK;
+    if (cm->pending) {
+        lag_status st = exchange(ctx, nullptr, nullptr, false, false);
+        if (st != LAG_OK) return st;
+        cm->pending = false;
+    }
+    const int R = c.nranks;
+    RouteArgs ra{};
+    ra.state = ctx->state; ra.tile_count = ctx->tile_count; ra.words = ctx->words;
+    ra.dead_rec = ctx->dead_rec; ra.dead_info = ctx->dead_info; ra.dead_cap = (uint32_t)ctx->cap;
+    ra.cuts = cm->d_cuts; ra.ncuts0 = cm->ncuts[0]; ra.ncuts1 = cm->ncuts[1]; ra.ncuts2 = cm->ncuts[2];
+    ra.lay0 = c.layout[0]; ra.lay1 = c.layout[1];
+    ra.bx = ctx->bits[0]; ra.by = ctx->bits[1];
+    ra.mx = (1u << ctx->bits[0]) - 1u; ra.my = (1u << ctx->bits[1]) - 1u;
+    ra.me = c.rank;
+    ra.count = cm->d_route_count; ra.pos = cm->d_route_pos;
+    std::vector<uint32_t> seg(R + 1, 0), cnt(R, 0);
+    uint32_t* d_seg = nullptr;
+    CKC(cudaMalloc(&d_seg, sizeof(uint32_t) * (R + 1)));
+    CKC(cudaMemsetAsync(cm->d_route_count, 0, sizeof(uint32_t) * 2 * R, ctx->stream));
+    const int blocks = ctx->num_sms * 4;
+    ra.pass = 0;
+    route_kernel<<<blocks, 256, 0, ctx->stream>>>(ra);
+    ++ctx->launches;
+    CKC(cudaMemcpyAsync(cnt.data(), cm->d_route_count, sizeof(uint32_t) * R, cudaMemcpyDeviceToHost, ctx->stream));
+    CKC(cudaStreamSynchronize(ctx->stream));
+    for (int r = 0; r < R; ++r) seg[r + 1] = seg[r] + cnt[r];
+    if (seg[R] > (uint32_t)cm->route_cap) { cudaFree(d_seg); lag_set_error(ctx, "route buffer overflow"); return LAG_EOVERFLOW; }
+    CKC(cudaMemcpyAsync(d_seg, seg.data(), sizeof(uint32_t) * (R + 1), cudaMemcpyHostToDevice, ctx->stream));
+    ra.pass = 1; ra.seg = d_seg; ra.out = cm->route;
+    route_kernel<<<blocks, 256, 0, ctx->stream>>>(ra);
+    ++ctx->launches;
+    // exchange the counts: everyone learns how much it receives from whom
+    uint32_t* d_all = nullptr;
+    CKC(cudaMalloc(&d_all, sizeof(uint32_t) * R * (R + 1)));
+    CKC(cudaMemcpyAsync(d_all, cnt.data(), sizeof(uint32_t) * R, cudaMemcpyHostToDevice, ctx->stream));
+    CKN(ncclAllGather(d_all, d_all + R, R, ncclUint32, cm->nccl, ctx->stream));
+    std::vector<uint32_t> all((size_t)R * R);
+    CKC(cudaMemcpyAsync(all.data(), d_all + R, sizeof(uint32_t) * R * R, cudaMemcpyDeviceToHost, ctx->stream));
+    CKC(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_all);
+    std::vector<uint32_t> rseg(R + 1, 0);
+    for (int r = 0; r < R; ++r) rseg[r + 1] = rseg[r] + (r == c.rank ? 0 : all[(size_t)r * R + c.rank]);
+    if (rseg[R] > (uint32_t)cm->route_cap) { cudaFree(d_seg); lag_set_error(ctx, "route receive overflow"); return LAG_EOVERFLOW; }
+    CKN(ncclGroupStart());
+    for (int r = 0; r < R; ++r) {
+        if (r == c.rank) continue;
+        if (cnt[r]) CKN(ncclSend(cm->route + seg[r], (size_t)cnt[r] * sizeof(RouteRec), ncclUint8, r, cm->nccl, ctx->stream));
+        const uint32_t in = all[(size_t)r * R + c.rank];
+        if (in) CKN(ncclRecv(cm->route_recv + rseg[r], (size_t)in * sizeof(RouteRec), ncclUint8, r, cm->nccl, ctx->stream));
+    }
+    CKN(ncclGroupEnd());
+    CKC(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_seg);
+    cm->n_returned = rseg[R];
+    return LAG_OK;
+}
+
+// Returned records for extract (valid when lag_comm_return_to_origin ran).
+void lag_comm_returned(lag_ctx_s* ctx, const float4** rec, int64_t* stride_f4, uint32_t* n) {
+    Comm* cm = ctx->comm;
+    *rec = cm ? reinterpret_cast<const float4*>(cm->route_recv) : nullptr;
+    *stride_f4 = sizeof(RouteRec) / sizeof(float4);
+    *n = cm ? cm->n_returned : 0;
+}
+
+extern "C" lag_status lag_nccl_unique_id(void* out, int64_t out_bytes) {
+    lag_ctx_s* ctx = nullptr;
+    if (!out || out_bytes < (int64_t)sizeof(ncclUniqueId)) {
+        lag_set_error(nullptr, "need %zu bytes for ncclUniqueId", sizeof(ncclUniqueId));
+        return LAG_EINVAL;
+    }
+    ncclUniqueId id;
+    CKN(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+    return LAG_OK;
+}

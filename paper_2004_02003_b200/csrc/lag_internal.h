@@ -1,0 +1,67 @@
+// lag_internal.h — context layout shared by lag_api.cu and lag_comm.cu.
+#pragma once
+#include "lag.h"
+#include "lag_kernels.cuh"
+
+#include <cuda_runtime.h>
+#include <string>
+
+namespace lag {
+enum : int { W_DEAD = 0, W_ERR = 1, W_NTILES = 2, kWords = 8 };
+struct Comm;   // lag_comm.cu
+}
+
+struct lag_ctx_s {
+    lag_config cfg{};
+    cudaStream_t stream = nullptr;
+    std::string msg = "no error";
+    // geometry
+    int ext[3] = {1, 1, 1};          // slice extent (nodes) incl. ghosts
+    int base[3] = {0, 0, 0};         // global node of slice element 0
+    int bits[3] = {0, 0, 0};         // packed seed-node widths
+    int64_t slice_floats = 0;
+    int num_sms = 148;
+    int advect_blocks_per_sm = 1;
+    // particles
+    int64_t max_seeds = 0, cap = 0;
+    int cap_tiles = 0;
+    int n_tiles = 0;                 // tiles holding seeds
+    int64_t n_seeds = 0, active_host = 0;
+    int first[3] = {0, 0, 0}, ns[3] = {1, 1, 1};
+    int stride = 1;
+    bool seeded = false;
+    bool stream_synced_needed = true;
+    int cycles_in_interval = 0;
+    int64_t cycles_total = 0;
+    int64_t launches = 0;
+    float4* state = nullptr;
+    uint8_t* tile_count = nullptr;
+    float4* dead_rec = nullptr;
+    uint32_t* dead_info = nullptr;
+    uint32_t* words = nullptr;                 // W_*
+    unsigned long long* counters = nullptr;    // CNT_*
+    uint32_t host_words[lag::kWords] = {0};
+    // extraction staging (device)
+    double* out_start = nullptr;
+    double* out_end = nullptr;
+    uint8_t* out_status = nullptr;
+    // host-pointer staging (end-to-end path)
+    float* stage[2] = {nullptr, nullptr};
+    const void* stage_src[2] = {nullptr, nullptr};
+    const void* last_v1 = nullptr;
+    // COMM
+    lag::Comm* comm = nullptr;
+};
+
+int lag_set_error(lag_ctx_s* ctx, const char* fmt, ...);
+lag_status lag_reset_interval(lag_ctx_s* ctx);
+
+// lag_comm.cu
+lag_status lag_comm_init(lag_ctx_s* ctx);
+void lag_comm_destroy(lag_ctx_s* ctx);
+lag_status lag_comm_reset(lag_ctx_s* ctx);
+lag_status lag_comm_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool v0_is_prev_v1);
+void lag_comm_fill_args(lag_ctx_s* ctx, lag::AdvectArgs* a);
+lag_status lag_comm_post_advect(lag_ctx_s* ctx);
+lag_status lag_comm_return_to_origin(lag_ctx_s* ctx);
+void lag_comm_returned(lag_ctx_s* ctx, const float4** rec, int64_t* stride_f4, uint32_t* n);

@@ -1,0 +1,461 @@
+// lag_kernels.cuh — sm_100a kernels of the in situ Lagrangian flow-map hot path.
+//
+// Paper: arXiv 2004.02003 (P:nnn = PAPER.md line).  Design: DESIGN.md.
+//
+// Particle record (16 B, one float4): (d_x, d_y, d_z, bits(g)) where g is the
+// particle's integer global seed node packed into 32 bits (bx | by | bz bits)
+// and d its displacement from g in cell units.  Position in index space is
+// u = g + d; keeping d small preserves fp32 precision.
+//
+// Particle list = warp tiles of 32 records + one u8 live count per tile.  The
+// advect kernel compacts survivors in place inside each tile (warp ballot),
+// so invalid particles are never launched again ("managing memory to
+// prevent invalid particles from being launched on GPU threads").  No atomics
+// on the hot path; order inside a tile is stable (deterministic).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lag {
+
+constexpr int kTile = 32;
+constexpr int kThreads = 256;
+
+enum : uint32_t { ERR_OVERFLOW = 1u, ERR_GHOST = 2u, ERR_NONFINITE = 4u };
+enum : int { CNT_STEPS = 0, CNT_TERM = 1, CNT_EXIT = 2, CNT_SENT = 3, CNT_RECV = 4, CNT_N = 8 };
+enum : uint8_t { ST_VALID = 0, ST_TERM = 1, ST_EXIT = 2 };
+
+struct AdvectArgs {
+    const float* __restrict__ v0;   // slice at t   (AoS, element 0 = global node base)
+    const float* __restrict__ v1;   // slice at t+dt
+    float4* state;                  // particle records, tiles of 32
+    uint8_t* tile_count;            // live records per tile
+    const int32_t* n_tiles_dev;     // device-side tile count (COMM appends) or nullptr
+    int32_t n_tiles;                // host-known tile count (used when n_tiles_dev == nullptr)
+    int32_t N[3];                   // global nodes
+    int32_t lo[3], hi[3];           // block [lo, hi)
+    int32_t base[3];                // global node index of slice element 0 (= lo - G)
+    int32_t cmax[3];                // largest local cell index a gather may use (ext - 2)
+    int32_t sx, sxy;                // slice pitch (nodes) of a row / a plane
+    float hdth[3], qdth[3], sdth[3];// dt/h * (1/2, 1/4, 1/6)
+    uint32_t bx, by;                // packed seed-node bit widths (x, y)
+    uint32_t mx, my;                // masks
+    // termination records (both modes): appended, scattered by extract
+    float4* dead_rec;
+    uint32_t* dead_info;            // (status << 24) | cycle
+    uint32_t* dead_count;
+    uint32_t dead_cap;
+    unsigned long long* counters;   // CNT_*
+    uint32_t* err;
+    int32_t cycle;
+    // COMM: outgoing slots, one per neighbour offset (3^dim):
+    // slot k = slot_rec[slot_base[k]] = header (u32 count) then slot_capv[k] records
+    float4* slot_rec;
+    int32_t slot_base[27];
+    int32_t slot_capv[27];
+};
+
+__device__ __forceinline__ void unpack_g(uint32_t w, const AdvectArgs& a, int g[3]) {
+    g[0] = (int)(w & a.mx);
+    g[1] = (int)((w >> a.bx) & a.my);
+    g[2] = (int)(w >> (a.bx + a.by));
+}
+
+// Corner gather: the 2^DIM corners of local cell li, DIM components each, AoS.
+// C layout: [(dz*2 + dy)*2 + dx][comp].
+template <int DIM>
+__device__ __forceinline__ void gather(const float* __restrict__ v, const int li[3],
+                                       int sx, int sxy, float* C) {
+    if constexpr (DIM == 3) {
+        const float* p = v + 3 * (li[0] + sx * li[1] + sxy * li[2]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int dy = r & 1, dz = r >> 1;
+            const float* q = p + 3 * (dy * sx + dz * sxy);
+#pragma unroll
+            for (int e = 0; e < 6; ++e) C[r * 6 + e] = __ldg(q + e);
+        }
+    } else {
+        const float* p = v + 2 * (li[0] + sx * li[1]);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const float* q = p + 2 * (r * sx);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) C[r * 4 + e] = __ldg(q + e);
+        }
+    }
+}
+
+// Multilinear interpolation inside one cell with fractional offsets f.
+template <int DIM>
+__device__ __forceinline__ void interp(const float* C, const float f[3], float out[3]) {
+    if constexpr (DIM == 3) {
+        const float ux = 1.f - f[0], uy = 1.f - f[1], uz = 1.f - f[2];
+        float w[8];
+        const float w00 = uy * uz, w10 = f[1] * uz, w01 = uy * f[2], w11 = f[1] * f[2];
+        w[0] = ux * w00; w[1] = f[0] * w00;
+        w[2] = ux * w10; w[3] = f[0] * w10;
+        w[4] = ux * w01; w[5] = f[0] * w01;
+        w[6] = ux * w11; w[7] = f[0] * w11;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            float s = w[0] * C[c];
+#pragma unroll
+            for (int k = 1; k < 8; ++k) s = fmaf(w[k], C[k * 3 + c], s);
+            out[c] = s;
+        }
+    } else {
+        const float ux = 1.f - f[0], uy = 1.f - f[1];
+        float w[4] = {ux * uy, f[0] * uy, ux * f[1], f[0] * f[1]};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            float s = w[0] * C[c];
+#pragma unroll
+            for (int k = 1; k < 4; ++k) s = fmaf(w[k], C[k * 2 + c], s);
+            out[c] = s;
+        }
+        out[2] = 0.f;
+    }
+}
+
+// Locate a stage sample e (displacement from g, cell units).
+// Returns ST_VALID / ST_EXIT / ST_TERM; fills the interpolation cell (local)
+// and fractional offsets.  All boundary decisions are integer compares on the
+// cell index c = g + floor(e) (exact).
+template <int DIM, bool BTO>
+__device__ __forceinline__ uint8_t locate(const AdvectArgs& a, const int g[3], const float e[3],
+                                          int li[3], float f[3], bool& ghost_bad) {
+    bool out_dom = false, out_blk = false, gb = false;
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) {
+        const float fl = floorf(e[ax]);
+        float fr = e[ax] - fl;                       // exact
+        int c = g[ax] + __float2int_rz(fl);
+        // closed global domain [0, N-1] in index space
+        out_dom |= (c < 0) | (c > a.N[ax] - 1) | ((c == a.N[ax] - 1) & (fr != 0.f));
+        if constexpr (BTO)                           // half-open block, closed at the global top
+            out_blk |= (c < a.lo[ax]) | ((c >= a.hi[ax]) & (a.hi[ax] < a.N[ax]));
+        if (c == a.N[ax] - 1) { c = a.N[ax] - 2; fr = 1.f; }   // closed upper face: f = 1
+        int l = c - a.base[ax];
+        if constexpr (!BTO) gb |= (l < 0) | (l > a.cmax[ax]);
+        l = min(max(l, 0), a.cmax[ax]);              // never read outside the slice
+        li[ax] = l;
+        f[ax] = fr;
+    }
+    if constexpr (DIM == 2) { li[2] = 0; f[2] = 0.f; }
+    const uint8_t st = out_dom ? ST_EXIT : (out_blk ? ST_TERM : ST_VALID);
+    if constexpr (!BTO) ghost_bad |= gb & (st == ST_VALID);
+    return st;
+}
+
+// The first failing stage decides the outcome (the oracle stops there).
+__device__ __forceinline__ uint8_t first_fail(uint8_t cur, uint8_t next) {
+    return cur != ST_VALID ? cur : next;
+}
+
+template <int DIM, bool BTO>
+__global__ void __launch_bounds__(kThreads, 2)
+advect_kernel(const AdvectArgs a) {
+    constexpr int NC = (1 << DIM) * DIM;             // corner floats per slice
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * kThreads) >> 5;
+    const int n_tiles = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
+
+    unsigned long long steps = 0, nterm = 0, nexit = 0, nsent = 0;
+    uint32_t errbits = 0;
+
+    for (int tile = warp; tile < n_tiles; tile += nwarps) {
+        const int cnt = a.tile_count[tile];
+        if (cnt == 0) continue;
+        const bool live = lane < cnt;
+        float4* trec = a.state + (size_t)tile * kTile;
+        float4 r = live ? trec[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        int g[3];
+        unpack_g(__float_as_uint(r.w), a, g);
+        const float d[3] = {r.x, r.y, DIM == 3 ? r.z : 0.f};
+
+        float S[NC], B[NC];
+        int cur[3], li[3];
+        float f[3], e[3];
+        bool ghost_bad = false;
+        uint8_t st = ST_VALID;
+
+        // ---- stage 1: q1 = x (already validated when committed) ----
+        locate<DIM, BTO>(a, g, d, li, f, ghost_bad);
+        if (live) {
+            gather<DIM>(a.v0, li, a.sx, a.sxy, S);
+            gather<DIM>(a.v1, li, a.sx, a.sxy, B);
+        }
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) cur[ax] = li[ax];
+        float k1[3];
+        interp<DIM>(S, f, k1);
+#pragma unroll
+        for (int i = 0; i < NC; ++i) S[i] += B[i];       // S = v0 + v1 (stages 2, 3)
+
+        // ---- stage 2: q2 = x + dt/2 k1, alpha = 1/2 ----
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], k1[ax], d[ax]);
+        st = first_fail(st, locate<DIM, BTO>(a, g, e, li, f, ghost_bad));
+        if (live && st == ST_VALID && (li[0] != cur[0] || li[1] != cur[1] || li[2] != cur[2])) {
+            gather<DIM>(a.v0, li, a.sx, a.sxy, S);
+            gather<DIM>(a.v1, li, a.sx, a.sxy, B);
+#pragma unroll
+            for (int i = 0; i < NC; ++i) S[i] += B[i];
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) cur[ax] = li[ax];
+        }
+        float T2[3];
+        interp<DIM>(S, f, T2);                          // T2 = 2 k2
+
+        // ---- stage 3: q3 = x + dt/2 k2 = x + dt/4 T2, alpha = 1/2 ----
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.qdth[ax], T2[ax], d[ax]);
+        st = first_fail(st, locate<DIM, BTO>(a, g, e, li, f, ghost_bad));
+        if (live && st == ST_VALID && (li[0] != cur[0] || li[1] != cur[1] || li[2] != cur[2])) {
+            gather<DIM>(a.v0, li, a.sx, a.sxy, S);
+            gather<DIM>(a.v1, li, a.sx, a.sxy, B);
+#pragma unroll
+            for (int i = 0; i < NC; ++i) S[i] += B[i];
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) cur[ax] = li[ax];
+        }
+        float T3[3];
+        interp<DIM>(S, f, T3);                          // T3 = 2 k3
+
+        // ---- stage 4: q4 = x + dt k3 = x + dt/2 T3, alpha = 1 ----
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], T3[ax], d[ax]);
+        st = first_fail(st, locate<DIM, BTO>(a, g, e, li, f, ghost_bad));
+        if (live && st == ST_VALID && (li[0] != cur[0] || li[1] != cur[1] || li[2] != cur[2])) {
+            gather<DIM>(a.v1, li, a.sx, a.sxy, B);
+        }
+        float k4[3];
+        interp<DIM>(B, f, k4);
+
+        // ---- update: x' = x + dt/6 (k1 + 2k2 + 2k3 + k4) ----
+        float dn[3];
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax)
+            dn[ax] = fmaf(a.sdth[ax], (k1[ax] + k4[ax]) + (T2[ax] + T3[ax]), d[ax]);
+        if constexpr (DIM == 2) dn[2] = 0.f;
+        bool finite = true;
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax) finite &= fabsf(dn[ax]) < 1.0e30f;
+        {
+            int lj[3]; float fj[3];
+            st = first_fail(st, locate<DIM, BTO>(a, g, dn, lj, fj, ghost_bad));
+        }
+        if (live && !finite) { errbits |= ERR_NONFINITE; st = ST_EXIT; }
+        if (live && ghost_bad) { errbits |= ERR_GHOST; if (st == ST_VALID) st = ST_EXIT; }
+
+        // ---- COMM: updated position in another block -> hand off ----
+        bool migrate = false;
+        int nb = 0;
+        if constexpr (!BTO) {
+            if (live && st == ST_VALID) {
+                int mul = 1;
+#pragma unroll
+                for (int ax = 0; ax < DIM; ++ax) {
+                    const int c = g[ax] + __float2int_rz(floorf(dn[ax]));
+                    const int o = (c < a.lo[ax]) ? -1 : ((c >= a.hi[ax] && a.hi[ax] < a.N[ax]) ? 1 : 0);
+                    migrate |= (o != 0);
+                    nb += (o + 1) * mul;
+                    mul *= 3;
+                }
+            }
+        }
+
+        // ---- particle management: compact survivors, record terminations ----
+        const bool keep = live && st == ST_VALID && !migrate;
+        const unsigned kmask = __ballot_sync(0xffffffffu, keep);
+        const unsigned dmask = __ballot_sync(0xffffffffu, live && st != ST_VALID);
+        const unsigned tmask = __ballot_sync(0xffffffffu, live && st == ST_TERM);
+        __syncwarp();
+        if (keep) {
+            const int pos = __popc(kmask & ((1u << lane) - 1u));
+            trec[pos] = make_float4(dn[0], dn[1], dn[2], r.w);
+        }
+        if constexpr (!BTO) {
+            const unsigned mmask = __ballot_sync(0xffffffffu, migrate);
+            if (migrate) {
+                const unsigned peers = __match_any_sync(mmask, nb);
+                const int leader = __ffs(peers) - 1;
+                float4* sb = a.slot_rec + a.slot_base[nb];
+                uint32_t base0 = 0;
+                if (lane == leader) base0 = atomicAdd(reinterpret_cast<uint32_t*>(sb), (uint32_t)__popc(peers));
+                base0 = __shfl_sync(peers, base0, leader);
+                const uint32_t pos = base0 + __popc(peers & ((1u << lane) - 1u));
+                if (pos < (uint32_t)a.slot_capv[nb])
+                    sb[1 + pos] = make_float4(dn[0], dn[1], dn[2], r.w);
+                else
+                    errbits |= ERR_OVERFLOW;
+            }
+            if (lane == 0) nsent += __popc(mmask);
+        }
+        if (dmask) {
+            uint32_t slot0 = 0;
+            if (lane == 0) slot0 = atomicAdd(a.dead_count, (uint32_t)__popc(dmask));
+            slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+            if (live && st != ST_VALID) {
+                const uint32_t s = slot0 + __popc(dmask & ((1u << lane) - 1u));
+                if (s < a.dead_cap) {
+                    a.dead_rec[s] = r;                   // pre-step position
+                    a.dead_info[s] = ((uint32_t)st << 24) | (uint32_t)(a.cycle & 0xffffff);
+                } else {
+                    errbits |= ERR_OVERFLOW;
+                }
+            }
+        }
+        if (lane == 0) {
+            a.tile_count[tile] = (uint8_t)__popc(kmask);
+            steps += (unsigned long long)cnt;
+            nterm += __popc(tmask);
+            nexit += __popc(dmask) - __popc(tmask);
+        }
+    }
+
+    // one atomic per CTA per counter
+    __shared__ unsigned long long s_cnt[4];
+    __shared__ uint32_t s_err;
+    if (threadIdx.x == 0) { s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0; s_err = 0; }
+    __syncthreads();
+    if (lane == 0 && steps) {
+        atomicAdd(&s_cnt[0], steps);
+        if (nterm) atomicAdd(&s_cnt[1], nterm);
+        if (nexit) atomicAdd(&s_cnt[2], nexit);
+        if (nsent) atomicAdd(&s_cnt[3], nsent);
+    }
+    if (errbits) atomicOr(&s_err, errbits);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_cnt[0]) atomicAdd(&a.counters[CNT_STEPS], s_cnt[0]);
+        if (s_cnt[1]) atomicAdd(&a.counters[CNT_TERM], s_cnt[1]);
+        if (s_cnt[2]) atomicAdd(&a.counters[CNT_EXIT], s_cnt[2]);
+        if (s_cnt[3]) atomicAdd(&a.counters[CNT_SENT], s_cnt[3]);
+        if (s_err) atomicOr(a.err, s_err);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// seeding: lattice nodes g = first + stride * (ix, iy, iz), x fastest
+struct SeedArgs {
+    float4* state;
+    uint8_t* tile_count;
+    int64_t n;
+    int32_t first[3], stride, ns[3];
+    uint32_t bx, by;
+};
+
+static __global__ void seed_kernel(const SeedArgs a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n_tiles = (a.n + kTile - 1) / kTile;
+    if (i < n_tiles * kTile) {
+        if (i < a.n) {
+            const int64_t ix = i % a.ns[0];
+            const int64_t t = i / a.ns[0];
+            const int64_t iy = t % a.ns[1];
+            const int64_t iz = t / a.ns[1];
+            const uint32_t gx = (uint32_t)(a.first[0] + a.stride * ix);
+            const uint32_t gy = (uint32_t)(a.first[1] + a.stride * iy);
+            const uint32_t gz = (uint32_t)(a.first[2] + a.stride * iz);
+            const uint32_t w = gx | (gy << a.bx) | (gz << (a.bx + a.by));
+            a.state[i] = make_float4(0.f, 0.f, 0.f, __uint_as_float(w));
+        }
+        if ((i % kTile) == 0) {
+            const int64_t rem = a.n - i;
+            a.tile_count[i / kTile] = (uint8_t)(rem >= kTile ? kTile : rem);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// extraction: scatter live and terminated records to seed order (fp64 output)
+struct ExtractArgs {
+    const float4* state;
+    const uint8_t* tile_count;
+    int32_t n_tiles;
+    const float4* dead_rec;
+    const uint32_t* dead_info;
+    uint32_t n_dead;
+    int64_t n;                      // seeds
+    int32_t dim;
+    int32_t first[3], stride, ns[3];
+    uint32_t bx, by, mx, my;
+    double o[3], h[3];
+    int32_t lo[3], hi[3];           // own block: records seeded elsewhere are skipped (COMM)
+    const float4* ret;              // COMM: records returned to this origin (32 B each:
+    uint32_t n_ret;                 //        float4 record, u32 info, pad)
+    double* start;                  // [n][dim]
+    double* end;                    // [n][dim]
+    uint8_t* status;                // [n]
+};
+
+__device__ __forceinline__ bool own_seed(const ExtractArgs& a, uint32_t w) {
+    const int g[3] = {(int)(w & a.mx), (int)((w >> a.bx) & a.my), (int)(w >> (a.bx + a.by))};
+    bool in = true;
+    for (int ax = 0; ax < 3; ++ax) in &= (g[ax] >= a.lo[ax]) & (g[ax] < a.hi[ax]);
+    return in;
+}
+
+__device__ __forceinline__ int64_t seed_index(const ExtractArgs& a, uint32_t w, int g[3]) {
+    g[0] = (int)(w & a.mx);
+    g[1] = (int)((w >> a.bx) & a.my);
+    g[2] = (int)(w >> (a.bx + a.by));
+    const int64_t ix = (g[0] - a.first[0]) / a.stride;
+    const int64_t iy = (g[1] - a.first[1]) / a.stride;
+    const int64_t iz = (g[2] - a.first[2]) / a.stride;
+    return ix + a.ns[0] * (iy + a.ns[1] * iz);
+}
+
+static __global__ void extract_start_kernel(const ExtractArgs a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const int64_t idx[3] = {i % a.ns[0], (i / a.ns[0]) % a.ns[1], i / ((int64_t)a.ns[0] * a.ns[1])};
+    for (int ax = 0; ax < a.dim; ++ax)
+        a.start[i * a.dim + ax] = a.o[ax] + (double)(a.first[ax] + a.stride * idx[ax]) * a.h[ax];
+}
+
+static __global__ void extract_live_kernel(const ExtractArgs a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t tile = i / kTile;
+    if (tile >= a.n_tiles) return;
+    if ((int)(i % kTile) >= a.tile_count[tile]) return;
+    const float4 r = a.state[i];
+    if (!own_seed(a, __float_as_uint(r.w))) return;
+    int g[3];
+    const int64_t s = seed_index(a, __float_as_uint(r.w), g);
+    const float d[3] = {r.x, r.y, r.z};
+    for (int ax = 0; ax < a.dim; ++ax)
+        a.end[s * a.dim + ax] = a.o[ax] + ((double)g[ax] + (double)d[ax]) * a.h[ax];
+    a.status[s] = ST_VALID;
+}
+
+static __global__ void extract_dead_kernel(const ExtractArgs a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n_dead) return;
+    const float4 r = a.dead_rec[i];
+    if (!own_seed(a, __float_as_uint(r.w))) return;
+    int g[3];
+    const int64_t s = seed_index(a, __float_as_uint(r.w), g);
+    const float d[3] = {r.x, r.y, r.z};
+    for (int ax = 0; ax < a.dim; ++ax)
+        a.end[s * a.dim + ax] = a.o[ax] + ((double)g[ax] + (double)d[ax]) * a.h[ax];
+    a.status[s] = (uint8_t)(a.dead_info[i] >> 24);
+}
+
+static __global__ void extract_returned_kernel(const ExtractArgs a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n_ret) return;
+    const float4 r = a.ret[2 * i];
+    const uint32_t info = __float_as_uint(a.ret[2 * i + 1].x);
+    int g[3];
+    const int64_t s = seed_index(a, __float_as_uint(r.w), g);
+    const float d[3] = {r.x, r.y, r.z};
+    for (int ax = 0; ax < a.dim; ++ax)
+        a.end[s * a.dim + ax] = a.o[ax] + ((double)g[ax] + (double)d[ax]) * a.h[ax];
+    a.status[s] = (uint8_t)(info >> 24);
+}
+
+}  // namespace lag

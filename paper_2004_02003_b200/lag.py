@@ -1,0 +1,225 @@
+"""Thin ctypes binding of liblag (include/lag.h).  Argument marshalling only:
+every step of the hot path runs in the library's CUDA kernels.  There is no
+CPU fallback — if liblag.so is missing the import fails loudly.
+
+Functions carry the C names (lag_init, lag_seed, lag_advect_cycle,
+lag_extract, lag_stats, lag_destroy, lag_last_error, lag_nccl_unique_id);
+a non-zero lag_status raises LagError.  Array arguments may be torch tensors
+(device or host), numpy arrays, or raw integer addresses.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblag.so")
+
+LAG_OK, LAG_EINVAL, LAG_ESTATE, LAG_EEMPTY, LAG_ENOMEM = 0, -1, -2, -3, -4
+LAG_ECUDA, LAG_ENCCL, LAG_EOVERFLOW, LAG_EGHOST, LAG_ENONFINITE = -5, -6, -7, -8, -9
+LAG_BTO, LAG_COMM = 0, 1
+LAG_VALID, LAG_TERM_BOUNDARY, LAG_EXIT_DOMAIN = 0, 1, 2
+LAG_NO_RESEED = 1
+STATUS_NAMES = {0: "LAG_OK", -1: "LAG_EINVAL", -2: "LAG_ESTATE", -3: "LAG_EEMPTY",
+                -4: "LAG_ENOMEM", -5: "LAG_ECUDA", -6: "LAG_ENCCL", -7: "LAG_EOVERFLOW",
+                -8: "LAG_EGHOST", -9: "LAG_ENONFINITE"}
+
+# every symbol include/lag.h declares
+EXPORTS = ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_stats",
+           "lag_destroy", "lag_last_error", "lag_nccl_unique_id", "lag_kernel_launches",
+           "lag_abi_version")
+
+
+class LagError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class lag_config(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("global_nodes", ctypes.c_int64 * 3), ("origin", ctypes.c_double * 3),
+                ("spacing", ctypes.c_double * 3), ("block_lo", ctypes.c_int64 * 3),
+                ("block_hi", ctypes.c_int64 * 3), ("ghost", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
+                ("layout", ctypes.c_int32 * 3), ("pad_", ctypes.c_int32),
+                ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+
+
+class lag_stats_t(ctypes.Structure):
+    _fields_ = [("seeded", ctypes.c_int64), ("active", ctypes.c_int64),
+                ("term_boundary", ctypes.c_int64), ("exit_domain", ctypes.c_int64),
+                ("sent", ctypes.c_int64), ("received", ctypes.c_int64),
+                ("particle_steps", ctypes.c_int64), ("cycles", ctypes.c_int64),
+                ("device_error", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"liblag.so not built at {path}: run `python __graft_entry__.py build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    vp = ctypes.c_void_p
+    lib.lag_init.argtypes = [P(lag_config), P(vp)]
+    lib.lag_seed.argtypes = [vp, ctypes.c_int32, P(ctypes.c_int64)]
+    lib.lag_advect_cycle.argtypes = [vp, vp, vp, ctypes.c_double]
+    lib.lag_extract.argtypes = [vp, vp, vp, vp, ctypes.c_int64, P(ctypes.c_int64), ctypes.c_uint32]
+    lib.lag_stats.argtypes = [vp, P(lag_stats_t)]
+    lib.lag_destroy.argtypes = [vp]
+    lib.lag_last_error.argtypes = [vp]
+    lib.lag_last_error.restype = ctypes.c_char_p
+    lib.lag_nccl_unique_id.argtypes = [vp, ctypes.c_int64]
+    lib.lag_kernel_launches.argtypes = [vp]
+    lib.lag_kernel_launches.restype = ctypes.c_int64
+    lib.lag_abi_version.restype = ctypes.c_int32
+    for name in ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_stats",
+                 "lag_destroy", "lag_nccl_unique_id"):
+        getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _addr(x) -> Optional[int]:
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):          # torch.Tensor
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):            # numpy array
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return x.ctypes.data
+    raise TypeError(f"cannot take the address of {type(x)}")
+
+
+def _check(st: int, ctx=None):
+    if st != LAG_OK:
+        msg = load().lag_last_error(ctx).decode(errors="replace")
+        raise LagError(st, msg)
+
+
+def lag_last_error(ctx=None) -> str:
+    return load().lag_last_error(ctx).decode(errors="replace")
+
+
+def lag_abi_version() -> int:
+    return load().lag_abi_version()
+
+
+def lag_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().lag_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+def make_config(dim: int, global_nodes: Sequence[int], origin: Sequence[float],
+                spacing: Sequence[float], block_lo: Sequence[int], block_hi: Sequence[int],
+                mode: int = LAG_BTO, ghost: int = 0, device: int = 0, rank: int = 0,
+                nranks: int = 1, layout: Sequence[int] = (1, 1, 1),
+                nccl_id: Optional[bytes] = None, stream: Optional[int] = None) -> lag_config:
+    c = lag_config()
+    c.dim, c.mode, c.ghost, c.device = dim, mode, ghost, device
+    c.rank, c.nranks = rank, nranks
+    for a in range(3):
+        c.global_nodes[a] = int(global_nodes[a])
+        c.origin[a] = float(origin[a])
+        c.spacing[a] = float(spacing[a])
+        c.block_lo[a] = int(block_lo[a])
+        c.block_hi[a] = int(block_hi[a])
+        c.layout[a] = int(layout[a])
+    if nccl_id is not None:
+        c._nccl_buf = ctypes.create_string_buffer(nccl_id, 128)   # keep alive with the struct
+        c.nccl_id = ctypes.cast(c._nccl_buf, ctypes.c_void_p)
+    c.stream = stream or None
+    return c
+
+
+def lag_init(cfg: lag_config) -> ctypes.c_void_p:
+    ctx = ctypes.c_void_p()
+    _check(load().lag_init(ctypes.byref(cfg), ctypes.byref(ctx)))
+    return ctx
+
+
+def lag_seed(ctx, stride: int) -> int:
+    n = ctypes.c_int64(0)
+    _check(load().lag_seed(ctx, int(stride), ctypes.byref(n)), ctx)
+    return n.value
+
+
+def lag_advect_cycle(ctx, v_t, v_t1, dt: float) -> None:
+    _check(load().lag_advect_cycle(ctx, _addr(v_t), _addr(v_t1), float(dt)), ctx)
+
+
+def lag_extract(ctx, start=None, end=None, status=None, capacity: Optional[int] = None,
+                flags: int = 0) -> int:
+    """Returns n; outputs are written into the given buffers.  Latched async
+    errors raise LagError after the outputs were written."""
+    n = ctypes.c_int64(0)
+    if capacity is None:
+        caps = [x.shape[0] for x in (start, end, status) if x is not None]
+        capacity = min(caps) if caps else 0
+    _check(load().lag_extract(ctx, _addr(start), _addr(end), _addr(status), int(capacity),
+                              ctypes.byref(n), int(flags)), ctx)
+    return n.value
+
+
+def lag_stats(ctx) -> dict:
+    s = lag_stats_t()
+    _check(load().lag_stats(ctx, ctypes.byref(s)), ctx)
+    return {f: getattr(s, f) for f, _ in lag_stats_t._fields_ if f != "pad_"}
+
+
+def lag_destroy(ctx) -> None:
+    _check(load().lag_destroy(ctx))
+
+
+def lag_kernel_launches(ctx) -> int:
+    return int(load().lag_kernel_launches(ctx))
+
+
+class Context:
+    """Owning handle for one block's lag_ctx (marshalling only)."""
+
+    def __init__(self, cfg: lag_config):
+        self.cfg = cfg
+        self.dim = cfg.dim
+        self.ctx = lag_init(cfg)
+        self.n = 0
+
+    def seed(self, stride: int) -> int:
+        self.n = lag_seed(self.ctx, stride)
+        return self.n
+
+    def advect(self, v_t, v_t1, dt: float) -> None:
+        lag_advect_cycle(self.ctx, v_t, v_t1, dt)
+
+    def extract(self, start=None, end=None, status=None, flags: int = 0) -> int:
+        return lag_extract(self.ctx, start, end, status, flags=flags)
+
+    def stats(self) -> dict:
+        return lag_stats(self.ctx)
+
+    def launches(self) -> int:
+        return lag_kernel_launches(self.ctx)
+
+    def close(self):
+        if self.ctx is not None:
+            lag_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
