@@ -37,7 +37,7 @@ UNIT = "particle-steps/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="lag", choices=["lag", "reference"])
     ap.add_argument("--config", default="C5")
@@ -105,51 +105,60 @@ def broadcast_bytes(b, world, rank):
 # clocks sampled during the timed region
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """NVML polling (2 ms) of SM clocks and clock-event reasons during the
+    timed region (the B200_PROFILING.md clocks line, at a rate that resolves
+    a region of a few tens of ms)."""
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+               "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
-    def __init__(self, index):
-        self.index = index
-        self.rows = []
-        self.proc = None
+    def __init__(self, cuda_index):
+        self.cuda_index = cuda_index
+        self.sm, self.mask = [], 0
+        self.stop_flag = False
+        self.handle = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            import torch
+            self.nv = pynvml
+            pynvml.nvmlInit()
+            p = torch.cuda.get_device_properties(self.cuda_index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            try:
+                self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.cuda_index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # pragma: no cover
+            self.err = repr(e)
+            self.handle = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
+    def _poll(self):
+        nv = self.nv
+        while not self.stop_flag:
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM))
+                self.mask |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for k, nm in enumerate(names):
-                if r[4 + k].lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        if self.handle is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self.stop_flag = True
+        self.thread.join(timeout=1)
+        reasons = sorted(k for k, v in self.REASONS.items()
+                         if hasattr(self.nv, v) and self.mask & getattr(self.nv, v))
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": self.max_sm, "reasons": reasons, "samples": len(self.sm),
+                "source": "NVML every 2 ms during the timed region"}
 
 
 # ---------------------------------------------------------------------------
@@ -282,36 +291,34 @@ def ncu_traffic(config):
         return None
 
 
-def cpu_baseline(cfg, seconds_target=12.0):
+def cpu_baseline(cfg, seconds_target=10.0, max_particles=None):
     """The fp64 oracle as it stands, on the host cores, on a bounded sample of
-    the same workload: a strided subset of the block's seeds advanced over the
-    first cycles of the interval."""
+    the same workload: the block's seeds (strided subset if max_particles)
+    advanced through whole intervals (reseeded each time) until about
+    `seconds_target` of CPU work has been done."""
     import lag_inputs as L
     import oracle
     g = cfg["grid"]
     block = L.decompose(g, cfg["layout"])[0]
-    cores = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    cores = int(os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1)))
     seeds = oracle.seeds(g, block.lo, block.hi, cfg["stride"])
-    ncyc = 5
-    sl = [L.field_at_nodes(cfg["field"], g, k * cfg["dt"]) for k in range(ncyc + 1)]
-    # calibrate on a small sample, then size for ~seconds_target
-    n0 = min(20000, seeds.shape[0])
-    it = oracle.Interval(g, block.lo, block.hi, cfg["stride"], g_seeds=seeds[:: max(1, seeds.shape[0] // n0)][:n0])
-    t0 = time.perf_counter()
-    it.cycle(sl[0], sl[1], cfg["dt"])
-    per = (time.perf_counter() - t0) / it.n
-    n = int(min(seeds.shape[0], max(n0, seconds_target / (per * ncyc))))
-    pick = seeds[:: max(1, seeds.shape[0] // n)][:n]
-    it = oracle.Interval(g, block.lo, block.hi, cfg["stride"], g_seeds=pick)
-    t0 = time.perf_counter()
-    for c in range(ncyc):
-        it.cycle(sl[c], sl[c + 1], cfg["dt"])
-    el = time.perf_counter() - t0
-    return {"value": it.n * ncyc / el, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]),
-            "kind": "oracle",
-            "sample": f"{it.n} of {seeds.shape[0]} seeds (strided) of the {cfg['name']} block, "
-                      f"{ncyc} cycles, fp64 C oracle with OpenMP; {el:.1f} s"}
+    if max_particles and seeds.shape[0] > max_particles:
+        seeds = seeds[:: seeds.shape[0] // max_particles][:max_particles]
+    ncyc = cfg["interval"]
+    sl = [L.field_at_nodes(cfg["field"], g, k * cfg["dt"], backend="torch").numpy()
+          for k in range(ncyc + 1)]
+    el, psteps, intervals = 0.0, 0, 0
+    while el < seconds_target and intervals < 50:
+        it = oracle.Interval(g, block.lo, block.hi, cfg["stride"], g_seeds=seeds)
+        t0 = time.perf_counter()
+        for c in range(ncyc):
+            psteps += it.active()
+            it.cycle(sl[c], sl[c + 1], cfg["dt"])
+        el += time.perf_counter() - t0
+        intervals += 1
+    return {"value": psteps / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{intervals} interval(s) of {ncyc} cycles over {seeds.shape[0]} seeds of the "
+                      f"{cfg['name']} block (fp64 C oracle, OpenMP), {el:.1f} s of CPU work"}
 
 
 def reference_arm(args):
@@ -322,8 +329,9 @@ def reference_arm(args):
     import lag_inputs as L
     cfg = L.make_config(args.config, nranks=1)
     vals = []
+    budget = max(1.0, 90.0 / max(1, args.steps))
     for _ in range(max(1, args.steps)):
-        vals.append(cpu_baseline(cfg, seconds_target=max(2.0, 60.0 / max(1, args.steps + args.warmup))))
+        vals.append(cpu_baseline(cfg, seconds_target=budget))
     v = statistics.median(x["value"] for x in vals)
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
