@@ -199,7 +199,7 @@ def make_config(name: str, nranks: int = 1, scale: Optional[int] = None,
         nn = scale or 512
         h = 1.0 / (nn - 1)
         grid = Grid(3, (nn, nn, nn), (0.0, 0.0, 0.0), (h, h, h))
-        dt = 0.25 * (1.0 / 511)
+        dt = 0.25 * h
         spec = FieldSpec("nyx", params=_nyx_modes(), period=500 * dt)
         cfg = dict(grid=grid, layout=(2, 2, 2), field=spec, dt=dt, cycles=500, interval=10,
                    stride=4 if scale is None else max(1, min(4, nn // 32)))

@@ -6,6 +6,7 @@
 #include "lag.h"
 #include "lag_internal.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -324,6 +325,17 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
         a.hi[ax] = (int)ctx->cfg.block_hi[ax];
         a.base[ax] = ctx->base[ax];
         a.cmax[ax] = ctx->ext[ax] - 2;
+        {
+            // fast ranges of global cell indices
+            const int N = (int)ctx->cfg.global_nodes[ax], lo = (int)ctx->cfg.block_lo[ax], hi = (int)ctx->cfg.block_hi[ax];
+            const int btop = (hi < N ? hi - 1 : N - 2);                 // last valid cell in the block
+            const int gmin = std::max(ctx->base[ax], 0);
+            const int gtop = std::min(ctx->base[ax] + ctx->ext[ax] - 2, N - 2);
+            a.bmin[ax] = lo; a.bspan[ax] = btop - lo;
+            if (ctx->cfg.mode == LAG_BTO) { a.gmin[ax] = lo; a.gspan[ax] = btop - lo; }
+            else { a.gmin[ax] = gmin; a.gspan[ax] = gtop - gmin; }
+            if (ax >= D) { a.bmin[ax] = a.gmin[ax] = 0; a.bspan[ax] = a.gspan[ax] = 0; }
+        }
         const double dth = ax < D ? dt / ctx->cfg.spacing[ax] : 0.0;
         a.hdth[ax] = (float)(0.5 * dth);
         a.qdth[ax] = (float)(0.25 * dth);

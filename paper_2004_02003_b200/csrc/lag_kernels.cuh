@@ -36,6 +36,10 @@ struct AdvectArgs {
     int32_t lo[3], hi[3];           // block [lo, hi)
     int32_t base[3];                // global node index of slice element 0 (= lo - G)
     int32_t cmax[3];                // largest local cell index a gather may use (ext - 2)
+    // fast-path cell ranges (global cell index c): gathers [gmin, gmin + gspan],
+    // block membership [bmin, bmin + bspan]; anything else takes the slow path
+    int32_t gmin[3], gspan[3];
+    int32_t bmin[3], bspan[3];
     int32_t sx, sxy;                // slice pitch (nodes) of a row / a plane
     float hdth[3], qdth[3], sdth[3];// dt/h * (1/2, 1/4, 1/6)
     uint32_t bx, by;                // packed seed-node bit widths (x, y)
@@ -86,7 +90,8 @@ __device__ __forceinline__ void gather(const float* __restrict__ v, const int li
     }
 }
 
-// Multilinear interpolation inside one cell with fractional offsets f.
+// Multilinear interpolation inside one cell with fractional offsets f
+// (two partial sums per component for ILP).
 template <int DIM>
 __device__ __forceinline__ void interp(const float* C, const float f[3], float out[3]) {
     if constexpr (DIM == 3) {
@@ -99,10 +104,13 @@ __device__ __forceinline__ void interp(const float* C, const float f[3], float o
         w[6] = ux * w11; w[7] = f[0] * w11;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            float s = w[0] * C[c];
+            float s0 = w[0] * C[c], s1 = w[1] * C[3 + c];
 #pragma unroll
-            for (int k = 1; k < 8; ++k) s = fmaf(w[k], C[k * 3 + c], s);
-            out[c] = s;
+            for (int k = 2; k < 8; k += 2) {
+                s0 = fmaf(w[k], C[k * 3 + c], s0);
+                s1 = fmaf(w[k + 1], C[(k + 1) * 3 + c], s1);
+            }
+            out[c] = s0 + s1;
         }
     } else {
         const float ux = 1.f - f[0], uy = 1.f - f[1];
@@ -118,39 +126,86 @@ __device__ __forceinline__ void interp(const float* C, const float f[3], float o
     }
 }
 
-// Locate a stage sample e (displacement from g, cell units).
-// Returns ST_VALID / ST_EXIT / ST_TERM; fills the interpolation cell (local)
-// and fractional offsets.  All boundary decisions are integer compares on the
-// cell index c = g + floor(e) (exact).
-template <int DIM, bool BTO>
-__device__ __forceinline__ uint8_t locate(const AdvectArgs& a, const int g[3], const float e[3],
-                                          int li[3], float f[3], bool& ghost_bad) {
-    bool out_dom = false, out_blk = false, gb = false;
+// Cell of a stage sample e (displacement from g, cell units):
+// c = g + floor(e), f = e - floor(e) (exact).  Fast path: every axis inside
+// the range [lo_, lo_ + span_] (one unsigned compare per axis).
+template <int DIM>
+__device__ __forceinline__ bool cells(const int g[3], const float e[3], const int32_t* rmin,
+                                      const int32_t* rspan, int c[3], float f[3]) {
+    bool ok = true;
 #pragma unroll
     for (int ax = 0; ax < DIM; ++ax) {
         const float fl = floorf(e[ax]);
-        float fr = e[ax] - fl;                       // exact
-        int c = g[ax] + __float2int_rz(fl);
-        // closed global domain [0, N-1] in index space
-        out_dom |= (c < 0) | (c > a.N[ax] - 1) | ((c == a.N[ax] - 1) & (fr != 0.f));
-        if constexpr (BTO)                           // half-open block, closed at the global top
-            out_blk |= (c < a.lo[ax]) | ((c >= a.hi[ax]) & (a.hi[ax] < a.N[ax]));
-        if (c == a.N[ax] - 1) { c = a.N[ax] - 2; fr = 1.f; }   // closed upper face: f = 1
-        int l = c - a.base[ax];
-        if constexpr (!BTO) gb |= (l < 0) | (l > a.cmax[ax]);
-        l = min(max(l, 0), a.cmax[ax]);              // never read outside the slice
-        li[ax] = l;
-        f[ax] = fr;
+        f[ax] = e[ax] - fl;                              // exact
+        c[ax] = g[ax] + __float2int_rz(fl);
+        ok &= (unsigned)(c[ax] - rmin[ax]) <= (unsigned)rspan[ax];
     }
-    if constexpr (DIM == 2) { li[2] = 0; f[2] = 0.f; }
-    const uint8_t st = out_dom ? ST_EXIT : (out_blk ? ST_TERM : ST_VALID);
-    if constexpr (!BTO) ghost_bad |= gb & (st == ST_VALID);
-    return st;
+    if constexpr (DIM == 2) { c[2] = 0; f[2] = 0.f; }
+    return ok;
 }
 
-// The first failing stage decides the outcome (the oracle stops there).
-__device__ __forceinline__ uint8_t first_fail(uint8_t cur, uint8_t next) {
-    return cur != ST_VALID ? cur : next;
+// Slow path (a sample near a block or global face): full classification with
+// integer compares on the cell index.
+//   EXIT : outside the closed global domain [0, N-1]
+//   TERM : (BTO) outside the half-open block, closed at the global top
+//   VALID: inside; the closed upper face c = N-1, f = 0 is moved to
+//          c = N-2, f = 1 (same point, interpolation cell inside the grid);
+//          COMM flags a gather outside the ghost layers.
+template <int DIM, bool BTO>
+__device__ __forceinline__ uint8_t classify_slow(const AdvectArgs& a, int c[3], float f[3],
+                                              bool& ghost_bad) {
+    bool out_dom = false, out_blk = false;
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) {
+        out_dom |= (c[ax] < 0) | (c[ax] > a.N[ax] - 1) | ((c[ax] == a.N[ax] - 1) & (f[ax] != 0.f));
+        if constexpr (BTO)
+            out_blk |= (c[ax] < a.lo[ax]) | ((c[ax] >= a.hi[ax]) & (a.hi[ax] < a.N[ax]));
+    }
+    if (out_dom) return ST_EXIT;
+    if (out_blk) return ST_TERM;
+    bool gb = false;
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) {
+        if (c[ax] == a.N[ax] - 1) { c[ax] = a.N[ax] - 2; f[ax] = 1.f; }
+        const int l = c[ax] - a.base[ax];
+        gb |= (l < 0) | (l > a.cmax[ax]);
+    }
+    if (gb) {                                            // COMM only: CFL >= 1 in a stage
+        ghost_bad = true;
+        return ST_EXIT;
+    }
+    return ST_VALID;
+}
+
+template <int DIM>
+__device__ __forceinline__ int node_index(const AdvectArgs& a, const int c[3]) {
+    const int lx = c[0] - a.base[0], ly = c[1] - a.base[1];
+    if constexpr (DIM == 3) return lx + a.sx * ly + a.sxy * (c[2] - a.base[2]);
+    else return lx + a.sx * ly;
+}
+
+// Corner gather by linear node index (see gather()).
+template <int DIM>
+__device__ __forceinline__ void gather_idx(const float* __restrict__ v, int idx, int sx, int sxy,
+                                           float* C) {
+    if constexpr (DIM == 3) {
+        const float* p = v + 3 * idx;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int dy = r & 1, dz = r >> 1;
+            const float* q = p + 3 * (dy * sx + dz * sxy);
+#pragma unroll
+            for (int e = 0; e < 6; ++e) C[r * 6 + e] = __ldg(q + e);
+        }
+    } else {
+        const float* p = v + 2 * idx;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const float* q = p + 2 * (r * sx);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) C[r * 4 + e] = __ldg(q + e);
+        }
+    }
 }
 
 template <int DIM, bool BTO>
@@ -165,30 +220,37 @@ advect_kernel(const AdvectArgs a) {
     unsigned long long steps = 0, nterm = 0, nexit = 0, nsent = 0;
     uint32_t errbits = 0;
 
-    for (int tile = warp; tile < n_tiles; tile += nwarps) {
-        const int cnt = a.tile_count[tile];
-        if (cnt == 0) continue;
+    // software pipeline: the next tile's count and records are in flight while
+    // the current tile computes
+    int tile = warp;
+    int cnt = tile < n_tiles ? a.tile_count[tile] : 0;
+    float4 r = tile < n_tiles ? a.state[(size_t)tile * kTile + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+
+    while (tile < n_tiles) {
+        const int ntile = tile + nwarps;
+        const int ncnt = ntile < n_tiles ? a.tile_count[ntile] : 0;
+        const float4 nr = ntile < n_tiles ? a.state[(size_t)ntile * kTile + lane]
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (cnt == 0) { tile = ntile; cnt = ncnt; r = nr; continue; }
         const bool live = lane < cnt;
         float4* trec = a.state + (size_t)tile * kTile;
-        float4 r = live ? trec[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
         int g[3];
         unpack_g(__float_as_uint(r.w), a, g);
         const float d[3] = {r.x, r.y, DIM == 3 ? r.z : 0.f};
 
         float S[NC], B[NC];
-        int cur[3], li[3];
+        int c[3];
         float f[3], e[3];
         bool ghost_bad = false;
         uint8_t st = ST_VALID;
 
-        // ---- stage 1: q1 = x (already validated when committed) ----
-        locate<DIM, BTO>(a, g, d, li, f, ghost_bad);
-        if (live) {
-            gather<DIM>(a.v0, li, a.sx, a.sxy, S);
-            gather<DIM>(a.v1, li, a.sx, a.sxy, B);
-        }
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) cur[ax] = li[ax];
+        // ---- stage 1: q1 = x (validated when committed) ----
+        if (!cells<DIM>(g, d, a.gmin, a.gspan, c, f) && live)
+            classify_slow<DIM, BTO>(a, c, f, ghost_bad);   // top-face clamp only
+        int cur = node_index<DIM>(a, c);
+        if (!live) cur = 0;
+        gather_idx<DIM>(a.v0, cur, a.sx, a.sxy, S);
+        gather_idx<DIM>(a.v1, cur, a.sx, a.sxy, B);
         float k1[3];
         interp<DIM>(S, f, k1);
 #pragma unroll
@@ -197,14 +259,17 @@ advect_kernel(const AdvectArgs a) {
         // ---- stage 2: q2 = x + dt/2 k1, alpha = 1/2 ----
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], k1[ax], d[ax]);
-        st = first_fail(st, locate<DIM, BTO>(a, g, e, li, f, ghost_bad));
-        if (live && st == ST_VALID && (li[0] != cur[0] || li[1] != cur[1] || li[2] != cur[2])) {
-            gather<DIM>(a.v0, li, a.sx, a.sxy, S);
-            gather<DIM>(a.v1, li, a.sx, a.sxy, B);
+        if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live)
+            st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
+        {
+            const int idx = node_index<DIM>(a, c);
+            if (live && st == ST_VALID && idx != cur) {
+                gather_idx<DIM>(a.v0, idx, a.sx, a.sxy, S);
+                gather_idx<DIM>(a.v1, idx, a.sx, a.sxy, B);
 #pragma unroll
-            for (int i = 0; i < NC; ++i) S[i] += B[i];
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) cur[ax] = li[ax];
+                for (int i = 0; i < NC; ++i) S[i] += B[i];
+                cur = idx;
+            }
         }
         float T2[3];
         interp<DIM>(S, f, T2);                          // T2 = 2 k2
@@ -212,14 +277,17 @@ advect_kernel(const AdvectArgs a) {
         // ---- stage 3: q3 = x + dt/2 k2 = x + dt/4 T2, alpha = 1/2 ----
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.qdth[ax], T2[ax], d[ax]);
-        st = first_fail(st, locate<DIM, BTO>(a, g, e, li, f, ghost_bad));
-        if (live && st == ST_VALID && (li[0] != cur[0] || li[1] != cur[1] || li[2] != cur[2])) {
-            gather<DIM>(a.v0, li, a.sx, a.sxy, S);
-            gather<DIM>(a.v1, li, a.sx, a.sxy, B);
+        if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live && st == ST_VALID)
+            st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
+        {
+            const int idx = node_index<DIM>(a, c);
+            if (live && st == ST_VALID && idx != cur) {
+                gather_idx<DIM>(a.v0, idx, a.sx, a.sxy, S);
+                gather_idx<DIM>(a.v1, idx, a.sx, a.sxy, B);
 #pragma unroll
-            for (int i = 0; i < NC; ++i) S[i] += B[i];
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) cur[ax] = li[ax];
+                for (int i = 0; i < NC; ++i) S[i] += B[i];
+                cur = idx;
+            }
         }
         float T3[3];
         interp<DIM>(S, f, T3);                          // T3 = 2 k3
@@ -227,9 +295,11 @@ advect_kernel(const AdvectArgs a) {
         // ---- stage 4: q4 = x + dt k3 = x + dt/2 T3, alpha = 1 ----
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], T3[ax], d[ax]);
-        st = first_fail(st, locate<DIM, BTO>(a, g, e, li, f, ghost_bad));
-        if (live && st == ST_VALID && (li[0] != cur[0] || li[1] != cur[1] || li[2] != cur[2])) {
-            gather<DIM>(a.v1, li, a.sx, a.sxy, B);
+        if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live && st == ST_VALID)
+            st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
+        {
+            const int idx = node_index<DIM>(a, c);
+            if (live && st == ST_VALID && idx != cur) gather_idx<DIM>(a.v1, idx, a.sx, a.sxy, B);
         }
         float k4[3];
         interp<DIM>(B, f, k4);
@@ -243,29 +313,37 @@ advect_kernel(const AdvectArgs a) {
         bool finite = true;
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) finite &= fabsf(dn[ax]) < 1.0e30f;
-        {
-            int lj[3]; float fj[3];
-            st = first_fail(st, locate<DIM, BTO>(a, g, dn, lj, fj, ghost_bad));
-        }
-        if (live && !finite) { errbits |= ERR_NONFINITE; st = ST_EXIT; }
-        if (live && ghost_bad) { errbits |= ERR_GHOST; if (st == ST_VALID) st = ST_EXIT; }
-
-        // ---- COMM: updated position in another block -> hand off ----
+        // membership of the updated position: fast = inside the block
         bool migrate = false;
         int nb = 0;
-        if constexpr (!BTO) {
-            if (live && st == ST_VALID) {
-                int mul = 1;
+        {
+            int cn[3];
+            float fn[3];
+            const bool inblk = cells<DIM>(g, dn, a.bmin, a.bspan, cn, fn);
+            if (!inblk && live && st == ST_VALID) {
+                bool gdummy = false;
+                if constexpr (BTO) {
+                    st = classify_slow<DIM, true>(a, cn, fn, gdummy);
+                } else {
+                    // COMM: in the domain but outside the block -> hand off
+                    bool out_dom = false;
+                    int mul = 1;
 #pragma unroll
-                for (int ax = 0; ax < DIM; ++ax) {
-                    const int c = g[ax] + __float2int_rz(floorf(dn[ax]));
-                    const int o = (c < a.lo[ax]) ? -1 : ((c >= a.hi[ax] && a.hi[ax] < a.N[ax]) ? 1 : 0);
-                    migrate |= (o != 0);
-                    nb += (o + 1) * mul;
-                    mul *= 3;
+                    for (int ax = 0; ax < DIM; ++ax) {
+                        out_dom |= (cn[ax] < 0) | (cn[ax] > a.N[ax] - 1) |
+                                   ((cn[ax] == a.N[ax] - 1) & (fn[ax] != 0.f));
+                        const int o = (cn[ax] < a.lo[ax]) ? -1
+                                      : ((cn[ax] >= a.hi[ax] && a.hi[ax] < a.N[ax]) ? 1 : 0);
+                        migrate |= (o != 0);
+                        nb += (o + 1) * mul;
+                        mul *= 3;
+                    }
+                    if (out_dom) { st = ST_EXIT; migrate = false; }
                 }
             }
         }
+        if (live && !finite) { errbits |= ERR_NONFINITE; st = ST_EXIT; migrate = false; }
+        if (live && ghost_bad) { errbits |= ERR_GHOST; if (st == ST_VALID) st = ST_EXIT; migrate = false; }
 
         // ---- particle management: compact survivors, record terminations ----
         const bool keep = live && st == ST_VALID && !migrate;
@@ -314,6 +392,7 @@ advect_kernel(const AdvectArgs a) {
             nterm += __popc(tmask);
             nexit += __popc(dmask) - __popc(tmask);
         }
+        tile = ntile; cnt = ncnt; r = nr;
     }
 
     // one atomic per CTA per counter

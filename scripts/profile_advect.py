@@ -11,6 +11,7 @@ import paper_2004_02003_b200 as P  # noqa: E402
 
 
 def main(config="C5", cycles=8):
+    cycles = int(cycles)
     cfg = L.make_config(config)
     g = cfg["grid"]
     b = L.decompose(g, cfg["layout"])[0]
@@ -32,4 +33,4 @@ def main(config="C5", cycles=8):
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["C5"]))
+    main(*(sys.argv[1:3] or ["C5"]))
