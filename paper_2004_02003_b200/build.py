@@ -36,8 +36,10 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Build liblag.so (or `out` with extra -D `defines`, for experiments)."""
+    lib = out or LIB
+    if out is None and not force and not _stale():
         return LIB
     inc, libdir = nccl_paths()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -45,7 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
            "-Xptxas", "-v" if verbose else "-O3",
-           "-o", LIB + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES] + \
+           *[f"-D{d}" for d in defines],
+           "-o", lib + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES] + \
           ["-L", libdir, "-l:libnccl.so.2", "-Xlinker", "-rpath", "-Xlinker", libdir]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -53,8 +56,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building liblag.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

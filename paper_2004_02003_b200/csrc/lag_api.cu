@@ -78,7 +78,7 @@ static lag_status validate(const lag_config* c) {
         const bool used = a < c->dim;
         const int64_t N = c->global_nodes[a];
         if (used) {
-            if (N < 2 || N > (int64_t(1) << 30)) { lag_set_error(ctx, "global_nodes[%d] = %lld must be in [2, 2^30]", a, (long long)N); return LAG_EINVAL; }
+            if (N < 2 || N >= (int64_t(1) << 22)) { lag_set_error(ctx, "global_nodes[%d] = %lld must be in [2, 2^22)", a, (long long)N); return LAG_EINVAL; }
             if (!(c->spacing[a] > 0.0) || !std::isfinite(c->spacing[a])) { lag_set_error(ctx, "spacing[%d] must be finite and > 0", a); return LAG_EINVAL; }
             if (!std::isfinite(c->origin[a])) { lag_set_error(ctx, "origin[%d] must be finite", a); return LAG_EINVAL; }
             if (!(0 <= c->block_lo[a] && c->block_lo[a] < c->block_hi[a] && c->block_hi[a] <= N)) {
@@ -353,9 +353,15 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
 
     const int tiles = ctx->cfg.mode == LAG_COMM ? ctx->cap_tiles : ctx->n_tiles;
     const int warps_per_block = kThreads / 32;
+    a.tiles_per_warp = kTilesPerWarp;
+#if LAG_ADV_PERSIST
     int blocks = (tiles + warps_per_block - 1) / warps_per_block;
     const int max_blocks = ctx->num_sms * ctx->advect_blocks_per_sm;
     if (blocks > max_blocks) blocks = max_blocks;
+#else
+    const int warps = (tiles + kTilesPerWarp - 1) / kTilesPerWarp;
+    int blocks = (warps + warps_per_block - 1) / warps_per_block;
+#endif
     if (blocks < 1) blocks = 1;
     if (D == 3) {
         if (ctx->cfg.mode == LAG_BTO) advect_kernel<3, true><<<blocks, kThreads, 0, ctx->stream>>>(a);

@@ -19,7 +19,24 @@
 namespace lag {
 
 constexpr int kTile = 32;
-constexpr int kThreads = 256;
+#ifndef LAG_ADV_THREADS
+#define LAG_ADV_THREADS 128
+#endif
+#ifndef LAG_ADV_MINB
+#define LAG_ADV_MINB 4
+#endif
+#ifndef LAG_ADV_TPW
+#define LAG_ADV_TPW 4
+#endif
+constexpr int kThreads = LAG_ADV_THREADS;     // advect CTA size
+constexpr int kMinBlocks = LAG_ADV_MINB;      // __launch_bounds__ min CTAs per SM
+constexpr int kTilesPerWarp = LAG_ADV_TPW;    // contiguous 32-particle tiles per warp
+#ifndef LAG_ADV_PERSIST
+#define LAG_ADV_PERSIST 1
+#endif
+#ifndef LAG_POLY
+#define LAG_POLY 0       // 1: polynomial-form trilinear (coefficients per corner set)
+#endif
 
 enum : uint32_t { ERR_OVERFLOW = 1u, ERR_GHOST = 2u, ERR_NONFINITE = 4u };
 enum : int { CNT_STEPS = 0, CNT_TERM = 1, CNT_EXIT = 2, CNT_SENT = 3, CNT_RECV = 4, CNT_N = 8 };
@@ -52,6 +69,7 @@ struct AdvectArgs {
     unsigned long long* counters;   // CNT_*
     uint32_t* err;
     int32_t cycle;
+    int32_t tiles_per_warp;         // contiguous tiles per warp (non-persistent grid)
     // COMM: outgoing slots, one per neighbour offset (3^dim):
     // slot k = slot_rec[slot_base[k]] = header (u32 count) then slot_capv[k] records
     float4* slot_rec;
@@ -126,6 +144,71 @@ __device__ __forceinline__ void interp(const float* C, const float f[3], float o
     }
 }
 
+// Trilinear polynomial form of one cell's corners (in place, per component):
+//   Tri(f) = p0 + fx (px + fy (pxy + fz pxyz) + fz pxz) + fy (py + fz pyz) + fz pz
+// Built once per gathered corner set (off the stage-to-stage critical path);
+// each evaluation is then 7 FFMA per component with a 4-deep chain.  Linear
+// in the corner values, so coefficients of v_t + v_t1 are the sums.
+template <int DIM>
+__device__ __forceinline__ void to_poly(float* C) {
+    if constexpr (!LAG_POLY) return;
+    if constexpr (DIM == 3) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float v000 = C[0 * 3 + c], v100 = C[1 * 3 + c], v010 = C[2 * 3 + c], v110 = C[3 * 3 + c];
+            const float v001 = C[4 * 3 + c], v101 = C[5 * 3 + c], v011 = C[6 * 3 + c], v111 = C[7 * 3 + c];
+            const float px = v100 - v000, py = v010 - v000, pz = v001 - v000;
+            const float d1 = v110 - v010, d2 = v101 - v001, d3 = v011 - v001, d4 = v111 - v011;
+            const float pxy = d1 - px;
+            C[0 * 3 + c] = v000;
+            C[1 * 3 + c] = px;
+            C[2 * 3 + c] = py;
+            C[3 * 3 + c] = pxy;
+            C[4 * 3 + c] = pz;
+            C[5 * 3 + c] = d2 - px;              // pxz
+            C[6 * 3 + c] = d3 - py;              // pyz
+            C[7 * 3 + c] = (d4 - d2) - pxy;      // pxyz
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const float v00 = C[0 * 2 + c], v10 = C[1 * 2 + c], v01 = C[2 * 2 + c], v11 = C[3 * 2 + c];
+            const float px = v10 - v00, py = v01 - v00;
+            C[1 * 2 + c] = px;
+            C[2 * 2 + c] = py;
+            C[3 * 2 + c] = (v11 - v01) - px;     // pxy
+        }
+    }
+}
+
+template <int DIM>
+__device__ __forceinline__ void interp(const float* C, const float f[3], float out[3]);
+
+template <int DIM>
+__device__ __forceinline__ void poly_eval(const float* P, const float f[3], float out[3]) {
+    if constexpr (!LAG_POLY) { interp<DIM>(P, f, out); return; }
+    if constexpr (DIM == 3) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float a = fmaf(f[2], P[7 * 3 + c], P[3 * 3 + c]);   // pxy + fz pxyz
+            float b = fmaf(f[1], a, P[1 * 3 + c]);                    // px + fy (...)
+            b = fmaf(f[2], P[5 * 3 + c], b);                          //    + fz pxz
+            const float t = fmaf(f[2], P[6 * 3 + c], P[2 * 3 + c]);   // py + fz pyz
+            float r = fmaf(f[2], P[4 * 3 + c], P[0 * 3 + c]);         // p0 + fz pz
+            r = fmaf(f[1], t, r);
+            out[c] = fmaf(f[0], b, r);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const float b = fmaf(f[1], P[3 * 2 + c], P[1 * 2 + c]);   // px + fy pxy
+            const float r = fmaf(f[1], P[2 * 2 + c], P[0 * 2 + c]);   // p0 + fy py
+            out[c] = fmaf(f[0], b, r);
+        }
+        out[2] = 0.f;
+    }
+}
+
 // Cell of a stage sample e (displacement from g, cell units):
 // c = g + floor(e), f = e - floor(e) (exact).  Fast path: every axis inside
 // the range [lo_, lo_ + span_] (one unsigned compare per axis).
@@ -137,7 +220,9 @@ __device__ __forceinline__ bool cells(const int g[3], const float e[3], const in
     for (int ax = 0; ax < DIM; ++ax) {
         const float fl = floorf(e[ax]);
         f[ax] = e[ax] - fl;                              // exact
-        c[ax] = g[ax] + __float2int_rz(fl);
+        // int(fl) without the XU pipe: |fl| < 2^22, so fl + 1.5*2^23 is exact
+        // and its low mantissa bits are the two's-complement integer
+        c[ax] = g[ax] + (__float_as_int(fl + 12582912.0f) - 0x4B400000);
         ok &= (unsigned)(c[ax] - rmin[ax]) <= (unsigned)rspan[ax];
     }
     if constexpr (DIM == 2) { c[2] = 0; f[2] = 0.f; }
@@ -188,6 +273,11 @@ __device__ __forceinline__ int node_index(const AdvectArgs& a, const int c[3]) {
 template <int DIM>
 __device__ __forceinline__ void gather_idx(const float* __restrict__ v, int idx, int sx, int sxy,
                                            float* C) {
+#ifdef LAG_EXP_NOLOAD   // timing experiment: synthetic corners, no velocity traffic
+#pragma unroll
+    for (int i = 0; i < (1 << DIM) * DIM; ++i) C[i] = __int_as_float(idx + i) * 1e-30f;
+    return;
+#endif
     if constexpr (DIM == 3) {
         const float* p = v + 3 * idx;
 #pragma unroll
@@ -209,25 +299,38 @@ __device__ __forceinline__ void gather_idx(const float* __restrict__ v, int idx,
 }
 
 template <int DIM, bool BTO>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
 advect_kernel(const AdvectArgs a) {
     constexpr int NC = (1 << DIM) * DIM;             // corner floats per slice
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * kThreads) >> 5;
-    const int n_tiles = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
+    const int n_tiles_all = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
+    // non-persistent grid: warp w owns tiles [w*tpw, (w+1)*tpw) (contiguous, so
+    // a CTA's particles are spatial neighbours); the block scheduler balances
+    // the load across SMs
+#if LAG_ADV_PERSIST
+    // persistent grid: warp w owns tiles w, w + W, w + 2W, ... (W = all warps),
+    // so the GPU sweeps the particle list as one compact window
+    const int tile0 = warp;
+    const int tstride = (gridDim.x * kThreads) >> 5;
+    const int n_tiles = n_tiles_all;
+#else
+    const int tile0 = warp * a.tiles_per_warp;
+    const int tstride = 1;
+    const int n_tiles = min(n_tiles_all, tile0 + a.tiles_per_warp);
+#endif
 
     unsigned long long steps = 0, nterm = 0, nexit = 0, nsent = 0;
     uint32_t errbits = 0;
 
     // software pipeline: the next tile's count and records are in flight while
     // the current tile computes
-    int tile = warp;
+    int tile = tile0;
     int cnt = tile < n_tiles ? a.tile_count[tile] : 0;
     float4 r = tile < n_tiles ? a.state[(size_t)tile * kTile + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
 
     while (tile < n_tiles) {
-        const int ntile = tile + nwarps;
+        const int ntile = tile + tstride;
         const int ncnt = ntile < n_tiles ? a.tile_count[ntile] : 0;
         const float4 nr = ntile < n_tiles ? a.state[(size_t)ntile * kTile + lane]
                                           : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -251,8 +354,10 @@ advect_kernel(const AdvectArgs a) {
         if (!live) cur = 0;
         gather_idx<DIM>(a.v0, cur, a.sx, a.sxy, S);
         gather_idx<DIM>(a.v1, cur, a.sx, a.sxy, B);
+        to_poly<DIM>(S);
+        to_poly<DIM>(B);
         float k1[3];
-        interp<DIM>(S, f, k1);
+        poly_eval<DIM>(S, f, k1);
 #pragma unroll
         for (int i = 0; i < NC; ++i) S[i] += B[i];       // S = v0 + v1 (stages 2, 3)
 
@@ -263,16 +368,22 @@ advect_kernel(const AdvectArgs a) {
             st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
         {
             const int idx = node_index<DIM>(a, c);
+#ifdef LAG_EXP_NORELOAD
+            if (false) {
+#else
             if (live && st == ST_VALID && idx != cur) {
+#endif
                 gather_idx<DIM>(a.v0, idx, a.sx, a.sxy, S);
                 gather_idx<DIM>(a.v1, idx, a.sx, a.sxy, B);
+                to_poly<DIM>(S);
+                to_poly<DIM>(B);
 #pragma unroll
                 for (int i = 0; i < NC; ++i) S[i] += B[i];
                 cur = idx;
             }
         }
         float T2[3];
-        interp<DIM>(S, f, T2);                          // T2 = 2 k2
+        poly_eval<DIM>(S, f, T2);                          // T2 = 2 k2
 
         // ---- stage 3: q3 = x + dt/2 k2 = x + dt/4 T2, alpha = 1/2 ----
 #pragma unroll
@@ -281,16 +392,22 @@ advect_kernel(const AdvectArgs a) {
             st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
         {
             const int idx = node_index<DIM>(a, c);
+#ifdef LAG_EXP_NORELOAD
+            if (false) {
+#else
             if (live && st == ST_VALID && idx != cur) {
+#endif
                 gather_idx<DIM>(a.v0, idx, a.sx, a.sxy, S);
                 gather_idx<DIM>(a.v1, idx, a.sx, a.sxy, B);
+                to_poly<DIM>(S);
+                to_poly<DIM>(B);
 #pragma unroll
                 for (int i = 0; i < NC; ++i) S[i] += B[i];
                 cur = idx;
             }
         }
         float T3[3];
-        interp<DIM>(S, f, T3);                          // T3 = 2 k3
+        poly_eval<DIM>(S, f, T3);                          // T3 = 2 k3
 
         // ---- stage 4: q4 = x + dt k3 = x + dt/2 T3, alpha = 1 ----
 #pragma unroll
@@ -299,10 +416,15 @@ advect_kernel(const AdvectArgs a) {
             st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
         {
             const int idx = node_index<DIM>(a, c);
-            if (live && st == ST_VALID && idx != cur) gather_idx<DIM>(a.v1, idx, a.sx, a.sxy, B);
+#ifndef LAG_EXP_NORELOAD
+            if (live && st == ST_VALID && idx != cur) {
+                gather_idx<DIM>(a.v1, idx, a.sx, a.sxy, B);
+                to_poly<DIM>(B);
+            }
+#endif
         }
         float k4[3];
-        interp<DIM>(B, f, k4);
+        poly_eval<DIM>(B, f, k4);
 
         // ---- update: x' = x + dt/6 (k1 + 2k2 + 2k3 + k4) ----
         float dn[3];
@@ -312,7 +434,7 @@ advect_kernel(const AdvectArgs a) {
         if constexpr (DIM == 2) dn[2] = 0.f;
         bool finite = true;
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) finite &= fabsf(dn[ax]) < 1.0e30f;
+        for (int ax = 0; ax < DIM; ++ax) finite &= fabsf(dn[ax]) < 4194304.f;   // 2^22 cells
         // membership of the updated position: fast = inside the block
         bool migrate = false;
         int nb = 0;
@@ -395,26 +517,15 @@ advect_kernel(const AdvectArgs a) {
         tile = ntile; cnt = ncnt; r = nr;
     }
 
-    // one atomic per CTA per counter
-    __shared__ unsigned long long s_cnt[4];
-    __shared__ uint32_t s_err;
-    if (threadIdx.x == 0) { s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0; s_err = 0; }
-    __syncthreads();
+    // one atomic per warp per counter (no CTA barrier: finished warps retire)
     if (lane == 0 && steps) {
-        atomicAdd(&s_cnt[0], steps);
-        if (nterm) atomicAdd(&s_cnt[1], nterm);
-        if (nexit) atomicAdd(&s_cnt[2], nexit);
-        if (nsent) atomicAdd(&s_cnt[3], nsent);
+        atomicAdd(&a.counters[CNT_STEPS], steps);
+        if (nterm) atomicAdd(&a.counters[CNT_TERM], nterm);
+        if (nexit) atomicAdd(&a.counters[CNT_EXIT], nexit);
+        if (nsent) atomicAdd(&a.counters[CNT_SENT], nsent);
     }
-    if (errbits) atomicOr(&s_err, errbits);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (s_cnt[0]) atomicAdd(&a.counters[CNT_STEPS], s_cnt[0]);
-        if (s_cnt[1]) atomicAdd(&a.counters[CNT_TERM], s_cnt[1]);
-        if (s_cnt[2]) atomicAdd(&a.counters[CNT_EXIT], s_cnt[2]);
-        if (s_cnt[3]) atomicAdd(&a.counters[CNT_SENT], s_cnt[3]);
-        if (s_err) atomicOr(a.err, s_err);
-    }
+    errbits = __reduce_or_sync(0xffffffffu, errbits);
+    if (lane == 0 && errbits) atomicOr(a.err, errbits);
 }
 
 // ---------------------------------------------------------------------------
