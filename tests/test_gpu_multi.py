@@ -1,0 +1,31 @@
+"""Multi-GPU parity (needs >= 2 GPUs; launched through torchrun).  The COMM
+baseline over NCCL must equal the single-block run bitwise (decomposition
+invariance) and match the fp64 oracle; BTO per rank vs the oracle."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("nproc,config,scale", [(2, "C2", 33), (2, "C5", 20), (4, "C2", 41), (8, "C4", 65)])
+def test_mgpu_comm_and_bto(nproc, config, scale):
+    if _ngpu() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + nproc),
+           os.path.join(ROOT, "scripts", "mgpu_check.py"), config, str(scale)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
+    rep = json.loads(lines[-1])
+    assert rep["ok"] and rep["sent"] > 0 and rep["comm_vs_single_bitwise_mismatching_arrays"] == 0
