@@ -46,11 +46,11 @@ def run_block(cfg, block, layout, rank, world, mode, slices, stride, nccl_id=Non
     n = ctx.seed(stride)
     for k in range(len(dev) - 1):
         ctx.advect(dev[k], dev[k + 1], cfg["dt"])
-    st_mid = ctx.stats()
     start = torch.empty((n, g.dim), dtype=torch.float64, device="cuda")
     end = torch.empty_like(start)
     status = torch.empty((n,), dtype=torch.uint8, device="cuda")
     ctx.extract(start, end, status, flags=P.LAG_NO_RESEED)
+    st_mid = ctx.stats()        # after extract: the last cycle's hand-offs were flushed
     ctx.close()
     return start.cpu().numpy(), end.cpu().numpy(), status.cpu().numpy(), st_mid
 
