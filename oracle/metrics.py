@@ -108,13 +108,20 @@ def barycentric_interpolate(points: np.ndarray, values: np.ndarray, queries: np.
     return out, inside
 
 
+def _recon_tile(args):
+    pts_start, pts_end, q = args
+    return barycentric_interpolate(pts_start, pts_end, q)
+
+
 def reconstruct_holes(g_seeds: np.ndarray, start: np.ndarray, end: np.ndarray,
                       valid: np.ndarray, hole: np.ndarray, stride: int,
-                      margin: int = 4, tile: int = 16):
+                      margin: int = 3, tile: int = 16, workers: int = 0):
     """Reconstruct end positions for `hole` seeds from the valid basis flows
     around them (own + adjacent blocks: with the global seed set the union is
-    the same).  Spatial tiles of `tile` lattice steps, each
-    triangulating the valid seeds within `margin` lattice steps of the tile.
+    the same).  Holes are grouped in spatial tiles of `tile`
+    lattice steps; each tile triangulates the valid seeds inside the bounding
+    box of its holes grown by `margin` lattice steps (reading R12).  Tiles are
+    independent and run in parallel over `workers` processes (0 = all cores).
     Returns (recon [n, dim] with NaN where not reconstructed, inside mask)."""
     g = np.asarray(g_seeds) // stride
     dim = start.shape[1]
@@ -125,17 +132,32 @@ def reconstruct_holes(g_seeds: np.ndarray, start: np.ndarray, end: np.ndarray,
         return recon, inside
     tkey = g[hidx, :dim] // tile
     uniq, inv = np.unique(tkey, axis=0, return_inverse=True)
+    inv = inv.ravel()
+    # valid seeds indexed on the lattice for fast box queries
+    shape = tuple(int(x) + 1 for x in g[:, :dim].max(axis=0))
+    lattice = np.full(shape, -1, dtype=np.int64)
     vidx = np.nonzero(valid)[0]
-    gv = g[vidx, :dim]
+    lattice[tuple(g[vidx, a] for a in range(dim))] = vidx
+    jobs, sels = [], []
     for t in range(uniq.shape[0]):
-        hsel = hidx[inv.ravel() == t]
-        lo = uniq[t] * tile - margin
-        hi = (uniq[t] + 1) * tile + margin
-        m = np.all((gv >= lo) & (gv < hi), axis=1)
-        pts = vidx[m]
+        hsel = hidx[inv == t]
+        lo = np.maximum(g[hsel, :dim].min(axis=0) - margin, 0)
+        hi = np.minimum(g[hsel, :dim].max(axis=0) + margin + 1, shape)
+        box = lattice[tuple(slice(int(lo[a]), int(hi[a])) for a in range(dim))].ravel()
+        pts = box[box >= 0]
         if pts.size < dim + 1:
             continue
-        vals, ins = barycentric_interpolate(start[pts], end[pts], start[hsel])
+        jobs.append((start[pts], end[pts], start[hsel]))
+        sels.append(hsel)
+    if workers == 1 or len(jobs) < 4:
+        results = [_recon_tile(j) for j in jobs]
+    else:
+        import multiprocessing as mp
+        import os
+        n = workers or os.cpu_count() or 1
+        with mp.get_context("fork").Pool(n) as pool:
+            results = pool.map(_recon_tile, jobs, chunksize=max(1, len(jobs) // (4 * n)))
+    for hsel, (vals, ins) in zip(sels, results):
         recon[hsel] = vals
         inside[hsel] = ins
     return recon, inside
