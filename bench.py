@@ -442,7 +442,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(cfg["name"]),
                          "kernel": "advect_kernel<3,true>", "peak_source": peak_src,
-                         "alg_bytes_per_launch": alg_bytes / cycles},
+                         "alg_bytes_per_launch": alg_bytes / cycles,
+                         "kernel_share_of_step": adv_ms / dev_ms},
             "comm": comm,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -155,7 +155,8 @@ def reconstruct_holes(g_seeds: np.ndarray, start: np.ndarray, end: np.ndarray,
         import multiprocessing as mp
         import os
         n = workers or os.cpu_count() or 1
-        with mp.get_context("fork").Pool(n) as pool:
+        # spawn, not fork: the caller may hold CUDA / thread-pool locks
+        with mp.get_context("spawn").Pool(n) as pool:
             results = pool.map(_recon_tile, jobs, chunksize=max(1, len(jobs) // (4 * n)))
     for hsel, (vals, ins) in zip(sels, results):
         recon[hsel] = vals

@@ -269,6 +269,90 @@ __device__ __forceinline__ int node_index(const AdvectArgs& a, const int c[3]) {
     else return lx + a.sx * ly;
 }
 
+// ---------------------------------------------------------------------------
+// Packed fp32x2 (Blackwell FFMA2 / FMUL2 / FADD2): the corner cache holds, per
+// corner row (dy, dz) and component c, the pair {V(x0).c, V(x0+1).c} of the
+// row's two x-neighbour nodes in one 64-bit register pair, so one packed
+// instruction serves two corners (half the FP issue slots of scalar code).
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+    f2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(f2_t r, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+    f2_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+    f2_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// number of corner pairs per slice: rows (2^(DIM-1)) x components (DIM)
+template <int DIM> struct Pairs { static constexpr int n = (1 << (DIM - 1)) * DIM; };
+
+// Gather the 2^DIM corners of local node idx (cell origin) into pairs:
+// P[row * DIM + c] = {V(row, x0).c, V(row, x0 + 1).c}, row = dy + 2 dz.
+template <int DIM>
+__device__ __forceinline__ void gather_pairs(const float* __restrict__ v, int idx, int sx, int sxy,
+                                             f2_t* P) {
+#ifdef LAG_EXP_NOLOAD   // timing experiment: synthetic corners, no velocity traffic
+#pragma unroll
+    for (int i = 0; i < Pairs<DIM>::n; ++i)
+        P[i] = f2_pack(__int_as_float(idx + i) * 1e-30f, __int_as_float(idx - i) * 1e-30f);
+    return;
+#endif
+    const float* p = v + DIM * idx;
+#pragma unroll
+    for (int r = 0; r < (1 << (DIM - 1)); ++r) {
+        const int dy = r & 1, dz = r >> 1;
+        const float* q = p + DIM * (dy * sx + dz * sxy);
+        float e[2 * DIM];
+#pragma unroll
+        for (int k = 0; k < 2 * DIM; ++k) e[k] = __ldg(q + k);
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) P[r * DIM + c] = f2_pack(e[c], e[DIM + c]);
+    }
+}
+
+// Trilinear (bilinear) interpolation from the pair cache at fractions f.
+template <int DIM>
+__device__ __forceinline__ void interp_pairs(const f2_t* P, const float f[3], float out[3]) {
+    const f2_t U = f2_pack(1.f - f[0], f[0]);            // x weights {1-fx, fx}
+    constexpr int R = 1 << (DIM - 1);
+    float wr[R];                                          // row weights
+    if constexpr (DIM == 3) {
+        const float uy = 1.f - f[1], uz = 1.f - f[2];
+        wr[0] = uy * uz; wr[1] = f[1] * uz; wr[2] = uy * f[2]; wr[3] = f[1] * f[2];
+    } else {
+        wr[0] = 1.f - f[1]; wr[1] = f[1];
+    }
+    f2_t W[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) W[r] = f2_mul(U, f2_pack(wr[r], wr[r]));   // broadcast operand
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        f2_t acc = f2_mul(W[0], P[c]);
+#pragma unroll
+        for (int r = 1; r < R; ++r) acc = f2_fma(W[r], P[r * DIM + c], acc);
+        float lo, hi;
+        f2_unpack(acc, lo, hi);
+        out[c] = lo + hi;
+    }
+    if constexpr (DIM == 2) out[2] = 0.f;
+}
+
 // Corner gather by linear node index (see gather()).
 template <int DIM>
 __device__ __forceinline__ void gather_idx(const float* __restrict__ v, int idx, int sx, int sxy,
@@ -341,7 +425,8 @@ advect_kernel(const AdvectArgs a) {
         unpack_g(__float_as_uint(r.w), a, g);
         const float d[3] = {r.x, r.y, DIM == 3 ? r.z : 0.f};
 
-        float S[NC], B[NC];
+        constexpr int NP = Pairs<DIM>::n;
+        f2_t S[NP], B[NP];
         int c[3];
         float f[3], e[3];
         bool ghost_bad = false;
@@ -352,14 +437,12 @@ advect_kernel(const AdvectArgs a) {
             classify_slow<DIM, BTO>(a, c, f, ghost_bad);   // top-face clamp only
         int cur = node_index<DIM>(a, c);
         if (!live) cur = 0;
-        gather_idx<DIM>(a.v0, cur, a.sx, a.sxy, S);
-        gather_idx<DIM>(a.v1, cur, a.sx, a.sxy, B);
-        to_poly<DIM>(S);
-        to_poly<DIM>(B);
+        gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
+        gather_pairs<DIM>(a.v1, cur, a.sx, a.sxy, B);
         float k1[3];
-        poly_eval<DIM>(S, f, k1);
+        interp_pairs<DIM>(S, f, k1);
 #pragma unroll
-        for (int i = 0; i < NC; ++i) S[i] += B[i];       // S = v0 + v1 (stages 2, 3)
+        for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);   // S = v0 + v1 (stages 2, 3)
 
         // ---- stage 2: q2 = x + dt/2 k1, alpha = 1/2 ----
 #pragma unroll
@@ -373,17 +456,15 @@ advect_kernel(const AdvectArgs a) {
 #else
             if (live && st == ST_VALID && idx != cur) {
 #endif
-                gather_idx<DIM>(a.v0, idx, a.sx, a.sxy, S);
-                gather_idx<DIM>(a.v1, idx, a.sx, a.sxy, B);
-                to_poly<DIM>(S);
-                to_poly<DIM>(B);
+                gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
+                gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
 #pragma unroll
-                for (int i = 0; i < NC; ++i) S[i] += B[i];
+                for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
                 cur = idx;
             }
         }
         float T2[3];
-        poly_eval<DIM>(S, f, T2);                          // T2 = 2 k2
+        interp_pairs<DIM>(S, f, T2);                          // T2 = 2 k2
 
         // ---- stage 3: q3 = x + dt/2 k2 = x + dt/4 T2, alpha = 1/2 ----
 #pragma unroll
@@ -397,17 +478,15 @@ advect_kernel(const AdvectArgs a) {
 #else
             if (live && st == ST_VALID && idx != cur) {
 #endif
-                gather_idx<DIM>(a.v0, idx, a.sx, a.sxy, S);
-                gather_idx<DIM>(a.v1, idx, a.sx, a.sxy, B);
-                to_poly<DIM>(S);
-                to_poly<DIM>(B);
+                gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
+                gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
 #pragma unroll
-                for (int i = 0; i < NC; ++i) S[i] += B[i];
+                for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
                 cur = idx;
             }
         }
         float T3[3];
-        poly_eval<DIM>(S, f, T3);                          // T3 = 2 k3
+        interp_pairs<DIM>(S, f, T3);                          // T3 = 2 k3
 
         // ---- stage 4: q4 = x + dt k3 = x + dt/2 T3, alpha = 1 ----
 #pragma unroll
@@ -418,13 +497,12 @@ advect_kernel(const AdvectArgs a) {
             const int idx = node_index<DIM>(a, c);
 #ifndef LAG_EXP_NORELOAD
             if (live && st == ST_VALID && idx != cur) {
-                gather_idx<DIM>(a.v1, idx, a.sx, a.sxy, B);
-                to_poly<DIM>(B);
+                gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
             }
 #endif
         }
         float k4[3];
-        poly_eval<DIM>(B, f, k4);
+        interp_pairs<DIM>(B, f, k4);
 
         // ---- update: x' = x + dt/6 (k1 + 2k2 + 2k3 + k4) ----
         float dn[3];
