@@ -119,7 +119,6 @@ typedef struct {
     int64_t received;        /* this interval: particles received from other ranks (COMM)   */
     int64_t particle_steps;  /* cumulative RK4 particle-steps since lag_init                */
     int64_t cycles;          /* cumulative lag_advect_cycle calls since lag_init            */
-    int64_t deferred;        /* cumulative particle-steps that took the general (slow) path */
     int32_t device_error;    /* latched async condition as a lag_status (0 = none)          */
     int32_t pad_;
 } lag_stats_t;

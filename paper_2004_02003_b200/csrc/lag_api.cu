@@ -207,7 +207,7 @@ extern "C" lag_status lag_destroy(lag_ctx ctx) {
 lag_status lag_reset_interval(lag_ctx_s* ctx) {
     // device words: [W_DEAD] dead count, [W_ERR] error bits, [W_NTILES] tile count (COMM)
     CK(cudaMemsetAsync(ctx->words, 0, kWords * sizeof(uint32_t), ctx->stream));
-    CK(cudaMemsetAsync(ctx->counters + CNT_TERM, 0, 4 * sizeof(unsigned long long), ctx->stream));   // TERM..RECV
+    CK(cudaMemsetAsync(ctx->counters + CNT_TERM, 0, 4 * sizeof(unsigned long long), ctx->stream));
     return LAG_OK;
 }
 
@@ -482,7 +482,6 @@ extern "C" lag_status lag_stats(lag_ctx ctx, lag_stats_t* out) {
     out->received = (int64_t)c[CNT_RECV];
     out->particle_steps = (int64_t)c[CNT_STEPS];
     out->cycles = ctx->cycles_total;
-    out->deferred = (int64_t)c[CNT_DEFER];
     out->active = out->seeded + out->received - out->sent - out->term_boundary - out->exit_domain;
     out->device_error = (int32_t)latched(ctx, ctx->host_words[W_ERR]);
     return LAG_OK;

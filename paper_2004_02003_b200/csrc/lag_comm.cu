@@ -249,7 +249,6 @@ __global__ void route_kernel(RouteArgs a) {
         if (i < n_live) {
             if ((int)(i % kTile) >= a.tile_count[i / kTile]) continue;
             r = a.state[i];
-            if (__float_as_uint(r.x) == 0x7fc0dead) continue;   // placeholder slot
             info = 0u;
         } else {
             r = a.dead_rec[i - n_live];

@@ -39,7 +39,7 @@ constexpr int kTilesPerWarp = LAG_ADV_TPW;    // contiguous 32-particle tiles pe
 #endif
 
 enum : uint32_t { ERR_OVERFLOW = 1u, ERR_GHOST = 2u, ERR_NONFINITE = 4u };
-enum : int { CNT_STEPS = 0, CNT_TERM = 1, CNT_EXIT = 2, CNT_SENT = 3, CNT_RECV = 4, CNT_DEFER = 5, CNT_N = 8 };
+enum : int { CNT_STEPS = 0, CNT_TERM = 1, CNT_EXIT = 2, CNT_SENT = 3, CNT_RECV = 4, CNT_N = 8 };
 enum : uint8_t { ST_VALID = 0, ST_TERM = 1, ST_EXIT = 2 };
 
 struct AdvectArgs {
@@ -299,21 +299,6 @@ __device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
     return d;
 }
 
-// L1 prefetch of the corner rows of local node idx in both slices (no
-// registers; the next tile's stage-1 gather then hits L1).
-template <int DIM>
-__device__ __forceinline__ void prefetch_corners(const float* v0, const float* v1, int idx, int sx, int sxy) {
-#ifndef LAG_EXP_NOPREFETCH
-#pragma unroll
-    for (int r = 0; r < (1 << (DIM - 1)); ++r) {
-        const int dy = r & 1, dz = r >> 1;
-        const size_t off = (size_t)DIM * (idx + dy * sx + dz * sxy);
-        asm volatile("prefetch.global.L1 [%0];" :: "l"(v0 + off));
-        asm volatile("prefetch.global.L1 [%0];" :: "l"(v1 + off));
-    }
-#endif
-}
-
 // number of corner pairs per slice: rows (2^(DIM-1)) x components (DIM)
 template <int DIM> struct Pairs { static constexpr int n = (1 << (DIM - 1)) * DIM; };
 
@@ -397,227 +382,34 @@ __device__ __forceinline__ void gather_idx(const float* __restrict__ v, int idx,
     }
 }
 
-// ---------------------------------------------------------------------------
-// Per-lane result of one RK4 step.
-struct StepOut {
-    float dn[3];       // updated displacement (valid when st == ST_VALID)
-    uint8_t st;        // ST_VALID / ST_TERM / ST_EXIT
-    bool migrate;      // COMM: updated position in neighbour block nb
-    int nb;
-    uint32_t err;      // ERR_* bits
-};
-
-// Classification of an updated position dn (shared by both paths): BTO keeps
-// it iff it is inside the block; COMM keeps it inside the block, hands it to
-// the neighbour block otherwise, EXIT outside the domain.
-template <int DIM, bool BTO>
-__device__ __forceinline__ void classify_update(const AdvectArgs& a, const int g[3], StepOut& o) {
-    bool finite = true;
-#pragma unroll
-    for (int ax = 0; ax < DIM; ++ax) finite &= fabsf(o.dn[ax]) < 4194304.f;   // 2^22 cells
-    if (!finite) { o.err |= ERR_NONFINITE; o.st = ST_EXIT; return; }
-    int cn[3];
-    float fn[3];
-    if (cells<DIM>(g, o.dn, a.bmin, a.bspan, cn, fn)) return;     // inside the block
-    if constexpr (BTO) {
-        bool gdummy = false;
-        o.st = classify_slow<DIM, true>(a, cn, fn, gdummy);
-    } else {
-        bool out_dom = false;
-        int mul = 1, nb = 0;
-        bool mig = false;
-#pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) {
-            out_dom |= (cn[ax] < 0) | (cn[ax] > a.N[ax] - 1) | ((cn[ax] == a.N[ax] - 1) & (fn[ax] != 0.f));
-            const int off = (cn[ax] < a.lo[ax]) ? -1 : ((cn[ax] >= a.hi[ax] && a.hi[ax] < a.N[ax]) ? 1 : 0);
-            mig |= (off != 0);
-            nb += (off + 1) * mul;
-            mul *= 3;
-        }
-        if (out_dom) o.st = ST_EXIT;
-        else { o.migrate = mig; o.nb = nb; }
-    }
-}
-
-// General path: one RK4 step with a full cell location and boundary test at
-// every stage and a corner reload whenever a stage sample changes cell.  Run
-// for the (about 10 %) particles the fast path defers, packed 32 per warp.
-template <int DIM, bool BTO>
-__device__ __forceinline__ void slow_step(const AdvectArgs& a, bool live, const float4 r, StepOut& o) {
-    constexpr int NP = Pairs<DIM>::n;
-    int g[3];
-    unpack_g(__float_as_uint(r.w), a, g);
-    const float d[3] = {r.x, r.y, DIM == 3 ? r.z : 0.f};
-    f2_t S[NP], B[NP];
-    int c[3];
-    float f[3], e[3];
-    bool ghost_bad = false;
-    o.st = ST_VALID; o.migrate = false; o.nb = 0; o.err = 0;
-
-    // stage 1: q1 = x (validated when committed; top-face clamp on the slow path)
-    if (!cells<DIM>(g, d, a.gmin, a.gspan, c, f) && live)
-        classify_slow<DIM, BTO>(a, c, f, ghost_bad);
-    int cur = live ? node_index<DIM>(a, c) : 0;
-    gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
-    gather_pairs<DIM>(a.v1, cur, a.sx, a.sxy, B);
-    float k1[3];
-    interp_pairs<DIM>(S, f, k1);
-#pragma unroll
-    for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
-
-    bool finite = true;                  // a NaN / huge velocity must latch ERR_NONFINITE
-    // stage 2: q2 = x + dt/2 k1
-#pragma unroll
-    for (int ax = 0; ax < DIM; ++ax) { e[ax] = fmaf(a.hdth[ax], k1[ax], d[ax]); finite &= fabsf(e[ax]) < 4194304.f; }
-    if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live)
-        o.st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
-    {
-        const int idx = node_index<DIM>(a, c);
-        if (live && o.st == ST_VALID && idx != cur) {
-            gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
-            gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
-#pragma unroll
-            for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
-            cur = idx;
-        }
-    }
-    float T2[3];
-    interp_pairs<DIM>(S, f, T2);
-
-    // stage 3: q3 = x + dt/4 T2
-#pragma unroll
-    for (int ax = 0; ax < DIM; ++ax) { e[ax] = fmaf(a.qdth[ax], T2[ax], d[ax]); finite &= fabsf(e[ax]) < 4194304.f; }
-    if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live && o.st == ST_VALID)
-        o.st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
-    {
-        const int idx = node_index<DIM>(a, c);
-        if (live && o.st == ST_VALID && idx != cur) {
-            gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
-            gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
-#pragma unroll
-            for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
-            cur = idx;
-        }
-    }
-    float T3[3];
-    interp_pairs<DIM>(S, f, T3);
-
-    // stage 4: q4 = x + dt/2 T3
-#pragma unroll
-    for (int ax = 0; ax < DIM; ++ax) { e[ax] = fmaf(a.hdth[ax], T3[ax], d[ax]); finite &= fabsf(e[ax]) < 4194304.f; }
-    if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live && o.st == ST_VALID)
-        o.st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
-    {
-        const int idx = node_index<DIM>(a, c);
-        if (live && o.st == ST_VALID && idx != cur) gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
-    }
-    float k4[3];
-    interp_pairs<DIM>(B, f, k4);
-
-#pragma unroll
-    for (int ax = 0; ax < DIM; ++ax)
-        o.dn[ax] = fmaf(a.sdth[ax], (k1[ax] + k4[ax]) + (T2[ax] + T3[ax]), d[ax]);
-    if constexpr (DIM == 2) o.dn[2] = 0.f;
-    if (live && o.st == ST_VALID) classify_update<DIM, BTO>(a, g, o);
-    if (live && ghost_bad) { o.err |= ERR_GHOST; o.st = ST_EXIT; o.migrate = false; }
-    if (live && !finite) { o.err |= ERR_NONFINITE; o.st = ST_EXIT; o.migrate = false; }
-}
-
-// Record the outcome of one lane: survivors are written to `slot` (in place),
-// terminations appended to the dead list, COMM hand-offs to the slot of their
-// neighbour.  Returns the ballots the caller needs for compaction / counters.
-struct Tally { unsigned long long term = 0, exit = 0, sent = 0, defer = 0; uint32_t err = 0; };
-
-template <bool BTO>
-__device__ __forceinline__ void record_dead_and_sent(const AdvectArgs& a, bool live, const float4 r,
-                                                     const StepOut& o, int lane, Tally& t) {
-    const unsigned dmask = __ballot_sync(0xffffffffu, live && o.st != ST_VALID);
-    if (dmask) {
-        uint32_t slot0 = 0;
-        if (lane == 0) slot0 = atomicAdd(a.dead_count, (uint32_t)__popc(dmask));
-        slot0 = __shfl_sync(0xffffffffu, slot0, 0);
-        if (live && o.st != ST_VALID) {
-            const uint32_t s = slot0 + __popc(dmask & ((1u << lane) - 1u));
-            if (s < a.dead_cap) {
-                a.dead_rec[s] = r;                       // pre-step position
-                a.dead_info[s] = ((uint32_t)o.st << 24) | (uint32_t)(a.cycle & 0xffffff);
-            } else {
-                t.err |= ERR_OVERFLOW;
-            }
-        }
-        const unsigned tmask = __ballot_sync(0xffffffffu, live && o.st == ST_TERM);
-        if (lane == 0) { t.term += __popc(tmask); t.exit += __popc(dmask) - __popc(tmask); }
-    }
-    if constexpr (!BTO) {
-        const bool mig = live && o.st == ST_VALID && o.migrate;
-        const unsigned mmask = __ballot_sync(0xffffffffu, mig);
-        if (mig) {
-            const unsigned peers = __match_any_sync(mmask, o.nb);
-            const int leader = __ffs(peers) - 1;
-            float4* sb = a.slot_rec + a.slot_base[o.nb];
-            uint32_t base0 = 0;
-            if (lane == leader) base0 = atomicAdd(reinterpret_cast<uint32_t*>(sb), (uint32_t)__popc(peers));
-            base0 = __shfl_sync(peers, base0, leader);
-            const uint32_t pos = base0 + __popc(peers & ((1u << lane) - 1u));
-            if (pos < (uint32_t)a.slot_capv[o.nb])
-                sb[1 + pos] = make_float4(o.dn[0], o.dn[1], o.dn[2], r.w);
-            else
-                t.err |= ERR_OVERFLOW;
-        }
-        if (lane == 0) t.sent += __popc(mmask);
-    }
-}
-
-// A slot holding this record is a dead placeholder (its particle terminated or
-// moved away after the fast path had reserved the slot); skipped and
-// compacted away by the next cycle, ignored by extraction.
-__device__ __forceinline__ bool is_placeholder(const float4 r) { return __float_as_uint(r.x) == 0x7fc0dead; }
-__device__ __forceinline__ float4 placeholder() { return make_float4(__uint_as_float(0x7fc0dead), 0.f, 0.f, 0.f); }
-
-constexpr int kQueue = 64;    // deferred-particle queue per warp (shared memory)
-
-template <int DIM, bool BTO>
-__device__ __forceinline__ void drain(const AdvectArgs& a, float4* q_rec, uint32_t* q_slot, int& qn,
-                                      int take, int lane, Tally& t) {
-    const bool live = lane < take;
-    const float4 r = live ? q_rec[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const uint32_t slot = live ? q_slot[lane] : 0u;
-    __syncwarp();
-    // shift the rest of the queue down
-    for (int i = take + lane; i < qn; i += 32) { q_rec[i - take] = q_rec[i]; q_slot[i - take] = q_slot[i]; }
-    __syncwarp();
-    qn -= take;
-    StepOut o;
-    slow_step<DIM, BTO>(a, live, r, o);
-    t.err |= o.err;
-    if (live) {
-        const bool keep = o.st == ST_VALID && !o.migrate;
-        a.state[slot] = keep ? make_float4(o.dn[0], o.dn[1], o.dn[2], r.w) : placeholder();
-    }
-    record_dead_and_sent<BTO>(a, live, r, o, lane, t);
-}
-
 template <int DIM, bool BTO>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 advect_kernel(const AdvectArgs a) {
-    constexpr int NP = Pairs<DIM>::n;
-    __shared__ float4 s_qrec[kThreads / 32][kQueue];
-    __shared__ uint32_t s_qslot[kThreads / 32][kQueue];
+    constexpr int NC = (1 << DIM) * DIM;             // corner floats per slice
     const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    float4* q_rec = s_qrec[wib];
-    uint32_t* q_slot = s_qslot[wib];
-    int qn = 0;
     const int warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
-    const int n_tiles = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
+    const int n_tiles_all = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
+    // non-persistent grid: warp w owns tiles [w*tpw, (w+1)*tpw) (contiguous, so
+    // a CTA's particles are spatial neighbours); the block scheduler balances
+    // the load across SMs
+#if LAG_ADV_PERSIST
     // persistent grid: warp w owns tiles w, w + W, w + 2W, ... (W = all warps),
     // so the GPU sweeps the particle list as one compact window
+    const int tile0 = warp;
     const int tstride = (gridDim.x * kThreads) >> 5;
+    const int n_tiles = n_tiles_all;
+#else
+    const int tile0 = warp * a.tiles_per_warp;
+    const int tstride = 1;
+    const int n_tiles = min(n_tiles_all, tile0 + a.tiles_per_warp);
+#endif
 
-    unsigned long long steps = 0;
-    Tally t;
+    unsigned long long steps = 0, nterm = 0, nexit = 0, nsent = 0;
+    uint32_t errbits = 0;
 
-    int tile = warp;
+    // software pipeline: the next tile's count and records are in flight while
+    // the current tile computes
+    int tile = tile0;
     int cnt = tile < n_tiles ? a.tile_count[tile] : 0;
     float4 r = tile < n_tiles ? a.state[(size_t)tile * kTile + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
 
@@ -626,104 +418,191 @@ advect_kernel(const AdvectArgs a) {
         const int ncnt = ntile < n_tiles ? a.tile_count[ntile] : 0;
         const float4 nr = ntile < n_tiles ? a.state[(size_t)ntile * kTile + lane]
                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-        const bool live = lane < cnt && !is_placeholder(r);
+        if (cnt == 0) { tile = ntile; cnt = ncnt; r = nr; continue; }
+        const bool live = lane < cnt;
         float4* trec = a.state + (size_t)tile * kTile;
         int g[3];
         unpack_g(__float_as_uint(r.w), a, g);
         const float d[3] = {r.x, r.y, DIM == 3 ? r.z : 0.f};
 
-        // ---- fast path: every stage sample and the update stay in the cell
-        //      of the committed position (inside the block by construction),
-        //      so no boundary test and no reload is needed; fractions are
-        //      tracked relative to that cell ----
-        int c[3];
-        float f0[3], f[3];
-        bool fast = cells<DIM>(g, d, a.gmin, a.gspan, c, f0) && live;
-        const int cur = fast ? node_index<DIM>(a, c) : 0;
+        constexpr int NP = Pairs<DIM>::n;
         f2_t S[NP], B[NP];
+        int c[3];
+        float f[3], e[3];
+        bool ghost_bad = false;
+        uint8_t st = ST_VALID;
+
+        // ---- stage 1: q1 = x (validated when committed) ----
+        if (!cells<DIM>(g, d, a.gmin, a.gspan, c, f) && live)
+            classify_slow<DIM, BTO>(a, c, f, ghost_bad);   // top-face clamp only
+        int cur = node_index<DIM>(a, c);
+        if (!live) cur = 0;
         gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
         gather_pairs<DIM>(a.v1, cur, a.sx, a.sxy, B);
         float k1[3];
-        interp_pairs<DIM>(S, f0, k1);
+        interp_pairs<DIM>(S, f, k1);
 #pragma unroll
         for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);   // S = v0 + v1 (stages 2, 3)
 
-        uint32_t out = 0;                     // any fraction outside [0, 1) (float bits as unsigned)
+        // ---- stage 2: q2 = x + dt/2 k1, alpha = 1/2 ----
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) { f[ax] = fmaf(a.hdth[ax], k1[ax], f0[ax]); out |= __float_as_uint(f[ax]) >= 0x3f800000u; }
-        float T2[3];
-        interp_pairs<DIM>(S, f, T2);          // T2 = 2 k2
-        {   // the next tile's record has arrived by now: prefetch its stage-1 corners
-            int ng[3], nc[3];
-            float nf[3];
-            unpack_g(__float_as_uint(nr.w), a, ng);
-            const float nd[3] = {nr.x, nr.y, DIM == 3 ? nr.z : 0.f};
-            const bool nok = cells<DIM>(ng, nd, a.gmin, a.gspan, nc, nf) && lane < ncnt;
-            if (nok) prefetch_corners<DIM>(a.v0, a.v1, node_index<DIM>(a, nc), a.sx, a.sxy);
+        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], k1[ax], d[ax]);
+        if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live)
+            st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
+        {
+            const int idx = node_index<DIM>(a, c);
+#ifdef LAG_EXP_NORELOAD
+            if (false) {
+#else
+            if (live && st == ST_VALID && idx != cur) {
+#endif
+                gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
+                gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
+#pragma unroll
+                for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
+                cur = idx;
+            }
         }
+        float T2[3];
+        interp_pairs<DIM>(S, f, T2);                          // T2 = 2 k2
+
+        // ---- stage 3: q3 = x + dt/2 k2 = x + dt/4 T2, alpha = 1/2 ----
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) { f[ax] = fmaf(a.qdth[ax], T2[ax], f0[ax]); out |= __float_as_uint(f[ax]) >= 0x3f800000u; }
+        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.qdth[ax], T2[ax], d[ax]);
+        if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live && st == ST_VALID)
+            st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
+        {
+            const int idx = node_index<DIM>(a, c);
+#ifdef LAG_EXP_NORELOAD
+            if (false) {
+#else
+            if (live && st == ST_VALID && idx != cur) {
+#endif
+                gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
+                gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
+#pragma unroll
+                for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
+                cur = idx;
+            }
+        }
         float T3[3];
-        interp_pairs<DIM>(S, f, T3);          // T3 = 2 k3
+        interp_pairs<DIM>(S, f, T3);                          // T3 = 2 k3
+
+        // ---- stage 4: q4 = x + dt k3 = x + dt/2 T3, alpha = 1 ----
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) { f[ax] = fmaf(a.hdth[ax], T3[ax], f0[ax]); out |= __float_as_uint(f[ax]) >= 0x3f800000u; }
+        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], T3[ax], d[ax]);
+        if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live && st == ST_VALID)
+            st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
+        {
+            const int idx = node_index<DIM>(a, c);
+#ifndef LAG_EXP_NORELOAD
+            if (live && st == ST_VALID && idx != cur) {
+                gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
+            }
+#endif
+        }
         float k4[3];
         interp_pairs<DIM>(B, f, k4);
-        fast &= (out == 0);
 
-        StepOut o;
-        o.st = ST_VALID; o.migrate = false; o.nb = 0; o.err = 0;
-        bool stay = true;
+        // ---- update: x' = x + dt/6 (k1 + 2k2 + 2k3 + k4) ----
+        float dn[3];
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) {
-            const float sum = (k1[ax] + k4[ax]) + (T2[ax] + T3[ax]);
-            o.dn[ax] = fmaf(a.sdth[ax], sum, d[ax]);
-            stay &= __float_as_uint(fmaf(a.sdth[ax], sum, f0[ax])) < 0x3f800000u;
+        for (int ax = 0; ax < DIM; ++ax)
+            dn[ax] = fmaf(a.sdth[ax], (k1[ax] + k4[ax]) + (T2[ax] + T3[ax]), d[ax]);
+        if constexpr (DIM == 2) dn[2] = 0.f;
+        bool finite = true;
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax) finite &= fabsf(dn[ax]) < 4194304.f;   // 2^22 cells
+        // membership of the updated position: fast = inside the block
+        bool migrate = false;
+        int nb = 0;
+        {
+            int cn[3];
+            float fn[3];
+            const bool inblk = cells<DIM>(g, dn, a.bmin, a.bspan, cn, fn);
+            if (!inblk && live && st == ST_VALID) {
+                bool gdummy = false;
+                if constexpr (BTO) {
+                    st = classify_slow<DIM, true>(a, cn, fn, gdummy);
+                } else {
+                    // COMM: in the domain but outside the block -> hand off
+                    bool out_dom = false;
+                    int mul = 1;
+#pragma unroll
+                    for (int ax = 0; ax < DIM; ++ax) {
+                        out_dom |= (cn[ax] < 0) | (cn[ax] > a.N[ax] - 1) |
+                                   ((cn[ax] == a.N[ax] - 1) & (fn[ax] != 0.f));
+                        const int o = (cn[ax] < a.lo[ax]) ? -1
+                                      : ((cn[ax] >= a.hi[ax] && a.hi[ax] < a.N[ax]) ? 1 : 0);
+                        migrate |= (o != 0);
+                        nb += (o + 1) * mul;
+                        mul *= 3;
+                    }
+                    if (out_dom) { st = ST_EXIT; migrate = false; }
+                }
+            }
         }
-        if constexpr (DIM == 2) o.dn[2] = 0.f;
-        if (fast && !stay) classify_update<DIM, BTO>(a, g, o);    // update left the cell
+        if (live && !finite) { errbits |= ERR_NONFINITE; st = ST_EXIT; migrate = false; }
+        if (live && ghost_bad) { errbits |= ERR_GHOST; if (st == ST_VALID) st = ST_EXIT; migrate = false; }
 
-        // ---- particle management: compact in place; deferred lanes keep a
-        //      slot that the general path fills ----
-        const bool defer = live && !fast;
-        const bool keep = defer || (fast && o.st == ST_VALID && !o.migrate);
+        // ---- particle management: compact survivors, record terminations ----
+        const bool keep = live && st == ST_VALID && !migrate;
         const unsigned kmask = __ballot_sync(0xffffffffu, keep);
+        const unsigned dmask = __ballot_sync(0xffffffffu, live && st != ST_VALID);
+        const unsigned tmask = __ballot_sync(0xffffffffu, live && st == ST_TERM);
         __syncwarp();
-        const int pos = __popc(kmask & ((1u << lane) - 1u));
-        if (keep && !defer) trec[pos] = make_float4(o.dn[0], o.dn[1], o.dn[2], r.w);
-        record_dead_and_sent<BTO>(a, fast, r, o, lane, t);
-        t.err |= o.err;
-        const unsigned qmask = __ballot_sync(0xffffffffu, defer);
-        if (defer) {
-            const int qi = qn + __popc(qmask & ((1u << lane) - 1u));
-            q_rec[qi] = r;
-            q_slot[qi] = (uint32_t)((size_t)tile * kTile + pos);
+        if (keep) {
+            const int pos = __popc(kmask & ((1u << lane) - 1u));
+            trec[pos] = make_float4(dn[0], dn[1], dn[2], r.w);
         }
-        qn += __popc(qmask);
-        t.defer += __popc(qmask);
-        const unsigned lmask = __ballot_sync(0xffffffffu, live);
+        if constexpr (!BTO) {
+            const unsigned mmask = __ballot_sync(0xffffffffu, migrate);
+            if (migrate) {
+                const unsigned peers = __match_any_sync(mmask, nb);
+                const int leader = __ffs(peers) - 1;
+                float4* sb = a.slot_rec + a.slot_base[nb];
+                uint32_t base0 = 0;
+                if (lane == leader) base0 = atomicAdd(reinterpret_cast<uint32_t*>(sb), (uint32_t)__popc(peers));
+                base0 = __shfl_sync(peers, base0, leader);
+                const uint32_t pos = base0 + __popc(peers & ((1u << lane) - 1u));
+                if (pos < (uint32_t)a.slot_capv[nb])
+                    sb[1 + pos] = make_float4(dn[0], dn[1], dn[2], r.w);
+                else
+                    errbits |= ERR_OVERFLOW;
+            }
+            if (lane == 0) nsent += __popc(mmask);
+        }
+        if (dmask) {
+            uint32_t slot0 = 0;
+            if (lane == 0) slot0 = atomicAdd(a.dead_count, (uint32_t)__popc(dmask));
+            slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+            if (live && st != ST_VALID) {
+                const uint32_t s = slot0 + __popc(dmask & ((1u << lane) - 1u));
+                if (s < a.dead_cap) {
+                    a.dead_rec[s] = r;                   // pre-step position
+                    a.dead_info[s] = ((uint32_t)st << 24) | (uint32_t)(a.cycle & 0xffffff);
+                } else {
+                    errbits |= ERR_OVERFLOW;
+                }
+            }
+        }
         if (lane == 0) {
             a.tile_count[tile] = (uint8_t)__popc(kmask);
-            steps += __popc(lmask);
+            steps += (unsigned long long)cnt;
+            nterm += __popc(tmask);
+            nexit += __popc(dmask) - __popc(tmask);
         }
-        __syncwarp();
-#ifdef LAG_EXP_NOSLOW
-        qn = 0;
-#endif
-        if (qn >= 32) drain<DIM, BTO>(a, q_rec, q_slot, qn, 32, lane, t);
         tile = ntile; cnt = ncnt; r = nr;
     }
-    if (qn > 0) drain<DIM, BTO>(a, q_rec, q_slot, qn, qn, lane, t);
 
     // one atomic per warp per counter (no CTA barrier: finished warps retire)
     if (lane == 0 && steps) {
         atomicAdd(&a.counters[CNT_STEPS], steps);
-        if (t.term) atomicAdd(&a.counters[CNT_TERM], t.term);
-        if (t.exit) atomicAdd(&a.counters[CNT_EXIT], t.exit);
-        if (t.sent) atomicAdd(&a.counters[CNT_SENT], t.sent);
-        if (t.defer) atomicAdd(&a.counters[CNT_DEFER], t.defer);
+        if (nterm) atomicAdd(&a.counters[CNT_TERM], nterm);
+        if (nexit) atomicAdd(&a.counters[CNT_EXIT], nexit);
+        if (nsent) atomicAdd(&a.counters[CNT_SENT], nsent);
     }
-    const uint32_t errbits = __reduce_or_sync(0xffffffffu, t.err);
+    errbits = __reduce_or_sync(0xffffffffu, errbits);
     if (lane == 0 && errbits) atomicOr(a.err, errbits);
 }
 
@@ -812,7 +691,6 @@ static __global__ void extract_live_kernel(const ExtractArgs a) {
     if (tile >= a.n_tiles) return;
     if ((int)(i % kTile) >= a.tile_count[tile]) return;
     const float4 r = a.state[i];
-    if (__float_as_uint(r.x) == 0x7fc0dead) return;      // placeholder slot
     if (!own_seed(a, __float_as_uint(r.w))) return;
     int g[3];
     const int64_t s = seed_index(a, __float_as_uint(r.w), g);

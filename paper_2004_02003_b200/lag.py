@@ -52,7 +52,6 @@ class lag_stats_t(ctypes.Structure):
                 ("term_boundary", ctypes.c_int64), ("exit_domain", ctypes.c_int64),
                 ("sent", ctypes.c_int64), ("received", ctypes.c_int64),
                 ("particle_steps", ctypes.c_int64), ("cycles", ctypes.c_int64),
-                ("deferred", ctypes.c_int64),
                 ("device_error", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 

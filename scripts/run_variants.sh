@@ -1,4 +1,4 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-export LAG_LIB=
-timeout 120 python scripts/profile_advect.py C5 20 > gpurun_out/plain_v4.log 2>&1 && \
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:advect -s 15 -c 1 -o gpurun_out/prof_advect_v4 python scripts/profile_advect.py C5 20 > gpurun_out/ncu_v4.log 2>&1; echo ncu $?
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | grep -E "Error|error|assert|FAILED|passed|failed" | head -20
+LAG_LIB= timeout 120 python scripts/time_advect.py C5 3 2>&1 | grep -v Warning
+for f in paper_2004_02003_b200/var_*.so; do LAG_LIB=$f timeout 120 python scripts/time_advect.py C5 3; done 2>&1 | grep -v Warning

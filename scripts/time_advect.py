@@ -40,8 +40,7 @@ def main(config="C5", intervals=3, stride=None):
     us = 1e3 * sum(ms) / len(ms)
     print(f"{os.environ.get('LAG_LIB', 'default')}: {config} {us:.1f} us/cycle "
           f"(first {1e3 * ms[0]:.1f}, last {1e3 * ms[I - 1]:.1f}), "
-          f"{st['particle_steps'] / (intervals + 1) / I / us * 1e-3:.2f} G p-steps/s, "
-          f"deferred {100 * st['deferred'] / max(1, st['particle_steps']):.1f}%")
+          f"{st['particle_steps'] / (intervals + 1) / I / us * 1e-3:.2f} G p-steps/s")
     ctx.close()
 
 
