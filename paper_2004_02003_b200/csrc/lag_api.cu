@@ -249,6 +249,7 @@ extern "C" lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out
     }
     SeedArgs sa{};
     sa.state = ctx->state; sa.tile_count = ctx->tile_count; sa.n = n; sa.stride = stride;
+    sa.n_tiles_word = ctx->cfg.mode == LAG_COMM ? ctx->words + W_NTILES : nullptr;
     for (int a = 0; a < 3; ++a) { sa.first[a] = ctx->first[a]; sa.ns[a] = ctx->ns[a]; }
     sa.bx = ctx->bits[0]; sa.by = ctx->bits[1];
     const int64_t total = (int64_t)ctx->n_tiles * kTile;
@@ -390,9 +391,20 @@ static lag_status latched(lag_ctx_s* ctx, uint32_t err) {
 }
 
 static lag_status copy_out(lag_ctx_s* ctx, void* dst, const void* src, size_t bytes) {
-    if (!dst || bytes == 0) return LAG_OK;
+    if (!dst || bytes == 0 || dst == src) return LAG_OK;
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
     return LAG_OK;
+}
+
+// Output written by the kernels directly when it is device memory of this
+// context's device; otherwise into the context's staging buffer, copied out.
+template <typename T>
+static T* out_target(lag_ctx_s* ctx, T* user, T* staging) {
+    if (!user) return staging;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, user) != cudaSuccess) { cudaGetLastError(); return staging; }
+    if (at.type == cudaMemoryTypeDevice && at.device == ctx->cfg.device) return user;
+    return staging;
 }
 
 extern "C" lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8_t* status,
@@ -411,16 +423,12 @@ extern "C" lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8
         if (st != LAG_OK) return st;
     }
     const int D = ctx->cfg.dim;
-    uint32_t n_dead = 0;
-    CK(cudaMemcpyAsync(&ctx->host_words[0], ctx->words, kWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    n_dead = ctx->host_words[W_DEAD];
-    if (n_dead > (uint32_t)ctx->cap) n_dead = (uint32_t)ctx->cap;
-    const int n_tiles = ctx->cfg.mode == LAG_COMM ? (int)ctx->host_words[W_NTILES] : ctx->n_tiles;
-
     ExtractArgs e{};
-    e.state = ctx->state; e.tile_count = ctx->tile_count; e.n_tiles = n_tiles;
-    e.dead_rec = ctx->dead_rec; e.dead_info = ctx->dead_info; e.n_dead = n_dead;
+    e.state = ctx->state; e.tile_count = ctx->tile_count;
+    e.n_tiles = ctx->cfg.mode == LAG_COMM ? ctx->cap_tiles : ctx->n_tiles;
+    e.n_tiles_dev = ctx->cfg.mode == LAG_COMM ? (const int32_t*)(ctx->words + W_NTILES) : nullptr;
+    e.dead_rec = ctx->dead_rec; e.dead_info = ctx->dead_info;
+    e.n_dead_dev = ctx->words + W_DEAD; e.dead_cap = (uint32_t)ctx->cap;
     e.n = ctx->n_seeds; e.dim = D; e.stride = ctx->stride;
     for (int a = 0; a < 3; ++a) {
         e.first[a] = ctx->first[a]; e.ns[a] = ctx->ns[a];
@@ -434,28 +442,27 @@ extern "C" lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8
         int64_t stride_f4 = 2;
         lag_comm_returned(ctx, &e.ret, &stride_f4, &e.n_ret);
     }
-    e.start = ctx->out_start; e.end = ctx->out_end; e.status = ctx->out_status;
+    e.start = out_target(ctx, start, ctx->out_start);
+    e.end = out_target(ctx, end, ctx->out_end);
+    e.status = out_target(ctx, status, ctx->out_status);
     const unsigned nb_seed = (unsigned)((ctx->n_seeds + 255) / 256);
     extract_start_kernel<<<nb_seed, 256, 0, ctx->stream>>>(e);
     ++ctx->launches;
-    if (n_tiles > 0) {
-        extract_live_kernel<<<(unsigned)(((int64_t)n_tiles * kTile + 255) / 256), 256, 0, ctx->stream>>>(e);
-        ++ctx->launches;
-    }
-    if (n_dead > 0) {
-        extract_dead_kernel<<<(n_dead + 255) / 256, 256, 0, ctx->stream>>>(e);
-        ++ctx->launches;
-    }
+    extract_live_kernel<<<(unsigned)(((int64_t)e.n_tiles * kTile + 255) / 256), 256, 0, ctx->stream>>>(e);
+    ++ctx->launches;
+    extract_dead_kernel<<<(unsigned)std::max(1, ctx->num_sms * 2), 256, 0, ctx->stream>>>(e);
+    ++ctx->launches;
     if (e.n_ret > 0) {
         extract_returned_kernel<<<(e.n_ret + 255) / 256, 256, 0, ctx->stream>>>(e);
         ++ctx->launches;
     }
     CK(cudaGetLastError());
     const size_t n = (size_t)ctx->n_seeds;
-    if ((st = copy_out(ctx, start, ctx->out_start, n * D * sizeof(double))) != LAG_OK) return st;
-    if ((st = copy_out(ctx, end, ctx->out_end, n * D * sizeof(double))) != LAG_OK) return st;
-    if ((st = copy_out(ctx, status, ctx->out_status, n)) != LAG_OK) return st;
-    CK(cudaStreamSynchronize(ctx->stream));
+    if ((st = copy_out(ctx, start, e.start, n * D * sizeof(double))) != LAG_OK) return st;
+    if ((st = copy_out(ctx, end, e.end, n * D * sizeof(double))) != LAG_OK) return st;
+    if ((st = copy_out(ctx, status, e.status, n)) != LAG_OK) return st;
+    CK(cudaMemcpyAsync(&ctx->host_words[0], ctx->words, kWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));      // the only host sync of the write cycle
     if (n_out) *n_out = ctx->n_seeds;
     const lag_status err = latched(ctx, ctx->host_words[W_ERR]);
     if (!(flags & LAG_NO_RESEED)) {

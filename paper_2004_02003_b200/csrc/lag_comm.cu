@@ -459,10 +459,7 @@ void lag_comm_destroy(lag_ctx_s* ctx) {
 
 lag_status lag_comm_reset(lag_ctx_s* ctx) {
     Comm* cm = ctx->comm;
-    // W_NTILES = seed tiles; empty outgoing slots; nothing pending
-    const uint32_t nt = (uint32_t)ctx->n_tiles;
-    CKC(cudaMemcpyAsync(ctx->words + W_NTILES, &nt, sizeof(nt), cudaMemcpyHostToDevice, ctx->stream));
-    CKC(cudaStreamSynchronize(ctx->stream));   // nt is a host stack variable
+    // empty outgoing slots; nothing pending (seed_kernel sets W_NTILES)
     CKC(cudaMemsetAsync(cm->slots, 0, sizeof(float4) * std::max<int64_t>(1, cm->slot_total), ctx->stream));
     cm->pending = false;
     cm->n_returned = 0;

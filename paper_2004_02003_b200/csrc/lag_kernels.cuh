@@ -611,6 +611,7 @@ advect_kernel(const AdvectArgs a) {
 struct SeedArgs {
     float4* state;
     uint8_t* tile_count;
+    uint32_t* n_tiles_word;         // COMM: device-side tile count to initialise (or nullptr)
     int64_t n;
     int32_t first[3], stride, ns[3];
     uint32_t bx, by;
@@ -619,6 +620,7 @@ struct SeedArgs {
 static __global__ void seed_kernel(const SeedArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t n_tiles = (a.n + kTile - 1) / kTile;
+    if (i == 0 && a.n_tiles_word) *a.n_tiles_word = (uint32_t)n_tiles;
     if (i < n_tiles * kTile) {
         if (i < a.n) {
             const int64_t ix = i % a.ns[0];
@@ -646,7 +648,9 @@ struct ExtractArgs {
     int32_t n_tiles;
     const float4* dead_rec;
     const uint32_t* dead_info;
-    uint32_t n_dead;
+    const uint32_t* n_dead_dev;     // device-side count of termination records
+    uint32_t dead_cap;
+    const int32_t* n_tiles_dev;     // COMM: device-side tile count (nullptr: n_tiles)
     int64_t n;                      // seeds
     int32_t dim;
     int32_t first[3], stride, ns[3];
@@ -688,7 +692,8 @@ static __global__ void extract_start_kernel(const ExtractArgs a) {
 static __global__ void extract_live_kernel(const ExtractArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t tile = i / kTile;
-    if (tile >= a.n_tiles) return;
+    const int n_tiles = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
+    if (tile >= n_tiles) return;
     if ((int)(i % kTile) >= a.tile_count[tile]) return;
     const float4 r = a.state[i];
     if (!own_seed(a, __float_as_uint(r.w))) return;
@@ -701,16 +706,18 @@ static __global__ void extract_live_kernel(const ExtractArgs a) {
 }
 
 static __global__ void extract_dead_kernel(const ExtractArgs a) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.n_dead) return;
-    const float4 r = a.dead_rec[i];
-    if (!own_seed(a, __float_as_uint(r.w))) return;
-    int g[3];
-    const int64_t s = seed_index(a, __float_as_uint(r.w), g);
-    const float d[3] = {r.x, r.y, r.z};
-    for (int ax = 0; ax < a.dim; ++ax)
-        a.end[s * a.dim + ax] = a.o[ax] + ((double)g[ax] + (double)d[ax]) * a.h[ax];
-    a.status[s] = (uint8_t)(a.dead_info[i] >> 24);
+    const uint32_t n_dead = min(*a.n_dead_dev, a.dead_cap);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_dead;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 r = a.dead_rec[i];
+        if (!own_seed(a, __float_as_uint(r.w))) continue;
+        int g[3];
+        const int64_t s = seed_index(a, __float_as_uint(r.w), g);
+        const float d[3] = {r.x, r.y, r.z};
+        for (int ax = 0; ax < a.dim; ++ax)
+            a.end[s * a.dim + ax] = a.o[ax] + ((double)g[ax] + (double)d[ax]) * a.h[ax];
+        a.status[s] = (uint8_t)(a.dead_info[i] >> 24);
+    }
 }
 
 static __global__ void extract_returned_kernel(const ExtractArgs a) {
