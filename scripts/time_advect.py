@@ -11,7 +11,7 @@ import lag_inputs as L  # noqa: E402
 import paper_2004_02003_b200 as P  # noqa: E402
 
 
-def main(config="C5", intervals=3, stride=None):
+def main(config="C5", intervals=3, stride=None, flush_l2=True):
     cfg = L.make_config(config)
     g = cfg["grid"]
     b = L.decompose(g, cfg["layout"])[0]
@@ -27,7 +27,8 @@ def main(config="C5", intervals=3, stride=None):
     for it in range(intervals + 1):
         ctx.seed(stride or cfg["stride"])
         for c in range(I):
-            flush.zero_()
+            if flush_l2:
+                flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
             ctx.advect(sl[c], sl[c + 1], cfg["dt"])
@@ -38,11 +39,12 @@ def main(config="C5", intervals=3, stride=None):
     ms = [a.elapsed_time(b) for a, b in times]
     st = ctx.stats()
     us = 1e3 * sum(ms) / len(ms)
-    print(f"{os.environ.get('LAG_LIB', 'default')}: {config} {us:.1f} us/cycle "
+    print(f"{os.environ.get('LAG_LIB', 'default')}: {config} {'flushed' if flush_l2 else 'warm-L2'} {us:.1f} us/cycle "
           f"(first {1e3 * ms[0]:.1f}, last {1e3 * ms[I - 1]:.1f}), "
           f"{st['particle_steps'] / (intervals + 1) / I / us * 1e-3:.2f} G p-steps/s")
     ctx.close()
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "C5", int(sys.argv[2]) if len(sys.argv) > 2 else 3)
+    main(sys.argv[1] if len(sys.argv) > 1 else "C5", int(sys.argv[2]) if len(sys.argv) > 2 else 3,
+         flush_l2="--warm" not in sys.argv)
