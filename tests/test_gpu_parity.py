@@ -188,3 +188,69 @@ def test_c5_full_size_sampled():
     gs = oracle.seeds(g, b.lo, b.hi, 1)[pick]
     orc = oracle.run_interval(g, b.lo, b.hi, 1, sl, cfg["dt"], g_seeds=gs, faces=(b.lo, b.hi))
     compare(cfg, orc, start[pick], end[pick], status[pick], label="C5 full sampled")
+
+
+def test_two_intervals_one_context_autoreseed():
+    """lag_extract reseeds by default: the second interval of the same context
+    matches the oracle started at the second interval's time."""
+    import torch
+    import paper_2004_02003_b200 as P
+    cfg = L.make_config("C2", scale=25)
+    g = cfg["grid"]
+    b = L.decompose(g, cfg["layout"])[6]
+    I = 10
+    sl = global_slices(cfg, 2 * I)
+    dev = [torch.from_numpy(np.ascontiguousarray(L.cut_block_slice(V, g, b, 0))).cuda() for V in sl]
+    ctx = P.Context(P.make_config(3, g.nodes, g.origin, g.spacing, b.lo, b.hi,
+                                  stream=torch.cuda.current_stream().cuda_stream))
+    n = ctx.seed(1)
+    outs = []
+    for it in range(2):
+        for k in range(I):
+            ctx.advect(dev[it * I + k], dev[it * I + k + 1], cfg["dt"])
+        start = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+        end = torch.empty_like(start)
+        st = torch.empty((n,), dtype=torch.uint8, device="cuda")
+        assert ctx.extract(start, end, st) == n          # default flags: reseed
+        outs.append((start.cpu().numpy(), end.cpu().numpy(), st.cpu().numpy()))
+    ctx.close()
+    for it in range(2):
+        orc = oracle_block(cfg, b, sl[it * I:(it + 1) * I + 1], 1, oracle.BTO)
+        compare(cfg, orc, *outs[it], label=f"interval {it}")
+
+
+def test_host_output_buffers():
+    """Outputs may be host memory (numpy): staged and copied by the library,
+    identical to device outputs."""
+    import torch
+    import paper_2004_02003_b200 as P
+    cfg = L.make_config("C2", scale=21)
+    g = cfg["grid"]
+    b = L.decompose(g, cfg["layout"])[2]
+    sl = global_slices(cfg, 5)
+    ref = gpu_block(cfg, b, sl, 1)
+    dev = [torch.from_numpy(np.ascontiguousarray(L.cut_block_slice(V, g, b, 0))).cuda() for V in sl]
+    ctx = P.Context(P.make_config(3, g.nodes, g.origin, g.spacing, b.lo, b.hi,
+                                  stream=torch.cuda.current_stream().cuda_stream))
+    n = ctx.seed(1)
+    for k in range(5):
+        ctx.advect(dev[k], dev[k + 1], cfg["dt"])
+    start = np.zeros((n, 3)); end = np.zeros((n, 3)); st = np.zeros(n, np.uint8)
+    ctx.extract(start, end, st)
+    ctx.close()
+    assert np.array_equal(start, ref[0]) and np.array_equal(end, ref[1]) and np.array_equal(st, ref[2])
+
+
+def test_whole_block_terminates():
+    """Every particle of the upstream block leaves it: all TERM_BOUNDARY with
+    the closed-form termination positions; particle-steps accounting."""
+    g = L.Grid(3, (17, 6, 6), (0.0, 0.0, 0.0), (1.0, 1.0, 1.0))
+    cfg = dict(grid=g, field=L.FieldSpec("uniform", (2.0, 0.0, 0.0)), dt=0.5, name="uniform")
+    sl = global_slices(cfg, 12)           # 1 cell per cycle, block 0 is 9 cells wide
+    b0 = L.decompose(g, (2, 1, 1))[0]
+    start, end, status, st = gpu_block(cfg, b0, sl, 1)
+    assert (status == 1).all()
+    x0 = start[:, 0]
+    cstar = np.ceil(b0.hi[0] - x0).astype(int) - 1     # first cycle whose step lands at/after the face
+    np.testing.assert_array_equal(end[:, 0], x0 + cstar)
+    assert st["particle_steps"] == int((cstar + 1).sum())
