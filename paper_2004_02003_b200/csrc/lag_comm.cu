@@ -474,7 +474,7 @@ static lag_status launch_append(lag_ctx_s* ctx) {
     a.npeers = (int)cm->peers.size();
     for (size_t i = 0; i < cm->peers.size(); ++i) { a.recv[i] = cm->peers[i].recv_slot; a.cap[i] = cm->peers[i].cap_recv; }
     a.slots = cm->slots;
-    a.noff = ctx->cfg.dim == 3 ? 27 : 9;
+    a.noff = kMaxOff;                               // all 27 offset headers (2-D uses 9..17)
     for (int k = 0; k < kMaxOff; ++k) a.slot_base[k] = cm->slot_base[k];
     append_kernel<<<1, 1024, 0, ctx->stream>>>(a);
     ++ctx->launches;

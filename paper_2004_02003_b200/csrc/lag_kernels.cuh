@@ -538,6 +538,7 @@ advect_kernel(const AdvectArgs a) {
                         nb += (o + 1) * mul;
                         mul *= 3;
                     }
+                    if constexpr (DIM == 2) nb += 9;     // offset index (ox+1) + 3(oy+1) + 9(oz+1), oz = 0
                     if (out_dom) { st = ST_EXIT; migrate = false; }
                 }
             }
