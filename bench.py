@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--no-comm", action="store_true", help="skip the comm-baseline arm")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the C3 (stride-2) line")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--warm-l2", action="store_true", help="do not flush L2 between cycles")
     return ap.parse_args()
@@ -279,6 +280,49 @@ def run_e2e(cfg, rank, world, steps, warmup):
             "timing": "wall clock around synchronize, max over ranks"}
 
 
+def algorithmic_bytes(name, psteps, cycles, slice_bytes):
+    """Algorithmic bytes of `cycles` advect launches: 32 B per particle-step
+    (float4 read + write) + the slice sectors the method's stage gathers touch
+    per cycle (profiles/algbytes.json, written by scripts/algbytes.py from the
+    oracle's touched-node maps; both whole slices if absent)."""
+    vel = 2.0 * slice_bytes
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "algbytes.json")))[name]
+        vel = 32.0 * float(np.mean([c["sectors_v_t"] + c["sectors_v_t1"] for c in d["cycles"]]))
+    except Exception:
+        pass
+    return 32.0 * psteps + cycles * vel
+
+
+def measure_secondary(name, rank, world, steps, warmup, flush):
+    """BTO throughput + roofline of another per-GPU workload (C3: stride 2,
+    the HBM-heavy configuration)."""
+    import torch
+    import lag_inputs as L
+    import paper_2004_02003_b200 as P
+    cfg = L.make_config(name, nranks=world)
+    arm = Arm(cfg, rank, world, P.LAG_BTO)
+    run_arm(arm, warmup, flush)
+    barrier(world)
+    torch.cuda.synchronize()
+    t_adv, t_other, psteps = run_arm(arm, steps, flush)
+    adv_ms, dev_ms = sum(t_adv), sum(t_adv) + sum(t_other)
+    dev_ms_max = allreduce_max(dev_ms, world)
+    total_ps = allreduce_sum(psteps, world)
+    cycles = steps * arm.interval
+    alg = algorithmic_bytes(name, psteps, cycles, arm.slice_bytes)
+    peak, _ = measured_peak()
+    ach = alg / (adv_ms / 1e3) / 1e9
+    out = {"workload": f"{name}: {cfg['field'].kind} field, {list(L.block_slice_extent(cfg['grid'], arm.block, 0))} "
+                       f"slice nodes per GPU, stride {cfg['stride']}, {arm.n} particles/GPU, interval {cfg['interval']}",
+           "value": total_ps / (dev_ms_max / 1e3), "unit": UNIT, "ms_per_step": dev_ms_max / steps,
+           "ms_per_cycle": allreduce_max(adv_ms, world) / cycles,
+           "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                        "alg_bytes_per_launch": alg / cycles}}
+    arm.ctx.close()
+    return out
+
+
 def measured_peak():
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -383,10 +427,10 @@ def main():
     total_ps = allreduce_sum(psteps, world)
     value = total_ps / (dev_ms_max / 1e3)
     # roofline of the dominant kernel (advect): algorithmic bytes per launch =
-    # 32 B x active particles (float4 read + write) + both slices read once
-    # (stride 1 touches every node) — DESIGN.md §roofline
+    # 32 B x active particles (float4 read + write) + the slice sectors the
+    # method touches (stride 1: every node) — DESIGN.md §6
     cycles = args.steps * arm.interval
-    alg_bytes = 32.0 * psteps + cycles * 2.0 * arm.slice_bytes
+    alg_bytes = algorithmic_bytes(cfg["name"], psteps, cycles, arm.slice_bytes)
     achieved = alg_bytes / (adv_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
     st = arm.ctx.stats()
@@ -413,6 +457,10 @@ def main():
                 "exchange": "NCCL grouped send/recv per cycle: halo (G=1, faces+edges+corners) + particle slots"}
         carm.ctx.close()
         del carm
+
+    secondary = None
+    if not args.no_secondary:
+        secondary = measure_secondary("C3", rank, world, max(2, args.steps // 2), 2, flush)
 
     e2e = None
     if not args.no_e2e:
@@ -445,6 +493,7 @@ def main():
                          "alg_bytes_per_launch": alg_bytes / cycles,
                          "kernel_share_of_step": adv_ms / dev_ms},
             "comm": comm,
+            "secondary": secondary,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
