@@ -344,6 +344,7 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
     }
     a.sx = ctx->ext[0];
     a.sxy = ctx->ext[0] * ctx->ext[1];
+    a.gidx0 = (a.gmin[0] - a.base[0]) + a.sx * (a.gmin[1] - a.base[1]) + a.sxy * (a.gmin[2] - a.base[2]);
     a.bx = ctx->bits[0]; a.by = ctx->bits[1];
     a.mx = (1u << ctx->bits[0]) - 1u; a.my = (1u << ctx->bits[1]) - 1u;
     a.dead_rec = ctx->dead_rec; a.dead_info = ctx->dead_info;

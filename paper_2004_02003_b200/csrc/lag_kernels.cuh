@@ -57,6 +57,7 @@ struct AdvectArgs {
     // block membership [bmin, bmin + bspan]; anything else takes the slow path
     int32_t gmin[3], gspan[3];
     int32_t bmin[3], bspan[3];
+    int32_t gidx0;                  // node index of global cell gmin (local slice coordinates)
     int32_t sx, sxy;                // slice pitch (nodes) of a row / a plane
     float hdth[3], qdth[3], sdth[3];// dt/h * (1/2, 1/4, 1/6)
     uint32_t bx, by;                // packed seed-node bit widths (x, y)
@@ -262,6 +263,49 @@ __device__ __forceinline__ uint8_t classify_slow(const AdvectArgs& a, int c[3], 
     return ST_VALID;
 }
 
+// Biased form used on the hot path: gb = g - rmin - bits(1.5*2^23) per
+// axis (per particle, once), so v = c - rmin is one add of the floor's float
+// bits and the range test one unsigned compare.
+constexpr int kMagicBits = 0x4B400000;    // bits of 12582912.0f = 1.5 * 2^23
+template <int DIM>
+__device__ __forceinline__ bool cells_b(const int gb[3], const float e[3], const int32_t* rspan,
+                                        int v[3], float f[3]) {
+    bool ok = true;
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) {
+        const float fl = floorf(e[ax]);
+        f[ax] = e[ax] - fl;                              // exact
+        v[ax] = gb[ax] + __float_as_int(fl + 12582912.0f);   // = c - rmin (|fl| < 2^22)
+        ok &= (unsigned)v[ax] <= (unsigned)rspan[ax];
+    }
+    if constexpr (DIM == 2) { v[2] = 0; f[2] = 0.f; }
+    return ok;
+}
+
+// Node index (local slice coordinates) of the cell with gather offsets v.
+template <int DIM>
+__device__ __forceinline__ int vindex(const AdvectArgs& a, const int v[3]) {
+    if constexpr (DIM == 3) return v[0] + a.sx * v[1] + a.sxy * v[2] + a.gidx0;
+    else return v[0] + a.sx * v[1] + a.gidx0;
+}
+
+// Slow path on gather offsets: convert to cells, classify, convert back.
+template <int DIM, bool BTO>
+__device__ __forceinline__ uint8_t classify_slow_v(const AdvectArgs& a, int v[3], float f[3],
+                                                   bool& ghost_bad);
+
+template <int DIM, bool BTO>
+__device__ __forceinline__ uint8_t classify_slow_v(const AdvectArgs& a, int v[3], float f[3],
+                                                   bool& ghost_bad) {
+    int c[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) c[ax] = v[ax] + a.gmin[ax];
+    const uint8_t st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) v[ax] = c[ax] - a.gmin[ax];
+    return st;
+}
+
 template <int DIM>
 __device__ __forceinline__ int node_index(const AdvectArgs& a, const int c[3]) {
     const int lx = c[0] - a.base[0], ly = c[1] - a.base[1];
@@ -433,9 +477,12 @@ advect_kernel(const AdvectArgs a) {
         uint8_t st = ST_VALID;
 
         // ---- stage 1: q1 = x (validated when committed) ----
-        if (!cells<DIM>(g, d, a.gmin, a.gspan, c, f) && live)
-            classify_slow<DIM, BTO>(a, c, f, ghost_bad);   // top-face clamp only
-        int cur = node_index<DIM>(a, c);
+        int gb[3];                            // g - gmin - magic (see cells_b)
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) gb[ax] = g[ax] - a.gmin[ax] - kMagicBits;
+        if (!cells_b<DIM>(gb, d, a.gspan, c, f) && live)
+            classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);   // top-face clamp only
+        int cur = vindex<DIM>(a, c);
         if (!live) cur = 0;
         gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
         gather_pairs<DIM>(a.v1, cur, a.sx, a.sxy, B);
@@ -447,10 +494,10 @@ advect_kernel(const AdvectArgs a) {
         // ---- stage 2: q2 = x + dt/2 k1, alpha = 1/2 ----
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], k1[ax], d[ax]);
-        if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live)
-            st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
+        if (!cells_b<DIM>(gb, e, a.gspan, c, f) && live)
+            st = classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);
         {
-            const int idx = node_index<DIM>(a, c);
+            const int idx = vindex<DIM>(a, c);
 #ifdef LAG_EXP_NORELOAD
             if (false) {
 #else
@@ -469,10 +516,10 @@ advect_kernel(const AdvectArgs a) {
         // ---- stage 3: q3 = x + dt/2 k2 = x + dt/4 T2, alpha = 1/2 ----
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.qdth[ax], T2[ax], d[ax]);
-        if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live && st == ST_VALID)
-            st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
+        if (!cells_b<DIM>(gb, e, a.gspan, c, f) && live && st == ST_VALID)
+            st = classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);
         {
-            const int idx = node_index<DIM>(a, c);
+            const int idx = vindex<DIM>(a, c);
 #ifdef LAG_EXP_NORELOAD
             if (false) {
 #else
@@ -491,10 +538,10 @@ advect_kernel(const AdvectArgs a) {
         // ---- stage 4: q4 = x + dt k3 = x + dt/2 T3, alpha = 1 ----
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], T3[ax], d[ax]);
-        if (!cells<DIM>(g, e, a.gmin, a.gspan, c, f) && live && st == ST_VALID)
-            st = classify_slow<DIM, BTO>(a, c, f, ghost_bad);
+        if (!cells_b<DIM>(gb, e, a.gspan, c, f) && live && st == ST_VALID)
+            st = classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);
         {
-            const int idx = node_index<DIM>(a, c);
+            const int idx = vindex<DIM>(a, c);
 #ifndef LAG_EXP_NORELOAD
             if (live && st == ST_VALID && idx != cur) {
                 gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
@@ -519,7 +566,12 @@ advect_kernel(const AdvectArgs a) {
         {
             int cn[3];
             float fn[3];
-            const bool inblk = cells<DIM>(g, dn, a.bmin, a.bspan, cn, fn);
+            int gbb[3];                       // g - bmin - magic
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) gbb[ax] = BTO ? gb[ax] : g[ax] - a.bmin[ax] - kMagicBits;
+            const bool inblk = cells_b<DIM>(gbb, dn, a.bspan, cn, fn);
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) cn[ax] += a.bmin[ax];         // back to cells (slow path)
             if (!inblk && live && st == ST_VALID) {
                 bool gdummy = false;
                 if constexpr (BTO) {

@@ -1,2 +1,4 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29557 scripts/mgpu_check.py C1 0 2>&1 | grep -v "^\*\|OMP_NUM\|^$" | grep -v "^  File\|^    " | head -40
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | grep -E "Error|error|assert|FAILED|passed|failed" | head -20
+timeout 120 python scripts/time_advect.py C5 3 2>&1 | grep -v Warning
+timeout 120 python scripts/time_advect.py C3 2 2>&1 | grep -v Warning
