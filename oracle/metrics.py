@@ -16,8 +16,9 @@ The paper's accuracy metric and its post hoc reconstruction, on CPU.
   barycentric interpolation of the end positions.  Reading R12: Qhull with
   joggle (QJ) over spatial tiles of the hole bands.
 * Eq. 2 (§3.3): linear interpolation through a reconstructed hole
-  equals interpolation between its valid neighbours — used as the hole-fill
-  cross-check (grid_fill_1d).
+  equals interpolation between its valid neighbours — grid_fill_1d (the pin)
+  and grid_fill (the lattice GridFill reconstruction), the
+  fast alternative to Delaunay for large flow maps.
 """
 from __future__ import annotations
 
@@ -164,15 +165,67 @@ def reconstruct_holes(g_seeds: np.ndarray, start: np.ndarray, end: np.ndarray,
     return recon, inside
 
 
-def agreement(grid, g_seeds, start, bto_end, bto_status, comm_end, comm_status, stride):
+def grid_fill(lat: np.ndarray, values: np.ndarray, valid: np.ndarray, hole: np.ndarray):
+    """GridFill reconstruction on the seed lattice (justified
+    by Eq. 2): each hole is filled by linear interpolation (Eq. 1)
+    between the nearest valid seeds on both sides along a lattice axis; the
+    fills of the axes that have both bounds are averaged.  `lat` are integer
+    lattice coordinates [n, dim] (seed node // stride); returns
+    (filled values [n, k] with NaN where no axis has both bounds, filled mask)."""
+    lat = np.asarray(lat)
+    dim = lat.shape[1]
+    lo = lat.min(axis=0)
+    shape = tuple(int(x) for x in (lat.max(axis=0) - lo + 1))
+    idx = tuple((lat[:, a] - lo[a]) for a in range(dim))
+    k = values.shape[1]
+    V = np.full(shape + (k,), np.nan)
+    ok = np.zeros(shape, dtype=bool)
+    V[idx] = np.where(valid[:, None], values, np.nan)
+    ok[idx] = valid
+    acc = np.zeros(shape + (k,))
+    cnt = np.zeros(shape)
+    for a in range(dim):
+        n = shape[a]
+        pos = np.arange(n).reshape([-1 if b == a else 1 for b in range(dim)])
+        pos = np.broadcast_to(pos, shape)
+        left = np.where(ok, pos, -1)
+        left = np.maximum.accumulate(left, axis=a)             # nearest valid at or before
+        right = np.where(ok, pos, n)
+        right = np.flip(np.minimum.accumulate(np.flip(right, axis=a), axis=a), axis=a)
+        both = (left >= 0) & (right < n) & ~ok
+        li = np.clip(left, 0, n - 1)
+        ri = np.clip(right, 0, n - 1)
+        vl = np.take_along_axis(V, li[..., None], axis=a) if False else np.take_along_axis(
+            V, np.expand_dims(li, -1).repeat(k, -1), axis=a)
+        vr = np.take_along_axis(V, np.expand_dims(ri, -1).repeat(k, -1), axis=a)
+        span = np.where(both, right - left, 1).astype(np.float64)
+        wr = np.where(both, (pos - left) / span, 0.0)
+        fill = (1.0 - wr)[..., None] * np.nan_to_num(vl) + wr[..., None] * np.nan_to_num(vr)
+        acc += np.where(both[..., None], fill, 0.0)
+        cnt += both
+    out = np.full(values.shape, np.nan)
+    got = cnt[idx] > 0
+    res = acc[idx] / np.maximum(cnt[idx], 1)[:, None]
+    out[got] = res[got]
+    filled = got & hole
+    return out, filled
+
+
+def agreement(grid, g_seeds, start, bto_end, bto_status, comm_end, comm_status, stride,
+              method: str = "delaunay"):
     """BTO-vs-comm flow-map agreement for one interval (§4.3):
     over seeds valid in the comm flow map, b = BTO end if valid, else its
-    reconstruction; L = Eq. 5, accuracy = Eq. 6.  Seeds whose reconstruction
-    falls outside the hull are excluded and counted."""
+    reconstruction (Delaunay + barycentric, P:267-274, or GridFill, Eq. 2);
+    L = Eq. 5, accuracy = Eq. 6.  Seeds that cannot be reconstructed (outside
+    the hull / no bounding pair) are excluded and counted."""
     comm_ok = np.asarray(comm_status) == 0
     bto_ok = np.asarray(bto_status) == 0
     hole = comm_ok & ~bto_ok
-    recon, inside = reconstruct_holes(g_seeds, start, bto_end, bto_ok, hole, stride)
+    if method == "gridfill":
+        lat = np.asarray(g_seeds)[:, :grid.dim] // stride
+        recon, inside = grid_fill(lat, bto_end, bto_ok, hole)
+    else:
+        recon, inside = reconstruct_holes(g_seeds, start, bto_end, bto_ok, hole, stride)
     b = np.where(bto_ok[:, None], bto_end, recon)
     use = comm_ok & (bto_ok | inside)
     diff = np.linalg.norm(b[use] - comm_end[use], axis=1)

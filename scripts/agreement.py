@@ -42,6 +42,8 @@ def main():
     ap.add_argument("--stride", type=int, default=None)
     ap.add_argument("--interval", type=int, default=None)
     ap.add_argument("--save", action="store_true")
+    ap.add_argument("--recon", default="delaunay", choices=["delaunay", "gridfill"])
+    ap.add_argument("--tag", default="")
     args = ap.parse_args()
     from oracle import metrics
     cfg = L.make_config(args.config, scale=args.scale, interval=args.interval)
@@ -96,7 +98,7 @@ def main():
         t_gpu += time.time() - t0
         t1 = time.time()
         r = metrics.agreement(g, gall, start.cpu().numpy(), b_end, b_st, m_end.cpu().numpy(),
-                              m_st.cpu().numpy(), stride)
+                              m_st.cpu().numpy(), stride, method=args.recon)
         t_cpu += time.time() - t1
         r["interval"] = it
         per.append(r)
@@ -115,15 +117,19 @@ def main():
         "excluded_outside_hull": int(sum(r["excluded"] for r in per)),
         "compared": int(sum(r["compared"] for r in per)),
         "gpu_seconds": t_gpu, "cpu_seconds": t_cpu, "cpu_cores": os.cpu_count(),
-        "method": "BTO: 8 blocks on one GPU; COMM map: single-block run (== decomposed COMM bitwise); "
-                  "holes reconstructed by Qhull-QJ Delaunay + barycentric over valid seeds in hole-band tiles",
+        "method": "BTO: one context per block on one GPU; COMM map: single-block run (== decomposed COMM "
+                  "bitwise); holes reconstructed by " + ("Qhull-QJ Delaunay + barycentric over valid seeds in "
+                  "hole-band tiles (P:267-274)" if args.recon == "delaunay" else
+                  "GridFill along lattice axes (Eq. 2, SPEC.md:323-331)"),
+        "reconstruction": args.recon,
         "per_interval": [{k: r[k] for k in ("interval", "L", "max_l2", "accuracy", "discarded", "holes", "excluded")}
                          for r in per],
     }
     print(json.dumps(out), flush=True)
     if args.save:
         os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-        json.dump(out, open(os.path.join(ROOT, "profiles", f"agreement_{cfg['name']}.json"), "w"), indent=1)
+        tag = args.tag or f"{cfg['name']}_i{I}_{args.recon}"
+        json.dump(out, open(os.path.join(ROOT, "profiles", f"agreement_{tag}.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":

@@ -435,3 +435,25 @@ def test_bto_update_only_exit_rotation():
     # the same particle without the block face moves to the closed-form x'_y
     free = oracle.rk4_free(g, V, V, dt, np.array([[x0, y0, 0.0]]))
     assert abs(free[0, 1] - (y0 + R * (dt - dt ** 3 / 6))) < 1e-6
+
+
+def test_grid_fill_affine_exact_and_eq2():
+    """GridFill (Eq. 2) on the seed lattice is exact on affine flow maps and
+    along a single lattice line reduces to grid_fill_1d / direct interpolation."""
+    rng = np.random.default_rng(9)
+    n = 12
+    ax = np.arange(n)
+    gz, gy, gx = np.meshgrid(ax, ax, ax, indexing="ij")
+    lat = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], 1)
+    M = rng.normal(size=(3, 3)); t = rng.normal(size=3)
+    end = (lat * 0.3) @ M.T + t
+    hole = (np.abs(lat[:, 0] - 6) <= 1) & (lat[:, 1] % 3 != 0)
+    out, filled = metrics.grid_fill(lat, end, ~hole, hole)
+    assert filled[hole].all()
+    np.testing.assert_allclose(out[hole], end[hole], atol=1e-12)
+    # one lattice line: equals the 1-D Eq. 2 fill
+    f = rng.normal(size=n)
+    valid = np.ones(n, bool); valid[[3, 4, 8]] = False
+    lat1 = np.stack([np.arange(n), np.zeros(n, int)], 1)
+    out1, fl1 = metrics.grid_fill(lat1, f[:, None], valid, ~valid)
+    np.testing.assert_allclose(out1[~valid, 0], metrics.grid_fill_1d(f, valid, np.arange(n))[~valid], atol=1e-12)
