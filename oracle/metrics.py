@@ -168,8 +168,8 @@ def reconstruct_holes(g_seeds: np.ndarray, start: np.ndarray, end: np.ndarray,
 def grid_fill(lat: np.ndarray, values: np.ndarray, valid: np.ndarray, hole: np.ndarray):
     """GridFill reconstruction on the seed lattice (justified
     by Eq. 2): each hole is filled by linear interpolation (Eq. 1)
-    between the nearest valid seeds on both sides along a lattice axis; the
-    fills of the axes that have both bounds are averaged.  `lat` are integer
+    between the nearest valid seeds on both sides along a lattice axis, using
+    the axis with the shortest such bracket (ties averaged; reading R12).  `lat` are integer
     lattice coordinates [n, dim] (seed node // stride); returns
     (filled values [n, k] with NaN where no axis has both bounds, filled mask)."""
     lat = np.asarray(lat)
@@ -182,8 +182,7 @@ def grid_fill(lat: np.ndarray, values: np.ndarray, valid: np.ndarray, hole: np.n
     ok = np.zeros(shape, dtype=bool)
     V[idx] = np.where(valid[:, None], values, np.nan)
     ok[idx] = valid
-    acc = np.zeros(shape + (k,))
-    cnt = np.zeros(shape)
+    fills, spans = [], []
     for a in range(dim):
         n = shape[a]
         pos = np.arange(n).reshape([-1 if b == a else 1 for b in range(dim)])
@@ -201,11 +200,17 @@ def grid_fill(lat: np.ndarray, values: np.ndarray, valid: np.ndarray, hole: np.n
         span = np.where(both, right - left, 1).astype(np.float64)
         wr = np.where(both, (pos - left) / span, 0.0)
         fill = (1.0 - wr)[..., None] * np.nan_to_num(vl) + wr[..., None] * np.nan_to_num(vr)
-        acc += np.where(both[..., None], fill, 0.0)
-        cnt += both
+        fills.append(fill[idx])
+        spans.append(np.where(both, right - left, np.iinfo(np.int64).max)[idx])
+    # Eq. 1 along the axis with the shortest valid bracket (the most local
+    # linear interpolant); ties are averaged
+    spans = np.stack(spans, 1)
+    best = spans.min(axis=1)
+    use = (spans == best[:, None]) & (best[:, None] < np.iinfo(np.int64).max)
+    cntv = use.sum(axis=1)
+    res = sum(np.where(use[:, a:a + 1], fills[a], 0.0) for a in range(dim)) / np.maximum(cntv, 1)[:, None]
     out = np.full(values.shape, np.nan)
-    got = cnt[idx] > 0
-    res = acc[idx] / np.maximum(cnt[idx], 1)[:, None]
+    got = cntv > 0
     out[got] = res[got]
     filled = got & hole
     return out, filled

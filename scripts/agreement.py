@@ -44,12 +44,15 @@ def main():
     ap.add_argument("--save", action="store_true")
     ap.add_argument("--recon", default="delaunay", choices=["delaunay", "gridfill"])
     ap.add_argument("--tag", default="")
+    ap.add_argument("--layout", default=None, help="blocks per axis, e.g. 2,2,2 (default: the config's)")
     args = ap.parse_args()
     from oracle import metrics
     cfg = L.make_config(args.config, scale=args.scale, interval=args.interval)
     g = cfg["grid"]
     stride = args.stride or cfg["stride"]
     I = cfg["interval"]
+    if args.layout:
+        cfg["layout"] = tuple(int(x) for x in args.layout.split(","))
     blocks = L.decompose(g, cfg["layout"])
     whole = L.Block(0, (0, 0, 0), (0, 0, 0), g.nodes)
     s = torch.cuda.current_stream()
