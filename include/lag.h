@@ -152,7 +152,9 @@ LAG_API lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out);
  * neighbours, advances, and hands particles whose updated position lies in
  * another block to its owner.  In COMM mode the ghost layers of the slice
  * arrays are written; interior nodes never are.
- * v_t, v_t1: slice arrays (see Conventions), device or host memory.
+ * v_t, v_t1: slice arrays (see Conventions), device or host memory.  Passing
+ * the same array twice is the frozen-snapshot regime (one accessible time
+ * step per cycle): identical results, corners gathered once.
  * Errors: LAG_ESTATE (no lag_seed), LAG_EINVAL (dt <= 0 or non-finite, NULL
  * slice), LAG_ECUDA, LAG_ENCCL.  Async conditions are latched (see lag_stats).
  */
@@ -172,6 +174,17 @@ LAG_API lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, double d
  */
 LAG_API lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8_t* status,
                        int64_t capacity, int64_t* n_out, uint32_t flags);
+
+/*
+ * lag_extract_ex — lag_extract plus, when term_cycle is not NULL, the cycle
+ * (0-based within the interval) at which each non-valid basis flow
+ * terminated, -1 for valid ones: with `end` this is the termination location
+ * on the block boundary the paper names as future work.  Same
+ * conventions and errors as lag_extract.
+ */
+LAG_API lag_status lag_extract_ex(lag_ctx ctx, double* start, double* end, uint8_t* status,
+                                  int32_t* term_cycle, int64_t capacity, int64_t* n_out,
+                                  uint32_t flags);
 
 /* lag_stats — synchronise the stream and report counters (see lag_stats_t). */
 LAG_API lag_status lag_stats(lag_ctx ctx, lag_stats_t* out);

@@ -170,6 +170,7 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     if ((st = dmalloc(ctx, &ctx->out_start, (size_t)owned * D)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->out_end, (size_t)owned * D)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->out_status, (size_t)owned)) != LAG_OK) return fail(st);
+    if ((st = dmalloc(ctx, &ctx->out_cycle, (size_t)owned)) != LAG_OK) return fail(st);
     {
         cudaError_t e = cudaMemsetAsync(ctx->counters, 0, CNT_N * sizeof(unsigned long long), ctx->stream);
         if (e == cudaSuccess) e = cudaMemsetAsync(ctx->words, 0, kWords * sizeof(uint32_t), ctx->stream);
@@ -197,7 +198,7 @@ extern "C" lag_status lag_destroy(lag_ctx ctx) {
     lag_comm_destroy(ctx);
     dfree(ctx->state); dfree(ctx->tile_count); dfree(ctx->dead_rec); dfree(ctx->dead_info);
     dfree(ctx->words); dfree(ctx->counters); dfree(ctx->out_start); dfree(ctx->out_end);
-    dfree(ctx->out_status); dfree(ctx->stage[0]); dfree(ctx->stage[1]);
+    dfree(ctx->out_status); dfree(ctx->out_cycle); dfree(ctx->stage[0]); dfree(ctx->stage[1]);
     delete ctx;
     return LAG_OK;
 }
@@ -317,6 +318,7 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
     }
     AdvectArgs a{};
     a.v0 = d0; a.v1 = d1;
+    a.frozen = d0 == d1 ? 1 : 0;
     a.state = ctx->state; a.tile_count = ctx->tile_count;
     a.n_tiles_dev = ctx->cfg.mode == LAG_COMM ? (const int32_t*)(ctx->words + W_NTILES) : nullptr;
     a.n_tiles = ctx->n_tiles;
@@ -410,10 +412,16 @@ static T* out_target(lag_ctx_s* ctx, T* user, T* staging) {
 
 extern "C" lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8_t* status,
                                   int64_t capacity, int64_t* n_out, uint32_t flags) {
+    return lag_extract_ex(ctx, start, end, status, nullptr, capacity, n_out, flags);
+}
+
+extern "C" lag_status lag_extract_ex(lag_ctx ctx, double* start, double* end, uint8_t* status,
+                                     int32_t* term_cycle, int64_t capacity, int64_t* n_out,
+                                     uint32_t flags) {
     if (n_out) *n_out = 0;
     if (!ctx) { lag_set_error(nullptr, "ctx is NULL"); return LAG_EINVAL; }
     if (!ctx->seeded) { lag_set_error(ctx, "lag_extract before lag_seed"); return LAG_ESTATE; }
-    if (capacity < ctx->n_seeds && (start || end || status)) {
+    if (capacity < ctx->n_seeds && (start || end || status || term_cycle)) {
         lag_set_error(ctx, "capacity %lld < %lld seeds", (long long)capacity, (long long)ctx->n_seeds);
         return LAG_EINVAL;
     }
@@ -446,6 +454,7 @@ extern "C" lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8
     e.start = out_target(ctx, start, ctx->out_start);
     e.end = out_target(ctx, end, ctx->out_end);
     e.status = out_target(ctx, status, ctx->out_status);
+    e.term_cycle = term_cycle ? out_target(ctx, term_cycle, ctx->out_cycle) : nullptr;
     const unsigned nb_seed = (unsigned)((ctx->n_seeds + 255) / 256);
     extract_start_kernel<<<nb_seed, 256, 0, ctx->stream>>>(e);
     ++ctx->launches;
@@ -462,6 +471,7 @@ extern "C" lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8
     if ((st = copy_out(ctx, start, e.start, n * D * sizeof(double))) != LAG_OK) return st;
     if ((st = copy_out(ctx, end, e.end, n * D * sizeof(double))) != LAG_OK) return st;
     if ((st = copy_out(ctx, status, e.status, n)) != LAG_OK) return st;
+    if ((st = copy_out(ctx, term_cycle, e.term_cycle, n * sizeof(int32_t))) != LAG_OK) return st;
     CK(cudaMemcpyAsync(&ctx->host_words[0], ctx->words, kWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));      // the only host sync of the write cycle
     if (n_out) *n_out = ctx->n_seeds;

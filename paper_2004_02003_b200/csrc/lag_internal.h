@@ -45,6 +45,7 @@ struct lag_ctx_s {
     double* out_start = nullptr;
     double* out_end = nullptr;
     uint8_t* out_status = nullptr;
+    int32_t* out_cycle = nullptr;
     // host-pointer staging (end-to-end path)
     float* stage[2] = {nullptr, nullptr};
     const void* stage_src[2] = {nullptr, nullptr};

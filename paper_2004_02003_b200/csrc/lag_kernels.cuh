@@ -58,6 +58,7 @@ struct AdvectArgs {
     int32_t gmin[3], gspan[3];
     int32_t bmin[3], bspan[3];
     int32_t gidx0;                  // node index of global cell gmin (local slice coordinates)
+    int32_t frozen;                 // v0 == v1: one snapshot per cycle; load corners once
     int32_t sx, sxy;                // slice pitch (nodes) of a row / a plane
     float hdth[3], qdth[3], sdth[3];// dt/h * (1/2, 1/4, 1/6)
     uint32_t bx, by;                // packed seed-node bit widths (x, y)
@@ -485,7 +486,12 @@ advect_kernel(const AdvectArgs a) {
         int cur = vindex<DIM>(a, c);
         if (!live) cur = 0;
         gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
-        gather_pairs<DIM>(a.v1, cur, a.sx, a.sxy, B);
+        if (a.frozen) {
+#pragma unroll
+            for (int i = 0; i < NP; ++i) B[i] = S[i];
+        } else {
+            gather_pairs<DIM>(a.v1, cur, a.sx, a.sxy, B);
+        }
         float k1[3];
         interp_pairs<DIM>(S, f, k1);
 #pragma unroll
@@ -504,7 +510,12 @@ advect_kernel(const AdvectArgs a) {
             if (live && st == ST_VALID && idx != cur) {
 #endif
                 gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
-                gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
+                if (a.frozen) {
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) B[i] = S[i];
+                } else {
+                    gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
+                }
 #pragma unroll
                 for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
                 cur = idx;
@@ -526,7 +537,12 @@ advect_kernel(const AdvectArgs a) {
             if (live && st == ST_VALID && idx != cur) {
 #endif
                 gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
-                gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
+                if (a.frozen) {
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) B[i] = S[i];
+                } else {
+                    gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
+                }
 #pragma unroll
                 for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
                 cur = idx;
@@ -715,6 +731,7 @@ struct ExtractArgs {
     double* start;                  // [n][dim]
     double* end;                    // [n][dim]
     uint8_t* status;                // [n]
+    int32_t* term_cycle;            // [n] or nullptr: cycle of termination, -1 if valid
 };
 
 __device__ __forceinline__ bool own_seed(const ExtractArgs& a, uint32_t w) {
@@ -740,6 +757,7 @@ static __global__ void extract_start_kernel(const ExtractArgs a) {
     const int64_t idx[3] = {i % a.ns[0], (i / a.ns[0]) % a.ns[1], i / ((int64_t)a.ns[0] * a.ns[1])};
     for (int ax = 0; ax < a.dim; ++ax)
         a.start[i * a.dim + ax] = a.o[ax] + (double)(a.first[ax] + a.stride * idx[ax]) * a.h[ax];
+    if (a.term_cycle) a.term_cycle[i] = -1;
 }
 
 static __global__ void extract_live_kernel(const ExtractArgs a) {
@@ -770,6 +788,7 @@ static __global__ void extract_dead_kernel(const ExtractArgs a) {
         for (int ax = 0; ax < a.dim; ++ax)
             a.end[s * a.dim + ax] = a.o[ax] + ((double)g[ax] + (double)d[ax]) * a.h[ax];
         a.status[s] = (uint8_t)(a.dead_info[i] >> 24);
+        if (a.term_cycle) a.term_cycle[s] = (int32_t)(a.dead_info[i] & 0xffffffu);
     }
 }
 
@@ -784,6 +803,7 @@ static __global__ void extract_returned_kernel(const ExtractArgs a) {
     for (int ax = 0; ax < a.dim; ++ax)
         a.end[s * a.dim + ax] = a.o[ax] + ((double)g[ax] + (double)d[ax]) * a.h[ax];
     a.status[s] = (uint8_t)(info >> 24);
+    if (a.term_cycle && (info >> 24) != ST_VALID) a.term_cycle[s] = (int32_t)(info & 0xffffffu);
 }
 
 }  // namespace lag

@@ -26,7 +26,7 @@ STATUS_NAMES = {0: "LAG_OK", -1: "LAG_EINVAL", -2: "LAG_ESTATE", -3: "LAG_EEMPTY
                 -8: "LAG_EGHOST", -9: "LAG_ENONFINITE"}
 
 # every symbol include/lag.h declares
-EXPORTS = ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_stats",
+EXPORTS = ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_extract_ex", "lag_stats",
            "lag_destroy", "lag_last_error", "lag_nccl_unique_id", "lag_kernel_launches",
            "lag_abi_version")
 
@@ -72,6 +72,7 @@ def load(path: str = LIB_PATH):
     lib.lag_seed.argtypes = [vp, ctypes.c_int32, P(ctypes.c_int64)]
     lib.lag_advect_cycle.argtypes = [vp, vp, vp, ctypes.c_double]
     lib.lag_extract.argtypes = [vp, vp, vp, vp, ctypes.c_int64, P(ctypes.c_int64), ctypes.c_uint32]
+    lib.lag_extract_ex.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int64, P(ctypes.c_int64), ctypes.c_uint32]
     lib.lag_stats.argtypes = [vp, P(lag_stats_t)]
     lib.lag_destroy.argtypes = [vp]
     lib.lag_last_error.argtypes = [vp]
@@ -80,7 +81,7 @@ def load(path: str = LIB_PATH):
     lib.lag_kernel_launches.argtypes = [vp]
     lib.lag_kernel_launches.restype = ctypes.c_int64
     lib.lag_abi_version.restype = ctypes.c_int32
-    for name in ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_stats",
+    for name in ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_extract_ex", "lag_stats",
                  "lag_destroy", "lag_nccl_unique_id"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -174,6 +175,17 @@ def lag_extract(ctx, start=None, end=None, status=None, capacity: Optional[int] 
     return n.value
 
 
+def lag_extract_ex(ctx, start=None, end=None, status=None, term_cycle=None,
+                   capacity: Optional[int] = None, flags: int = 0) -> int:
+    n = ctypes.c_int64(0)
+    if capacity is None:
+        caps = [x.shape[0] for x in (start, end, status, term_cycle) if x is not None]
+        capacity = min(caps) if caps else 0
+    _check(load().lag_extract_ex(ctx, _addr(start), _addr(end), _addr(status), _addr(term_cycle),
+                                 int(capacity), ctypes.byref(n), int(flags)), ctx)
+    return n.value
+
+
 def lag_stats(ctx) -> dict:
     s = lag_stats_t()
     _check(load().lag_stats(ctx, ctypes.byref(s)), ctx)
@@ -204,7 +216,9 @@ class Context:
     def advect(self, v_t, v_t1, dt: float) -> None:
         lag_advect_cycle(self.ctx, v_t, v_t1, dt)
 
-    def extract(self, start=None, end=None, status=None, flags: int = 0) -> int:
+    def extract(self, start=None, end=None, status=None, flags: int = 0, term_cycle=None) -> int:
+        if term_cycle is not None:
+            return lag_extract_ex(self.ctx, start, end, status, term_cycle, flags=flags)
         return lag_extract(self.ctx, start, end, status, flags=flags)
 
     def stats(self) -> dict:

@@ -29,7 +29,7 @@ def oracle_block(cfg, block, slices, stride, mode, g_seeds=None):
 
 
 def gpu_block(cfg, block, slices, stride, mode=0, ghost=0, host=False, device=0,
-              stream=None, extract_flags=0):
+              stream=None, extract_flags=0, term_cycle=False, same_tensor=None):
     """Run one interval of one block on the GPU through the C ABI.  Returns
     (start, end, status) as numpy arrays plus the Context stats."""
     import torch
@@ -47,12 +47,18 @@ def gpu_block(cfg, block, slices, stride, mode=0, ghost=0, host=False, device=0,
     try:
         n = ctx.seed(stride)
         for k in range(len(dev) - 1):
-            ctx.advect(dev[k], dev[k + 1], cfg["dt"])
+            if same_tensor is not None:          # frozen snapshot: v_t and v_t1 are one array
+                ctx.advect(dev[k], dev[k] if same_tensor else dev[k + 1], cfg["dt"])
+            else:
+                ctx.advect(dev[k], dev[k + 1], cfg["dt"])
         start = torch.empty((n, g.dim), dtype=torch.float64, device=f"cuda:{device}")
         end = torch.empty_like(start)
         status = torch.empty((n,), dtype=torch.uint8, device=f"cuda:{device}")
-        ctx.extract(start, end, status, flags=extract_flags)
+        tc = torch.empty((n,), dtype=torch.int32, device=f"cuda:{device}") if term_cycle else None
+        ctx.extract(start, end, status, flags=extract_flags, term_cycle=tc)
         st = ctx.stats()
+        if term_cycle:
+            st = dict(st, term_cycle=tc.cpu().numpy())
     finally:
         ctx.close()
     return start.cpu().numpy(), end.cpu().numpy(), status.cpu().numpy(), st

@@ -254,3 +254,53 @@ def test_whole_block_terminates():
     cstar = np.ceil(b0.hi[0] - x0).astype(int) - 1     # first cycle whose step lands at/after the face
     np.testing.assert_array_equal(end[:, 0], x0 + cstar)
     assert st["particle_steps"] == int((cstar + 1).sum())
+
+
+def test_frozen_snapshot_single_gather():
+    """Frozen snapshot (one accessible time step): passing the same
+    array as v_t and v_t1 gathers corners once and gives bitwise the results of
+    two distinct arrays with equal content; both match the oracle."""
+    cfg = L.make_config("C2", scale=25)
+    b = L.decompose(cfg["grid"], cfg["layout"])[1]
+    sl = global_slices(cfg, 8)
+    frozen = [sl[k] for k in range(8) for _ in (0, 1)]        # pairs (V_k, V_k)
+    # distinct arrays with identical content: slices V_k, copy(V_k)
+    a = gpu_block(cfg, b, sl, 1, same_tensor=True)
+    pairs = []
+    for k in range(8):
+        pairs += [sl[k], sl[k].copy()]
+    import torch
+    import paper_2004_02003_b200 as P
+    g = cfg["grid"]
+    dev = [torch.from_numpy(np.ascontiguousarray(L.cut_block_slice(V, g, b, 0))).cuda() for V in pairs]
+    ctx = P.Context(P.make_config(3, g.nodes, g.origin, g.spacing, b.lo, b.hi,
+                                  stream=torch.cuda.current_stream().cuda_stream))
+    n = ctx.seed(1)
+    for k in range(8):
+        ctx.advect(dev[2 * k], dev[2 * k + 1], cfg["dt"])
+    out = [torch.empty((n, 3), dtype=torch.float64, device="cuda") for _ in range(2)]
+    stt = torch.empty((n,), dtype=torch.uint8, device="cuda")
+    ctx.extract(out[0], out[1], stt)
+    ctx.close()
+    assert np.array_equal(a[1], out[1].cpu().numpy()) and np.array_equal(a[2], stt.cpu().numpy())
+    orc = oracle.Interval(g, b.lo, b.hi, 1, oracle.BTO, faces=(b.lo, b.hi))
+    for k in range(8):
+        orc.cycle(sl[k], sl[k], cfg["dt"])
+    compare(cfg, orc, *a[:3], label="frozen")
+
+
+def test_termination_cycles_match_oracle():
+    """lag_extract_ex returns the termination cycle of each non-valid flow
+    (P:884 future work: termination locations on the boundary); it equals
+    the oracle's wherever the statuses agree, -1 for valid flows."""
+    cfg = L.make_config("C2", scale=33)
+    b = L.decompose(cfg["grid"], cfg["layout"])[4]
+    sl = global_slices(cfg, 25)
+    start, end, status, st = gpu_block(cfg, b, sl, 1, term_cycle=True)
+    orc = oracle_block(cfg, b, sl, 1, oracle.BTO)
+    compare(cfg, orc, start, end, status)
+    tc = st["term_cycle"]
+    same = status == orc.status
+    assert (status != 0).sum() > 0
+    assert np.array_equal(tc[same], orc.term_cycle[same])
+    assert (tc[status == 0] == -1).all()
