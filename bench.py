@@ -489,7 +489,7 @@ def main():
                        "parallelism": f"dp{world} (one block per GPU, no collective)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(cfg["name"]),
-                         "kernel": "advect_kernel<3,true>", "peak_source": peak_src,
+                         "kernel": "advect_kernel<3,true,false>", "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes / cycles,
                          "kernel_share_of_step": adv_ms / dev_ms},
             "comm": comm,

@@ -183,9 +183,9 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     // occupancy-sized persistent grid for the advect kernel
     int occ = 1;
     if (D == 3)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<3, true> : advect_kernel<3, false>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<3, true, false> : advect_kernel<3, false, false>, kThreads, 0);
     else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<2, true> : advect_kernel<2, false>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<2, true, false> : advect_kernel<2, false, false>, kThreads, 0);
     ctx->advect_blocks_per_sm = occ > 0 ? occ : 1;
     *out = ctx;
     return LAG_OK;
@@ -367,12 +367,23 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
     int blocks = (warps + warps_per_block - 1) / warps_per_block;
 #endif
     if (blocks < 1) blocks = 1;
+    const bool bto = ctx->cfg.mode == LAG_BTO;
     if (D == 3) {
-        if (ctx->cfg.mode == LAG_BTO) advect_kernel<3, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
-        else advect_kernel<3, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
+        if (a.frozen) {
+            if (bto) advect_kernel<3, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
+            else advect_kernel<3, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
+        } else {
+            if (bto) advect_kernel<3, true, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
+            else advect_kernel<3, false, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
+        }
     } else {
-        if (ctx->cfg.mode == LAG_BTO) advect_kernel<2, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
-        else advect_kernel<2, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
+        if (a.frozen) {
+            if (bto) advect_kernel<2, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
+            else advect_kernel<2, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
+        } else {
+            if (bto) advect_kernel<2, true, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
+            else advect_kernel<2, false, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
+        }
     }
     ++ctx->launches;
     CK(cudaGetLastError());

@@ -427,7 +427,7 @@ __device__ __forceinline__ void gather_idx(const float* __restrict__ v, int idx,
     }
 }
 
-template <int DIM, bool BTO>
+template <int DIM, bool BTO, bool FROZEN>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 advect_kernel(const AdvectArgs a) {
     constexpr int NC = (1 << DIM) * DIM;             // corner floats per slice
@@ -486,7 +486,7 @@ advect_kernel(const AdvectArgs a) {
         int cur = vindex<DIM>(a, c);
         if (!live) cur = 0;
         gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
-        if (a.frozen) {
+        if constexpr (FROZEN) {
 #pragma unroll
             for (int i = 0; i < NP; ++i) B[i] = S[i];
         } else {
@@ -510,7 +510,7 @@ advect_kernel(const AdvectArgs a) {
             if (live && st == ST_VALID && idx != cur) {
 #endif
                 gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
-                if (a.frozen) {
+                if constexpr (FROZEN) {
 #pragma unroll
                     for (int i = 0; i < NP; ++i) B[i] = S[i];
                 } else {
@@ -537,7 +537,7 @@ advect_kernel(const AdvectArgs a) {
             if (live && st == ST_VALID && idx != cur) {
 #endif
                 gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
-                if (a.frozen) {
+                if constexpr (FROZEN) {
 #pragma unroll
                     for (int i = 0; i < NP; ++i) B[i] = S[i];
                 } else {

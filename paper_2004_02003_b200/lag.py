@@ -72,7 +72,8 @@ def load(path: str = LIB_PATH):
     lib.lag_seed.argtypes = [vp, ctypes.c_int32, P(ctypes.c_int64)]
     lib.lag_advect_cycle.argtypes = [vp, vp, vp, ctypes.c_double]
     lib.lag_extract.argtypes = [vp, vp, vp, vp, ctypes.c_int64, P(ctypes.c_int64), ctypes.c_uint32]
-    lib.lag_extract_ex.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int64, P(ctypes.c_int64), ctypes.c_uint32]
+    if hasattr(lib, "lag_extract_ex"):      # (older experiment builds lack it)
+        lib.lag_extract_ex.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int64, P(ctypes.c_int64), ctypes.c_uint32]
     lib.lag_stats.argtypes = [vp, P(lag_stats_t)]
     lib.lag_destroy.argtypes = [vp]
     lib.lag_last_error.argtypes = [vp]
@@ -83,7 +84,8 @@ def load(path: str = LIB_PATH):
     lib.lag_abi_version.restype = ctypes.c_int32
     for name in ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_extract_ex", "lag_stats",
                  "lag_destroy", "lag_nccl_unique_id"):
-        getattr(lib, name).restype = ctypes.c_int
+        if hasattr(lib, name):
+            getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
 

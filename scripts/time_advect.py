@@ -11,7 +11,7 @@ import lag_inputs as L  # noqa: E402
 import paper_2004_02003_b200 as P  # noqa: E402
 
 
-def main(config="C5", intervals=3, stride=None, flush_l2=True):
+def main(config="C5", intervals=3, stride=None, flush_l2=True, frozen=False):
     cfg = L.make_config(config)
     g = cfg["grid"]
     b = L.decompose(g, cfg["layout"])[0]
@@ -31,7 +31,7 @@ def main(config="C5", intervals=3, stride=None, flush_l2=True):
                 flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
-            ctx.advect(sl[c], sl[c + 1], cfg["dt"])
+            ctx.advect(sl[c], sl[c] if frozen else sl[c + 1], cfg["dt"])
             e1.record(s)
             if it > 0:
                 times.append((e0, e1))
@@ -39,7 +39,7 @@ def main(config="C5", intervals=3, stride=None, flush_l2=True):
     ms = [a.elapsed_time(b) for a, b in times]
     st = ctx.stats()
     us = 1e3 * sum(ms) / len(ms)
-    print(f"{os.environ.get('LAG_LIB', 'default')}: {config} {'flushed' if flush_l2 else 'warm-L2'} {us:.1f} us/cycle "
+    print(f"{os.environ.get('LAG_LIB', 'default')}: {config} {'flushed' if flush_l2 else 'warm-L2'}{' frozen' if frozen else ''} {us:.1f} us/cycle "
           f"(first {1e3 * ms[0]:.1f}, last {1e3 * ms[I - 1]:.1f}), "
           f"{st['particle_steps'] / (intervals + 1) / I / us * 1e-3:.2f} G p-steps/s")
     ctx.close()
@@ -47,4 +47,4 @@ def main(config="C5", intervals=3, stride=None, flush_l2=True):
 
 if __name__ == "__main__":
     main(sys.argv[1] if len(sys.argv) > 1 else "C5", int(sys.argv[2]) if len(sys.argv) > 2 else 3,
-         flush_l2="--warm" not in sys.argv)
+         flush_l2="--warm" not in sys.argv, frozen="--frozen" in sys.argv)
