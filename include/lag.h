@@ -78,6 +78,7 @@ typedef enum {
 } lag_status;
 
 typedef enum { LAG_BTO = 0, LAG_COMM = 1 } lag_mode;
+typedef enum { LAG_XCHG_NCCL = 0, LAG_XCHG_PEER = 1 } lag_exchange;
 
 /* Per-basis-flow status returned by lag_extract. */
 typedef enum {
@@ -103,7 +104,9 @@ typedef struct {
     int32_t rank;                /* COMM: this block's rank (x-fastest in layout)         */
     int32_t nranks;              /* COMM: number of ranks = prod(layout)                  */
     int32_t layout[3];           /* COMM: blocks per axis                                 */
-    int32_t pad_;
+    int32_t exchange;            /* COMM transport: LAG_XCHG_NCCL (grouped NCCL send/recv)
+                                    or LAG_XCHG_PEER (the kernels read/write the
+                                    neighbours' memory over NVLink, CUDA IPC)             */
     const void* nccl_id;         /* COMM: 128-byte ncclUniqueId shared by all ranks (from
                                     lag_nccl_unique_id on one rank); NULL for BTO         */
     void*   stream;              /* cudaStream_t the library enqueues on (borrowed);

@@ -105,6 +105,7 @@ static lag_status validate(const lag_config* c) {
         }
         if (prod != c->nranks || c->rank < 0 || c->rank >= c->nranks) { lag_set_error(ctx, "rank/nranks/layout mismatch"); return LAG_EINVAL; }
         if (c->nranks > 1 && !c->nccl_id) { lag_set_error(ctx, "COMM mode with nranks > 1 needs nccl_id"); return LAG_EINVAL; }
+        if (c->exchange != LAG_XCHG_NCCL && c->exchange != LAG_XCHG_PEER) { lag_set_error(ctx, "exchange must be LAG_XCHG_NCCL or LAG_XCHG_PEER"); return LAG_EINVAL; }
     }
     // slice extent must fit 32-bit element offsets
     int64_t nodes = 1;
@@ -401,6 +402,7 @@ static lag_status latched(lag_ctx_s* ctx, uint32_t err) {
     if (err & ERR_OVERFLOW) { lag_set_error(ctx, "latched: exchange slot or particle list overflow"); return LAG_EOVERFLOW; }
     if (err & ERR_GHOST) { lag_set_error(ctx, "latched: a stage sample left the ghost layers (CFL >= 1?)"); return LAG_EGHOST; }
     if (err & ERR_NONFINITE) { lag_set_error(ctx, "latched: non-finite velocity reached a particle"); return LAG_ENONFINITE; }
+    if (err & ERR_XCHG) { lag_set_error(ctx, "latched: peer exchange timed out waiting for a neighbour"); return LAG_ENCCL; }
     return LAG_OK;
 }
 

@@ -26,6 +26,25 @@
 
 using namespace lag;
 
+// lag_peer.cu (LAG_XCHG_PEER transport)
+struct PeerState;
+lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>& prank,
+                         const std::vector<int>& poff, const std::vector<int>& pback,
+                         const std::vector<uint32_t>& cap_recv, int64_t halo_send_floats,
+                         const std::vector<int64_t>& send_box_off, const std::vector<int64_t>& send_box_by_off,
+                         const std::vector<int>& recv_box_x0y0z0nxnynz, int64_t halo_recv_floats,
+                         PeerState** out);
+void lag_peer_destroy(PeerState* ps);
+float4* lag_peer_remote_slot(PeerState* ps, int i, int prank, int pback, int q);
+float4* lag_peer_inbox_slot(PeerState* ps, int q, int poff);
+float* lag_peer_outbox(PeerState* ps, int q);
+unsigned long long& lag_peer_seq(PeerState* ps);
+lag_status lag_peer_signal(lag_ctx_s* ctx, PeerState* ps, const std::vector<int>& prank,
+                           const std::vector<int>& pback, int kind, unsigned long long value);
+lag_status lag_peer_wait(lag_ctx_s* ctx, PeerState* ps, const std::vector<int>& poff,
+                         unsigned long long need_halo, unsigned long long need_part);
+lag_status lag_peer_unpack(lag_ctx_s* ctx, PeerState* ps, float* v0, float* v1, bool with_v0, int parity);
+
 #define CKC(call)                                                                  \
     do {                                                                           \
         cudaError_t e_ = (call);                                                   \
@@ -101,6 +120,9 @@ struct Comm {
     uint32_t* d_route_pos = nullptr;
     int64_t route_cap = 0;
     uint32_t n_returned = 0;
+    // LAG_XCHG_PEER transport
+    PeerState* peer = nullptr;
+    std::vector<int> prank, poff, pback;
 };
 
 // ---------------------------------------------------------------------------
@@ -158,11 +180,12 @@ struct AppendArgs {
     unsigned long long* counters;
     int cap_tiles;
     int npeers;
-    const float4* recv[kMaxOff];
+    float4* recv[kMaxOff];
     uint32_t cap[kMaxOff];
-    float4* slots;                  // outgoing slots: headers reset here
+    float4* slots;                  // outgoing slots: headers reset here (NCCL)
     int32_t slot_base[kMaxOff];
     int noff;
+    int zero_recv;                  // peer transport: reset the consumed inbox headers instead
 };
 
 // single block: received particles become new tiles at the end of the list
@@ -197,8 +220,12 @@ __global__ void __launch_bounds__(1024) append_kernel(AppendArgs a) {
         const uint32_t rem = total - t * kTile;
         a.tile_count[old_tiles + t] = (uint8_t)(rem >= (uint32_t)kTile ? kTile : rem);
     }
-    if (threadIdx.x < (unsigned)a.noff)
+    __syncthreads();                 // every count read before any header reset
+    if (a.zero_recv) {
+        if (threadIdx.x < (unsigned)a.npeers) *reinterpret_cast<uint32_t*>(a.recv[threadIdx.x]) = 0u;
+    } else if (threadIdx.x < (unsigned)a.noff) {
         *reinterpret_cast<uint32_t*>(a.slots + a.slot_base[threadIdx.x]) = 0u;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         a.words[W_NTILES] = old_tiles + new_tiles;
@@ -442,12 +469,31 @@ lag_status lag_comm_init(lag_ctx_s* ctx) {
     cm->route_cap = ctx->cap;
     CKC(cudaMalloc(&cm->route, sizeof(RouteRec) * std::max<int64_t>(1, cm->route_cap)));
     CKC(cudaMalloc(&cm->route_recv, sizeof(RouteRec) * std::max<int64_t>(1, cm->route_cap)));
+    for (const Peer& p : cm->peers) { cm->prank.push_back(p.rank); cm->poff.push_back(p.off); cm->pback.push_back(p.back); }
+    if (c.exchange == LAG_XCHG_PEER && !cm->peers.empty()) {
+        std::vector<uint32_t> caps;
+        std::vector<int64_t> send_off, send_by_off(kMaxOff, 0);
+        std::vector<int> rbox;
+        for (const Peer& p : cm->peers) {
+            caps.push_back(p.cap_recv);
+            const Box& sb = cm->send_boxes[(size_t)p.send_box];
+            send_off.push_back(sb.off);
+            send_by_off[p.off] = sb.off;
+            const Box& rb = cm->recv_boxes[(size_t)p.recv_box];
+            rbox.insert(rbox.end(), {rb.x0, rb.y0, rb.z0, rb.nx, rb.ny, rb.nz});
+        }
+        lag_status st = lag_peer_init(ctx, cm->nccl, cm->prank, cm->poff, cm->pback, caps,
+                                      cm->halo_send_floats, send_off, send_by_off, rbox,
+                                      cm->halo_recv_floats, &cm->peer);
+        if (st != LAG_OK) return st;
+    }
     return LAG_OK;
 }
 
 void lag_comm_destroy(lag_ctx_s* ctx) {
     Comm* cm = ctx->comm;
     if (!cm) return;
+    lag_peer_destroy(cm->peer);
     if (cm->nccl) ncclCommDestroy(cm->nccl);
     cudaFree(cm->d_send_boxes); cudaFree(cm->d_recv_boxes);
     cudaFree(cm->halo_send); cudaFree(cm->halo_recv);
@@ -466,13 +512,18 @@ lag_status lag_comm_reset(lag_ctx_s* ctx) {
     return LAG_OK;
 }
 
-static lag_status launch_append(lag_ctx_s* ctx) {
+static lag_status launch_append(lag_ctx_s* ctx, int peer_parity = -1) {
     Comm* cm = ctx->comm;
     AppendArgs a{};
     a.state = ctx->state; a.tile_count = ctx->tile_count; a.words = ctx->words;
     a.counters = ctx->counters; a.cap_tiles = ctx->cap_tiles;
     a.npeers = (int)cm->peers.size();
-    for (size_t i = 0; i < cm->peers.size(); ++i) { a.recv[i] = cm->peers[i].recv_slot; a.cap[i] = cm->peers[i].cap_recv; }
+    for (size_t i = 0; i < cm->peers.size(); ++i) {
+        a.recv[i] = peer_parity >= 0 ? lag_peer_inbox_slot(cm->peer, peer_parity, cm->peers[i].off)
+                                     : cm->peers[i].recv_slot;
+        a.cap[i] = cm->peers[i].cap_recv;
+    }
+    a.zero_recv = peer_parity >= 0 ? 1 : 0;
     a.slots = cm->slots;
     a.noff = kMaxOff;                               // all 27 offset headers (2-D uses 9..17)
     for (int k = 0; k < kMaxOff; ++k) a.slot_base[k] = cm->slot_base[k];
@@ -529,10 +580,36 @@ static lag_status exchange(lag_ctx_s* ctx, float* v0, float* v1, bool halo, bool
     return launch_append(ctx);
 }
 
+// Peer transport, one cycle: pack -> signal halo -> wait -> pull ghosts ->
+// append the previous cycle's hand-offs (see lag_peer.cu).
+static lag_status peer_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool with_v0) {
+    Comm* cm = ctx->comm;
+    const unsigned long long seq = ++lag_peer_seq(cm->peer);
+    const int q = (int)(seq & 1);
+    const int np = (int)cm->peers.size();
+    const int64_t sfl = (with_v0 ? 2 : 1) * cm->halo_send_floats;
+    if (sfl > 0) {
+        BoxArgs b{};
+        b.v0 = v0; b.v1 = v1; b.v0w = v0; b.boxes = cm->d_send_boxes; b.nbox = with_v0 ? 2 * np : np;
+        b.buf = lag_peer_outbox(cm->peer, q); b.sx = ctx->ext[0]; b.sxy = ctx->ext[0] * ctx->ext[1];
+        b.dim = ctx->cfg.dim; b.total = sfl;
+        const int blocks = (int)std::min<int64_t>((sfl + 255) / 256, (int64_t)ctx->num_sms * 8);
+        halo_pack_kernel<<<blocks, 256, 0, ctx->stream>>>(b);
+        ++ctx->launches;
+        CKC(cudaGetLastError());
+    }
+    lag_status st;
+    if ((st = lag_peer_signal(ctx, cm->peer, cm->prank, cm->pback, 0, seq)) != LAG_OK) return st;
+    if ((st = lag_peer_wait(ctx, cm->peer, cm->poff, seq, seq - 1)) != LAG_OK) return st;
+    if ((st = lag_peer_unpack(ctx, cm->peer, v0, v1, with_v0, q)) != LAG_OK) return st;
+    return launch_append(ctx, q ^ 1);
+}
+
 lag_status lag_comm_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool v0_is_prev_v1) {
     Comm* cm = ctx->comm;
     if (cm->peers.empty()) return LAG_OK;
-    lag_status st = exchange(ctx, v0, v1, true, !v0_is_prev_v1);
+    lag_status st = cm->peer ? peer_pre_advect(ctx, v0, v1, !v0_is_prev_v1)
+                             : exchange(ctx, v0, v1, true, !v0_is_prev_v1);
     cm->pending = false;
     return st;
 }
@@ -540,11 +617,25 @@ lag_status lag_comm_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool v0_is_
 void lag_comm_fill_args(lag_ctx_s* ctx, AdvectArgs* a) {
     Comm* cm = ctx->comm;
     a->slot_rec = cm->slots;
-    for (int k = 0; k < kMaxOff; ++k) { a->slot_base[k] = cm->slot_base[k]; a->slot_capv[k] = cm->slot_capv[k]; }
+    for (int k = 0; k < kMaxOff; ++k) {
+        a->slot_base[k] = cm->slot_base[k];
+        a->slot_capv[k] = cm->slot_capv[k];
+        a->slot_ptr[k] = cm->slots + cm->slot_base[k];
+    }
+    a->peer_fence = 0;
+    if (cm->peer) {
+        const int q = (int)(lag_peer_seq(cm->peer) & 1);
+        for (size_t i = 0; i < cm->peers.size(); ++i)
+            a->slot_ptr[cm->peers[i].off] = lag_peer_remote_slot(cm->peer, (int)i, cm->peers[i].rank, cm->peers[i].back, q);
+        a->peer_fence = 1;
+    }
 }
 
 lag_status lag_comm_post_advect(lag_ctx_s* ctx) {
-    ctx->comm->pending = !ctx->comm->peers.empty();
+    Comm* cm = ctx->comm;
+    cm->pending = !cm->peers.empty();
+    if (cm->peer && !cm->peers.empty())
+        return lag_peer_signal(ctx, cm->peer, cm->prank, cm->pback, 1, lag_peer_seq(cm->peer));
     return LAG_OK;
 }
 
@@ -556,7 +647,14 @@ lag_status lag_comm_return_to_origin(lag_ctx_s* ctx) {
     cm->n_returned = 0;
     if (c.nranks == 1) return LAG_OK;
     if (cm->pending) {
-        lag_status st = exchange(ctx, nullptr, nullptr, false, false);
+        lag_status st;
+        if (cm->peer) {
+            const unsigned long long seq = lag_peer_seq(cm->peer);
+            if ((st = lag_peer_wait(ctx, cm->peer, cm->poff, 0, seq)) != LAG_OK) return st;
+            st = launch_append(ctx, (int)(seq & 1));
+        } else {
+            st = exchange(ctx, nullptr, nullptr, false, false);
+        }
         if (st != LAG_OK) return st;
         cm->pending = false;
     }

@@ -38,7 +38,7 @@ constexpr int kTilesPerWarp = LAG_ADV_TPW;    // contiguous 32-particle tiles pe
 #define LAG_POLY 0       // 1: polynomial-form trilinear (coefficients per corner set)
 #endif
 
-enum : uint32_t { ERR_OVERFLOW = 1u, ERR_GHOST = 2u, ERR_NONFINITE = 4u };
+enum : uint32_t { ERR_OVERFLOW = 1u, ERR_GHOST = 2u, ERR_NONFINITE = 4u, ERR_XCHG = 8u };
 enum : int { CNT_STEPS = 0, CNT_TERM = 1, CNT_EXIT = 2, CNT_SENT = 3, CNT_RECV = 4, CNT_N = 8 };
 enum : uint8_t { ST_VALID = 0, ST_TERM = 1, ST_EXIT = 2 };
 
@@ -77,6 +77,8 @@ struct AdvectArgs {
     float4* slot_rec;
     int32_t slot_base[27];
     int32_t slot_capv[27];
+    float4* slot_ptr[27];           // slot of offset k: local (NCCL) or the owner's inbox (peer)
+    int32_t peer_fence;             // peer exchange: fence remote stores system-wide
 };
 
 __device__ __forceinline__ void unpack_g(uint32_t w, const AdvectArgs& a, int g[3]) {
@@ -629,7 +631,7 @@ advect_kernel(const AdvectArgs a) {
             if (migrate) {
                 const unsigned peers = __match_any_sync(mmask, nb);
                 const int leader = __ffs(peers) - 1;
-                float4* sb = a.slot_rec + a.slot_base[nb];
+                float4* sb = a.slot_ptr[nb];
                 uint32_t base0 = 0;
                 if (lane == leader) base0 = atomicAdd(reinterpret_cast<uint32_t*>(sb), (uint32_t)__popc(peers));
                 base0 = __shfl_sync(peers, base0, leader);
@@ -638,6 +640,7 @@ advect_kernel(const AdvectArgs a) {
                     sb[1 + pos] = make_float4(dn[0], dn[1], dn[2], r.w);
                 else
                     errbits |= ERR_OVERFLOW;
+                if (a.peer_fence) __threadfence_system();   // remote stores before the ready flag
             }
             if (lane == 0) nsent += __popc(mmask);
         }

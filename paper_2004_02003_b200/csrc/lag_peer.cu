@@ -1,0 +1,313 @@
+// lag_peer.cu — COMM mode over NVLink peer memory (exchange = LAG_XCHG_PEER):
+// the per-cycle exchange of the Lagrangian-MPI baseline done by
+// the kernels themselves, with no NCCL call on the per-cycle path.
+//
+// Every rank owns one CUDA-IPC allocation, mapped by its neighbours:
+//   flags  [2][27] u64  — "halo ready" / "particles ready" sequence numbers,
+//                         one word per sending neighbour (its offset index)
+//   inbox  [2 parities][sum over peers of (1 + cap) float4] — particle slots
+//                         the neighbours' advect kernels fill with remote stores
+//   outbox [2 parities][2 slices][halo floats] — my packed ghost sources, read
+//                         by the neighbours with remote loads
+// Per cycle (seq = 1, 2, ...; parity q = seq & 1):
+//   pack my faces -> outbox[q]; signal halo(seq) to each neighbour;
+//   wait until every neighbour signalled halo >= seq and particles >= seq-1
+//   (bounded spin, latched error on timeout); ghost layers <- neighbours'
+//   outbox[q] (remote loads); append inbox[q^1] (previous cycle's hand-offs);
+//   advect writes leaving particles into the owner's inbox[q] (remote atomics
+//   + stores); signal particles(seq).
+// Two parities suffice: a neighbour reuses parity q at seq+2 only after it
+// waited for my halo(seq+1), which I signal after consuming parity q.
+#include "lag_internal.h"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+using namespace lag;
+
+#define CKC(call)                                                                  \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess) {                                                   \
+            lag_set_error(ctx, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                          __FILE__, __LINE__);                                     \
+            return LAG_ECUDA;                                                      \
+        }                                                                          \
+    } while (0)
+#define CKN(call)                                                                  \
+    do {                                                                           \
+        ncclResult_t r_ = (call);                                                  \
+        if (r_ != ncclSuccess) {                                                   \
+            lag_set_error(ctx, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_),    \
+                          __FILE__, __LINE__);                                     \
+            return LAG_ENCCL;                                                      \
+        }                                                                          \
+    } while (0)
+
+namespace lag {
+
+constexpr int kOff = 27;
+constexpr int kMaxPeers = 26;
+// per-rank layout table published to every rank (int64 words)
+enum : int { T_INBOX = 0, T_INBOX_PAR = 1, T_OUTBOX = 2, T_HALO = 3, T_RECV = 4, T_SEND = 4 + kOff,
+             T_WORDS = 4 + 2 * kOff };
+
+struct PeerBox {            // one ghost box to fill from a remote outbox
+    int x0, y0, z0, nx, ny, nz;
+    int64_t off;            // float offset of this box in the flattened copy
+    const float* src[2][2]; // [parity][slice 0 = v_t, 1 = v_t1] remote source
+    int slice;
+};
+
+struct PeerArgs {
+    // wait
+    const unsigned long long* my_flags;   // [2][27]
+    int npeers;
+    int back[kMaxPeers];                  // offset index of each peer as seen from me
+    unsigned long long need_halo, need_part;
+    uint32_t* err;
+    long long timeout_cycles;
+    // signal
+    unsigned long long* remote_flags[kMaxPeers];  // neighbour's flags base
+    int my_index_at_peer[kMaxPeers];              // my offset index as seen from the peer
+    int kind;                                     // 0 = halo, 1 = particles
+    unsigned long long value;
+};
+
+__global__ void peer_signal_kernel(PeerArgs a) {
+    const int p = threadIdx.x;
+    if (p >= a.npeers) return;
+    __threadfence_system();                       // prior packs / remote stores visible first
+    volatile unsigned long long* f = a.remote_flags[p] + a.kind * kOff + a.my_index_at_peer[p];
+    *f = a.value;
+    __threadfence_system();
+}
+
+__global__ void peer_wait_kernel(PeerArgs a) {
+    const int p = threadIdx.x;
+    if (p < a.npeers) {
+        const volatile unsigned long long* fh = a.my_flags + 0 * kOff + a.back[p];
+        const volatile unsigned long long* fp = a.my_flags + 1 * kOff + a.back[p];
+        const long long t0 = clock64();
+        while (*fh < a.need_halo || *fp < a.need_part) {
+            if (clock64() - t0 > a.timeout_cycles) { atomicOr(a.err, ERR_XCHG); break; }
+            __nanosleep(200);
+        }
+        __threadfence_system();
+    }
+}
+
+struct PeerUnpackArgs {
+    float* v0;
+    float* v1;
+    const PeerBox* boxes;
+    int nbox;
+    int parity;
+    int sx, sxy, dim;
+    int64_t total;
+};
+
+__global__ void peer_unpack_kernel(PeerUnpackArgs a) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int k = 0;
+        while (k + 1 < a.nbox && a.boxes[k + 1].off <= i) ++k;
+        const PeerBox& b = a.boxes[k];
+        const int64_t j = i - b.off;
+        const int comp = (int)(j % a.dim);
+        const int64_t node = j / a.dim;
+        const int x = (int)(node % b.nx), y = (int)((node / b.nx) % b.ny), z = (int)(node / ((int64_t)b.nx * b.ny));
+        float* dst = b.slice ? a.v1 : a.v0;
+        dst[(int64_t)a.dim * ((b.x0 + x) + (int64_t)a.sx * (b.y0 + y) + (int64_t)a.sxy * (b.z0 + z)) + comp] =
+            b.src[a.parity][b.slice][j];
+    }
+}
+
+}  // namespace lag
+
+// ---------------------------------------------------------------------------
+
+struct PeerState {
+    char* mem = nullptr;                      // my IPC allocation
+    size_t bytes = 0;
+    std::vector<char*> remote;                // per peer: mapped neighbour allocation
+    std::vector<int64_t> table;               // nranks * T_WORDS
+    unsigned long long* flags = nullptr;      // mine
+    float4* inbox[2] = {nullptr, nullptr};
+    float* outbox = nullptr;                  // [2][2][halo]
+    std::vector<lag::PeerBox> boxes;          // v1 boxes then v0 boxes
+    lag::PeerBox* d_boxes = nullptr;
+    int64_t halo_recv_floats = 0;
+    int64_t halo_send_floats = 0;
+    std::vector<int64_t> my_table;            // my own layout words
+    unsigned long long seq = 0;
+};
+
+lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>& prank,
+                         const std::vector<int>& poff, const std::vector<int>& pback,
+                         const std::vector<uint32_t>& cap_recv, int64_t halo_send_floats,
+                         const std::vector<int64_t>& send_box_off, const std::vector<int64_t>& send_box_by_off,
+                         const std::vector<int>& recv_box_x0y0z0nxnynz, int64_t halo_recv_floats,
+                         PeerState** out) {
+    *out = nullptr;
+    PeerState* ps = new PeerState();
+    const int R = ctx->cfg.nranks;
+    const int np = (int)prank.size();
+    // my layout: flags | inbox[2] | outbox[2][2]
+    int64_t inbox_f4 = 0;
+    std::vector<int64_t> recv_off(kOff, -1);
+    for (int i = 0; i < np; ++i) { recv_off[pback[i] >= 0 ? poff[i] : 0] = inbox_f4; inbox_f4 += cap_recv[i] + 1; }
+    const size_t flags_bytes = 2 * kOff * sizeof(unsigned long long);
+    const size_t inbox_off = 256;
+    const size_t inbox_bytes = (size_t)std::max<int64_t>(1, inbox_f4) * sizeof(float4);
+    const size_t outbox_off = inbox_off + 2 * inbox_bytes;
+    const size_t outbox_bytes = (size_t)std::max<int64_t>(1, halo_send_floats) * sizeof(float);
+    ps->bytes = outbox_off + 4 * outbox_bytes;
+    (void)flags_bytes;
+    CKC(cudaMalloc(&ps->mem, ps->bytes));
+    CKC(cudaMemset(ps->mem, 0, ps->bytes));
+    ps->flags = reinterpret_cast<unsigned long long*>(ps->mem);
+    ps->inbox[0] = reinterpret_cast<float4*>(ps->mem + inbox_off);
+    ps->inbox[1] = reinterpret_cast<float4*>(ps->mem + inbox_off + inbox_bytes);
+    ps->outbox = reinterpret_cast<float*>(ps->mem + outbox_off);
+    ps->halo_recv_floats = halo_recv_floats;
+    ps->halo_send_floats = std::max<int64_t>(1, halo_send_floats);
+    // publish layout + IPC handle
+    std::vector<int64_t> mine(T_WORDS, -1);
+    mine[T_INBOX] = (int64_t)inbox_off;
+    mine[T_INBOX_PAR] = (int64_t)inbox_bytes;
+    mine[T_OUTBOX] = (int64_t)outbox_off;
+    mine[T_HALO] = halo_send_floats;
+    for (int k = 0; k < kOff; ++k) { mine[T_RECV + k] = recv_off[k]; mine[T_SEND + k] = send_box_by_off[k]; }
+    ps->my_table = mine;
+    cudaIpcMemHandle_t h;
+    CKC(cudaIpcGetMemHandle(&h, ps->mem));
+    const size_t rec = T_WORDS * sizeof(int64_t) + sizeof(h);
+    std::vector<char> host(rec * (R + 1));
+    std::memcpy(host.data(), mine.data(), T_WORDS * sizeof(int64_t));
+    std::memcpy(host.data() + T_WORDS * sizeof(int64_t), &h, sizeof(h));
+    char* d = nullptr;
+    CKC(cudaMalloc(&d, rec * (R + 1)));
+    CKC(cudaMemcpyAsync(d, host.data(), rec, cudaMemcpyHostToDevice, ctx->stream));
+    CKN(ncclAllGather(d, d + rec, rec, ncclUint8, nccl, ctx->stream));
+    CKC(cudaMemcpyAsync(host.data() + rec, d + rec, rec * R, cudaMemcpyDeviceToHost, ctx->stream));
+    CKC(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d);
+    ps->table.assign((size_t)R * T_WORDS, 0);
+    ps->remote.assign(np, nullptr);
+    for (int r = 0; r < R; ++r)
+        std::memcpy(&ps->table[(size_t)r * T_WORDS], host.data() + rec * (r + 1), T_WORDS * sizeof(int64_t));
+    for (int i = 0; i < np; ++i) {
+        cudaIpcMemHandle_t hr;
+        std::memcpy(&hr, host.data() + rec * (prank[i] + 1) + T_WORDS * sizeof(int64_t), sizeof(hr));
+        void* ptr = nullptr;
+        CKC(cudaIpcOpenMemHandle(&ptr, hr, cudaIpcMemLazyEnablePeerAccess));
+        ps->remote[i] = (char*)ptr;
+    }
+    // ghost boxes to pull: for peer i, its outbox box toward me (my index at it = back)
+    for (int slice = 1; slice >= 0; --slice) {
+        int64_t off = 0;
+        for (int i = 0; i < np; ++i) {
+            const int* bx = &recv_box_x0y0z0nxnynz[6 * i];
+            PeerBox b{};
+            b.x0 = bx[0]; b.y0 = bx[1]; b.z0 = bx[2]; b.nx = bx[3]; b.ny = bx[4]; b.nz = bx[5];
+            b.slice = slice;
+            const int64_t* t = &ps->table[(size_t)prank[i] * T_WORDS];
+            // peer's outbox parity q = [v_t1 boxes | v_t boxes] (the pack-buffer layout)
+            for (int q = 0; q < 2; ++q)
+                for (int sl = 0; sl < 2; ++sl)
+                    b.src[q][sl] = reinterpret_cast<const float*>(ps->remote[i] + t[T_OUTBOX] +
+                                   (size_t)(q * 2 + (sl == 1 ? 0 : 1)) * std::max<int64_t>(1, t[T_HALO]) * sizeof(float)) +
+                                   t[T_SEND + pback[i]];
+            b.off = off + (slice == 0 ? halo_recv_floats : 0);
+            off += (int64_t)b.nx * b.ny * b.nz * ctx->cfg.dim;
+            ps->boxes.push_back(b);
+        }
+    }
+    CKC(cudaMalloc(&ps->d_boxes, sizeof(PeerBox) * std::max<size_t>(1, ps->boxes.size())));
+    if (!ps->boxes.empty())
+        CKC(cudaMemcpy(ps->d_boxes, ps->boxes.data(), sizeof(PeerBox) * ps->boxes.size(), cudaMemcpyHostToDevice));
+    (void)send_box_off;
+    *out = ps;
+    return LAG_OK;
+}
+
+void lag_peer_destroy(PeerState* ps) {
+    if (!ps) return;
+    for (char* p : ps->remote) if (p) cudaIpcCloseMemHandle(p);
+    cudaFree(ps->d_boxes);
+    cudaFree(ps->mem);
+    delete ps;
+}
+
+// remote inbox slot (parity q) that I (sending toward peer i) fill
+float4* lag_peer_remote_slot(PeerState* ps, int i, int prank, int pback, int q) {
+    const int64_t* t = &ps->table[(size_t)prank * T_WORDS];
+    return reinterpret_cast<float4*>(ps->remote[i] + t[T_INBOX] + (size_t)q * t[T_INBOX_PAR]) + t[T_RECV + pback];
+}
+
+lag_status lag_peer_signal(lag_ctx_s* ctx, PeerState* ps, const std::vector<int>& prank,
+                           const std::vector<int>& pback, int kind, unsigned long long value) {
+    const int np = (int)prank.size();
+    if (np == 0) return LAG_OK;
+    PeerArgs a{};
+    a.npeers = np;
+    a.kind = kind;
+    a.value = value;
+    for (int i = 0; i < np; ++i) {
+        a.remote_flags[i] = reinterpret_cast<unsigned long long*>(ps->remote[i]);
+        a.my_index_at_peer[i] = pback[i];
+    }
+    peer_signal_kernel<<<1, 32, 0, ctx->stream>>>(a);
+    ++ctx->launches;
+    CKC(cudaGetLastError());
+    return LAG_OK;
+}
+
+lag_status lag_peer_wait(lag_ctx_s* ctx, PeerState* ps, const std::vector<int>& poff,
+                         unsigned long long need_halo, unsigned long long need_part) {
+    const int np = (int)poff.size();
+    if (np == 0) return LAG_OK;
+    PeerArgs a{};
+    a.my_flags = ps->flags;
+    a.npeers = np;
+    for (int i = 0; i < np; ++i) a.back[i] = poff[i];     // the peer writes at its offset index from me
+    a.need_halo = need_halo;
+    a.need_part = need_part;
+    a.err = ctx->words + W_ERR;
+    a.timeout_cycles = 8000000000LL;                      // ~4 s at 2 GHz
+    peer_wait_kernel<<<1, 32, 0, ctx->stream>>>(a);
+    ++ctx->launches;
+    CKC(cudaGetLastError());
+    return LAG_OK;
+}
+
+lag_status lag_peer_unpack(lag_ctx_s* ctx, PeerState* ps, float* v0, float* v1, bool with_v0, int parity) {
+    const int nb = (int)ps->boxes.size() / 2;
+    if (nb == 0) return LAG_OK;
+    PeerUnpackArgs u{};
+    u.v0 = v0; u.v1 = v1;
+    u.boxes = ps->d_boxes;                                // v1 boxes first, then v0 boxes
+    u.nbox = with_v0 ? 2 * nb : nb;
+    u.parity = parity;
+    u.sx = ctx->ext[0]; u.sxy = ctx->ext[0] * ctx->ext[1]; u.dim = ctx->cfg.dim;
+    u.total = (with_v0 ? 2 : 1) * ps->halo_recv_floats;
+    const int blocks = (int)std::min<int64_t>((u.total + 255) / 256, (int64_t)ctx->num_sms * 8);
+    peer_unpack_kernel<<<std::max(1, blocks), 256, 0, ctx->stream>>>(u);
+    ++ctx->launches;
+    CKC(cudaGetLastError());
+    return LAG_OK;
+}
+
+float4* lag_peer_inbox_slot(PeerState* ps, int q, int poff) {
+    // my inbox slot (parity q) filled by the neighbour at offset index poff
+    const int64_t* t = ps->my_table.data();
+    return ps->inbox[q] + t[T_RECV + poff];
+}
+
+float* lag_peer_outbox(PeerState* ps, int q) { return ps->outbox + (size_t)q * 2 * ps->halo_send_floats; }
+
+unsigned long long& lag_peer_seq(PeerState* ps) { return ps->seq; }

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("LAG_LIB") or os.path.join(HERE, "liblag.so")
 LAG_OK, LAG_EINVAL, LAG_ESTATE, LAG_EEMPTY, LAG_ENOMEM = 0, -1, -2, -3, -4
 LAG_ECUDA, LAG_ENCCL, LAG_EOVERFLOW, LAG_EGHOST, LAG_ENONFINITE = -5, -6, -7, -8, -9
 LAG_BTO, LAG_COMM = 0, 1
+LAG_XCHG_NCCL, LAG_XCHG_PEER = 0, 1
 LAG_VALID, LAG_TERM_BOUNDARY, LAG_EXIT_DOMAIN = 0, 1, 2
 LAG_NO_RESEED = 1
 STATUS_NAMES = {0: "LAG_OK", -1: "LAG_EINVAL", -2: "LAG_ESTATE", -3: "LAG_EEMPTY",
@@ -43,7 +44,7 @@ class lag_config(ctypes.Structure):
                 ("spacing", ctypes.c_double * 3), ("block_lo", ctypes.c_int64 * 3),
                 ("block_hi", ctypes.c_int64 * 3), ("ghost", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
-                ("layout", ctypes.c_int32 * 3), ("pad_", ctypes.c_int32),
+                ("layout", ctypes.c_int32 * 3), ("exchange", ctypes.c_int32),
                 ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
 
 
@@ -130,10 +131,12 @@ def make_config(dim: int, global_nodes: Sequence[int], origin: Sequence[float],
                 spacing: Sequence[float], block_lo: Sequence[int], block_hi: Sequence[int],
                 mode: int = LAG_BTO, ghost: int = 0, device: int = 0, rank: int = 0,
                 nranks: int = 1, layout: Sequence[int] = (1, 1, 1),
-                nccl_id: Optional[bytes] = None, stream: Optional[int] = None) -> lag_config:
+                nccl_id: Optional[bytes] = None, stream: Optional[int] = None,
+                exchange: int = 0) -> lag_config:
     c = lag_config()
     c.dim, c.mode, c.ghost, c.device = dim, mode, ghost, device
     c.rank, c.nranks = rank, nranks
+    c.exchange = int(exchange)
     for a in range(3):
         c.global_nodes[a] = int(global_nodes[a])
         c.origin[a] = float(origin[a])

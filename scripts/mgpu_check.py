@@ -29,7 +29,7 @@ import lag_inputs as L  # noqa: E402
 import paper_2004_02003_b200 as P  # noqa: E402
 
 
-def run_block(cfg, block, layout, rank, world, mode, slices, stride, nccl_id=None):
+def run_block(cfg, block, layout, rank, world, mode, slices, stride, nccl_id=None, exchange=0):
     g = cfg["grid"]
     ghost = 1 if mode == P.LAG_COMM else 0
     lo = [block.lo[a] - ghost if a < g.dim else 0 for a in range(3)]
@@ -41,7 +41,7 @@ def run_block(cfg, block, layout, rank, world, mode, slices, stride, nccl_id=Non
                        ghost=ghost, device=torch.cuda.current_device(), rank=rank,
                        nranks=world if mode == P.LAG_COMM else 1,
                        layout=layout if mode == P.LAG_COMM else (1, 1, 1),
-                       nccl_id=nccl_id, stream=s.cuda_stream)
+                       nccl_id=nccl_id, stream=s.cuda_stream, exchange=exchange)
     ctx = P.Context(pc)
     n = ctx.seed(stride)
     for k in range(len(dev) - 1):
@@ -80,10 +80,16 @@ def main():
     dist.broadcast_object_list(obj, src=0)
     t0 = time.time()
     comm = run_block(cfg, me, layout, rank, world, P.LAG_COMM, slices, stride, nccl_id=obj[0])
+    obj2 = [P.lag_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj2, src=0)
+    peer = run_block(cfg, me, layout, rank, world, P.LAG_COMM, slices, stride, nccl_id=obj2[0],
+                     exchange=P.LAG_XCHG_PEER)
     bto = run_block(cfg, me, layout, rank, world, P.LAG_BTO, slices, stride)
     comm_all = [None] * world
     bto_all = [None] * world
+    peer_all = [None] * world
     dist.all_gather_object(comm_all, comm)
+    dist.all_gather_object(peer_all, peer)
     dist.all_gather_object(bto_all, bto)
     ok = True
     report = dict(config=config, scale=scale, world=world, layout=list(layout), cycles=ncyc)
@@ -103,6 +109,13 @@ def main():
                 if not np.array_equal(arr_c, arr_s[idx]):
                     mism += 1
         report["comm_vs_single_bitwise_mismatching_arrays"] = mism
+        pm = sum(int(not np.array_equal(x, y)) for c, pz in zip(comm_all, peer_all) for x, y in zip(c[:3], pz[:3]))
+        psent = sum(int(c[3]["sent"]) for c in peer_all)
+        precv = sum(int(c[3]["received"]) for c in peer_all)
+        report["peer_vs_nccl_bitwise_mismatching_arrays"] = pm
+        report["peer_sent"] = psent
+        report["peer_received"] = precv
+        ok &= pm == 0 and psent == precv and psent == sent
         report["sent"] = sent
         report["received"] = recv
         ok &= mism == 0 and sent == recv and sent > 0

@@ -30,3 +30,4 @@ def test_mgpu_comm_and_bto(nproc, config, scale):
     assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
     rep = json.loads(lines[-1])
     assert rep["ok"] and rep["sent"] > 0 and rep["comm_vs_single_bitwise_mismatching_arrays"] == 0
+    assert rep["peer_vs_nccl_bitwise_mismatching_arrays"] == 0 and rep["peer_sent"] == rep["sent"]
