@@ -161,7 +161,8 @@ lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>
     std::vector<int64_t> recv_off(kOff, -1);
     for (int i = 0; i < np; ++i) { recv_off[pback[i] >= 0 ? poff[i] : 0] = inbox_f4; inbox_f4 += cap_recv[i] + 1; }
     const size_t flags_bytes = 2 * kOff * sizeof(unsigned long long);
-    const size_t inbox_off = 256;
+    const size_t inbox_off = 512;                       // after the 2 x 27 u64 flags (432 B)
+    static_assert(2 * kOff * sizeof(unsigned long long) <= 512, "flags overlap the inbox");
     const size_t inbox_bytes = (size_t)std::max<int64_t>(1, inbox_f4) * sizeof(float4);
     const size_t outbox_off = inbox_off + 2 * inbox_bytes;
     const size_t outbox_bytes = (size_t)std::max<int64_t>(1, halo_send_floats) * sizeof(float);
