@@ -174,7 +174,7 @@ class Arm:
     """One block of the weak-scaling layout on this rank, driven through the
     C ABI binding (paper_2004_02003_b200)."""
 
-    def __init__(self, cfg, rank, world, mode, nccl_id=None, host=False):
+    def __init__(self, cfg, rank, world, mode, nccl_id=None, host=False, exchange=0):
         import torch
         import lag_inputs as L
         import paper_2004_02003_b200 as P
@@ -199,7 +199,7 @@ class Arm:
                            mode=mode, ghost=self.ghost, device=torch.cuda.current_device(),
                            rank=rank, nranks=world if mode == P.LAG_COMM else 1,
                            layout=cfg["layout"] if mode == P.LAG_COMM else (1, 1, 1),
-                           nccl_id=nccl_id, stream=self.stream.cuda_stream)
+                           nccl_id=nccl_id, stream=self.stream.cuda_stream, exchange=exchange)
         self.ctx = P.Context(pc)
         self.n = self.ctx.seed(cfg["stride"])
         dev = "cpu" if host else "cuda"
@@ -439,24 +439,33 @@ def main():
     del arm
 
     # ---------------- comm baseline (Lagrangian-MPI analogue) ----------------
+    # both transports; the BTO speed-up is quoted against the faster one
     comm = None
     if not args.no_comm:
-        nid = broadcast_bytes(P.lag_nccl_unique_id() if rank == 0 else None, world, rank) if world > 1 else None
-        carm = Arm(cfg, rank, world, P.LAG_COMM, nccl_id=nid)
-        run_arm(carm, args.warmup, flush)
-        barrier(world)
-        c_adv, c_other, c_ps = run_arm(carm, args.steps, flush)
-        c_ms = allreduce_max(sum(c_adv) + sum(c_other), world)
-        c_total = allreduce_sum(c_ps, world)
-        cst = carm.ctx.stats()
-        comm = {"value": c_total / (c_ms / 1e3), "unit": UNIT,
-                "ms_per_step": c_ms / args.steps,
-                "ms_per_cycle": allreduce_max(sum(c_adv), world) / cycles,
-                "bto_speedup": (c_ms / dev_ms_max),
-                "sent_last_interval": int(cst["sent"]), "received_last_interval": int(cst["received"]),
-                "exchange": "NCCL grouped send/recv per cycle: halo (G=1, faces+edges+corners) + particle slots"}
-        carm.ctx.close()
-        del carm
+        comm = {}
+        transports = [("nccl", P.LAG_XCHG_NCCL)] + ([("peer", P.LAG_XCHG_PEER)] if world > 1 else [])
+        for tname, xch in transports:
+            nid = broadcast_bytes(P.lag_nccl_unique_id() if rank == 0 else None, world, rank) if world > 1 else None
+            carm = Arm(cfg, rank, world, P.LAG_COMM, nccl_id=nid, exchange=xch)
+            run_arm(carm, args.warmup, flush)
+            barrier(world)
+            c_adv, c_other, c_ps = run_arm(carm, args.steps, flush)
+            c_ms = allreduce_max(sum(c_adv) + sum(c_other), world)
+            c_total = allreduce_sum(c_ps, world)
+            cst = carm.ctx.stats()
+            comm[tname] = {"value": c_total / (c_ms / 1e3), "unit": UNIT,
+                           "ms_per_step": c_ms / args.steps,
+                           "ms_per_cycle": allreduce_max(sum(c_adv), world) / cycles,
+                           "bto_speedup": (c_ms / dev_ms_max),
+                           "sent_last_interval": int(cst["sent"]),
+                           "received_last_interval": int(cst["received"])}
+            carm.ctx.close()
+            del carm
+        best = max(comm.values(), key=lambda d: d["value"])
+        comm.update({"value": best["value"], "unit": UNIT, "bto_speedup": best["bto_speedup"],
+                     "exchange": "per cycle: ghost layer (G=1, faces+edges+corners) of v_t1 + particle "
+                                 "hand-offs; 'nccl' = one grouped NCCL send/recv, 'peer' = kernels read / "
+                                 "write the neighbours' memory over NVLink (CUDA IPC); value/speedup = faster"})
 
     secondary = None
     if not args.no_secondary:
