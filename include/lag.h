@@ -124,6 +124,8 @@ typedef struct {
     int64_t cycles;          /* cumulative lag_advect_cycle calls since lag_init            */
     int32_t device_error;    /* latched async condition as a lag_status (0 = none)          */
     int32_t pad_;
+    double  phase_ms[3];     /* with env LAG_PHASE_TIMING=1: cumulative device time of the
+                                pre-advect exchange, the advect kernel, the post-advect signal */
 } lag_stats_t;
 
 /*

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -188,6 +189,13 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<2, true, false> : advect_kernel<2, false, false>, kThreads, 0);
     ctx->advect_blocks_per_sm = occ > 0 ? occ : 1;
+    {
+        const char* pt = getenv("LAG_PHASE_TIMING");
+        ctx->phase_timing = pt && pt[0] == '1';
+        if (ctx->phase_timing)
+            for (int i = 0; i < 64; ++i)
+                for (int j = 0; j < 4; ++j) cudaEventCreate(&ctx->ph_ev[i][j]);
+    }
     *out = ctx;
     return LAG_OK;
 }
@@ -199,6 +207,9 @@ extern "C" lag_status lag_destroy(lag_ctx ctx) {
     lag_comm_destroy(ctx);
     dfree(ctx->state); dfree(ctx->tile_count); dfree(ctx->dead_rec); dfree(ctx->dead_info);
     dfree(ctx->words); dfree(ctx->counters); dfree(ctx->out_start); dfree(ctx->out_end);
+    if (ctx->phase_timing)
+        for (int i = 0; i < 64; ++i)
+            for (int j = 0; j < 4; ++j) cudaEventDestroy(ctx->ph_ev[i][j]);
     dfree(ctx->out_status); dfree(ctx->out_cycle); dfree(ctx->stage[0]); dfree(ctx->stage[1]);
     delete ctx;
     return LAG_OK;
@@ -300,6 +311,16 @@ static lag_status resolve_slice(lag_ctx_s* ctx, void* p, int avoid, float** out,
     return LAG_OK;
 }
 
+// Fold recorded phase events into ph_ms (synchronises on the events).
+static void fold_phases(lag_ctx_s* ctx) {
+    for (int i = 0; i < ctx->ph_n; ++i) {
+        float ms;
+        for (int j = 0; j < 3; ++j)
+            if (cudaEventElapsedTime(&ms, ctx->ph_ev[i][j], ctx->ph_ev[i][j + 1]) == cudaSuccess) ctx->ph_ms[j] += ms;
+    }
+    ctx->ph_n = 0;
+}
+
 extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, double dt) {
     if (!ctx) { lag_set_error(nullptr, "ctx is NULL"); return LAG_EINVAL; }
     if (!ctx->seeded) { lag_set_error(ctx, "lag_advect_cycle before lag_seed"); return LAG_ESTATE; }
@@ -313,10 +334,14 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
     if ((st = resolve_slice(ctx, v_t, -1, &d0, &s0)) != LAG_OK) return st;
     if ((st = resolve_slice(ctx, v_t1, s0, &d1, &s1)) != LAG_OK) return st;
     const int D = ctx->cfg.dim;
+    if (ctx->phase_timing && ctx->ph_n == 64) fold_phases(ctx);
+    cudaEvent_t* ev = ctx->phase_timing ? ctx->ph_ev[ctx->ph_n++] : nullptr;
+    if (ev) cudaEventRecord(ev[0], ctx->stream);
     if (ctx->cfg.mode == LAG_COMM) {
         st = lag_comm_pre_advect(ctx, d0, d1, v_t == ctx->last_v1);
         if (st != LAG_OK) return st;
     }
+    if (ev) cudaEventRecord(ev[1], ctx->stream);
     AdvectArgs a{};
     a.v0 = d0; a.v1 = d1;
     a.frozen = d0 == d1 ? 1 : 0;
@@ -388,10 +413,12 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
     }
     ++ctx->launches;
     CK(cudaGetLastError());
+    if (ev) cudaEventRecord(ev[2], ctx->stream);
     if (ctx->cfg.mode == LAG_COMM) {
         st = lag_comm_post_advect(ctx);
         if (st != LAG_OK) return st;
     }
+    if (ev) cudaEventRecord(ev[3], ctx->stream);
     ctx->last_v1 = v_t1;
     ++ctx->cycles_in_interval;
     ++ctx->cycles_total;
@@ -515,5 +542,9 @@ extern "C" lag_status lag_stats(lag_ctx ctx, lag_stats_t* out) {
     out->cycles = ctx->cycles_total;
     out->active = out->seeded + out->received - out->sent - out->term_boundary - out->exit_domain;
     out->device_error = (int32_t)latched(ctx, ctx->host_words[W_ERR]);
+    if (ctx->phase_timing) {
+        fold_phases(ctx);
+        out->phase_ms[0] = ctx->ph_ms[0]; out->phase_ms[1] = ctx->ph_ms[1]; out->phase_ms[2] = ctx->ph_ms[2];
+    }
     return LAG_OK;
 }

@@ -52,6 +52,11 @@ struct lag_ctx_s {
     const void* last_v1 = nullptr;
     // COMM
     lag::Comm* comm = nullptr;
+    // phase timing (LAG_PHASE_TIMING=1): events around pre-exchange / advect / post
+    bool phase_timing = false;
+    cudaEvent_t ph_ev[64][4] = {};
+    int ph_n = 0;
+    double ph_ms[3] = {0.0, 0.0, 0.0};
 };
 
 int lag_set_error(lag_ctx_s* ctx, const char* fmt, ...);

@@ -53,7 +53,8 @@ class lag_stats_t(ctypes.Structure):
                 ("term_boundary", ctypes.c_int64), ("exit_domain", ctypes.c_int64),
                 ("sent", ctypes.c_int64), ("received", ctypes.c_int64),
                 ("particle_steps", ctypes.c_int64), ("cycles", ctypes.c_int64),
-                ("device_error", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+                ("device_error", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("phase_ms", ctypes.c_double * 3)]
 
 
 _lib = None
@@ -194,7 +195,9 @@ def lag_extract_ex(ctx, start=None, end=None, status=None, term_cycle=None,
 def lag_stats(ctx) -> dict:
     s = lag_stats_t()
     _check(load().lag_stats(ctx, ctypes.byref(s)), ctx)
-    return {f: getattr(s, f) for f, _ in lag_stats_t._fields_ if f != "pad_"}
+    d = {f: getattr(s, f) for f, _ in lag_stats_t._fields_ if f not in ("pad_", "phase_ms")}
+    d["phase_ms"] = list(s.phase_ms)
+    return d
 
 
 def lag_destroy(ctx) -> None:
