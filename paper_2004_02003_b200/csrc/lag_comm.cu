@@ -17,6 +17,7 @@
 // to its origin rank ("each compute node returns its particles to
 // their originating nodes"; untimed write cycle).
 #include "lag_internal.h"
+#include "lag_append.cuh"
 
 #include <nccl.h>
 
@@ -44,6 +45,12 @@ lag_status lag_peer_signal(lag_ctx_s* ctx, PeerState* ps, const std::vector<int>
 lag_status lag_peer_wait(lag_ctx_s* ctx, PeerState* ps, const std::vector<int>& poff,
                          unsigned long long need_halo, unsigned long long need_part);
 lag_status lag_peer_unpack(lag_ctx_s* ctx, PeerState* ps, float* v0, float* v1, bool with_v0, int parity);
+uint32_t* lag_peer_done_counter(PeerState* ps);
+unsigned long long* lag_peer_remote_flag(PeerState* ps, int i, int kind, int pback);
+lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_boxes, int nsend,
+                             int64_t sfl, float* v0, float* v1, bool with_v0, bool halo,
+                             const std::vector<int>& poff, const std::vector<int>& pback,
+                             unsigned long long need_part, const void* append_args);
 
 #define CKC(call)                                                                  \
     do {                                                                           \
@@ -66,14 +73,7 @@ lag_status lag_peer_unpack(lag_ctx_s* ctx, PeerState* ps, float* v0, float* v1, 
 
 namespace lag {
 
-constexpr int kMaxOff = 27;
 constexpr int kMaxCuts = 65;
-
-struct Box {            // local slice coordinates
-    int x0, y0, z0, nx, ny, nz;
-    int64_t off;        // float offset in the pack buffer
-    int slice;          // 0 = v_t, 1 = v_t1
-};
 
 struct RouteRec {       // return-to-origin record (32 B)
     float4 rec;
@@ -170,66 +170,6 @@ __global__ void halo_unpack_kernel(BoxArgs a) {
         const int x = (int)(node % b.nx), y = (int)((node / b.nx) % b.ny), z = (int)(node / ((int64_t)b.nx * b.ny));
         float* dst = b.slice ? a.v1 : a.v0w;
         dst[(int64_t)a.dim * ((b.x0 + x) + (int64_t)a.sx * (b.y0 + y) + (int64_t)a.sxy * (b.z0 + z)) + comp] = a.buf[i];
-    }
-}
-
-struct AppendArgs {
-    float4* state;
-    uint8_t* tile_count;
-    uint32_t* words;
-    unsigned long long* counters;
-    int cap_tiles;
-    int npeers;
-    float4* recv[kMaxOff];
-    uint32_t cap[kMaxOff];
-    float4* slots;                  // outgoing slots: headers reset here (NCCL)
-    int32_t slot_base[kMaxOff];
-    int noff;
-    int zero_recv;                  // peer transport: reset the consumed inbox headers instead
-};
-
-// single block: received particles become new tiles at the end of the list
-__global__ void __launch_bounds__(1024) append_kernel(AppendArgs a) {
-    __shared__ uint32_t pre[kMaxOff + 1];
-    __shared__ uint32_t old_tiles;
-    if (threadIdx.x == 0) {
-        uint32_t s = 0;
-        for (int p = 0; p < a.npeers; ++p) {
-            pre[p] = s;
-            uint32_t c = *reinterpret_cast<const uint32_t*>(a.recv[p]);
-            if (c > a.cap[p]) { c = a.cap[p]; atomicOr(a.words + W_ERR, ERR_OVERFLOW); }
-            s += c;
-        }
-        pre[a.npeers] = s;
-        old_tiles = a.words[W_NTILES];
-    }
-    __syncthreads();
-    uint32_t total = pre[a.npeers];
-    const uint32_t room = (uint32_t)(a.cap_tiles - (int)old_tiles) * kTile;
-    if (total > room) {
-        if (threadIdx.x == 0) atomicOr(a.words + W_ERR, ERR_OVERFLOW);
-        total = room;
-    }
-    for (uint32_t j = threadIdx.x; j < total; j += blockDim.x) {
-        int p = 0;
-        while (p + 1 < a.npeers && pre[p + 1] <= j) ++p;
-        a.state[(size_t)old_tiles * kTile + j] = a.recv[p][1 + (j - pre[p])];
-    }
-    const uint32_t new_tiles = (total + kTile - 1) / kTile;
-    for (uint32_t t = threadIdx.x; t < new_tiles; t += blockDim.x) {
-        const uint32_t rem = total - t * kTile;
-        a.tile_count[old_tiles + t] = (uint8_t)(rem >= (uint32_t)kTile ? kTile : rem);
-    }
-    __syncthreads();                 // every count read before any header reset
-    if (a.zero_recv) {
-        if (threadIdx.x < (unsigned)a.npeers) *reinterpret_cast<uint32_t*>(a.recv[threadIdx.x]) = 0u;
-    } else if (threadIdx.x < (unsigned)a.noff) {
-        *reinterpret_cast<uint32_t*>(a.slots + a.slot_base[threadIdx.x]) = 0u;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        a.words[W_NTILES] = old_tiles + new_tiles;
-        if (total) atomicAdd(&a.counters[CNT_RECV], (unsigned long long)total);
     }
 }
 
@@ -512,7 +452,17 @@ lag_status lag_comm_reset(lag_ctx_s* ctx) {
     return LAG_OK;
 }
 
+static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity);
+
 static lag_status launch_append(lag_ctx_s* ctx, int peer_parity = -1) {
+    AppendArgs a = append_args(ctx, peer_parity);
+    append_kernel<<<1, 1024, 0, ctx->stream>>>(a);
+    ++ctx->launches;
+    CKC(cudaGetLastError());
+    return LAG_OK;
+}
+
+static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity) {
     Comm* cm = ctx->comm;
     AppendArgs a{};
     a.state = ctx->state; a.tile_count = ctx->tile_count; a.words = ctx->words;
@@ -527,10 +477,7 @@ static lag_status launch_append(lag_ctx_s* ctx, int peer_parity = -1) {
     a.slots = cm->slots;
     a.noff = kMaxOff;                               // all 27 offset headers (2-D uses 9..17)
     for (int k = 0; k < kMaxOff; ++k) a.slot_base[k] = cm->slot_base[k];
-    append_kernel<<<1, 1024, 0, ctx->stream>>>(a);
-    ++ctx->launches;
-    CKC(cudaGetLastError());
-    return LAG_OK;
+    return a;
 }
 
 // One NCCL group: optional halo boxes (v1 [+ v0]) and the pending particle slots.
@@ -580,29 +527,13 @@ static lag_status exchange(lag_ctx_s* ctx, float* v0, float* v1, bool halo, bool
     return launch_append(ctx);
 }
 
-// Peer transport, one cycle: pack -> signal halo -> wait -> pull ghosts ->
-// append the previous cycle's hand-offs (see lag_peer.cu).
+// Peer transport, one cycle: one fused exchange kernel (lag_peer.cu).
 static lag_status peer_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool with_v0) {
     Comm* cm = ctx->comm;
     const unsigned long long seq = ++lag_peer_seq(cm->peer);
-    const int q = (int)(seq & 1);
-    const int np = (int)cm->peers.size();
-    const int64_t sfl = (with_v0 ? 2 : 1) * cm->halo_send_floats;
-    if (sfl > 0) {
-        BoxArgs b{};
-        b.v0 = v0; b.v1 = v1; b.v0w = v0; b.boxes = cm->d_send_boxes; b.nbox = with_v0 ? 2 * np : np;
-        b.buf = lag_peer_outbox(cm->peer, q); b.sx = ctx->ext[0]; b.sxy = ctx->ext[0] * ctx->ext[1];
-        b.dim = ctx->cfg.dim; b.total = sfl;
-        const int blocks = (int)std::min<int64_t>((sfl + 255) / 256, (int64_t)ctx->num_sms * 8);
-        halo_pack_kernel<<<blocks, 256, 0, ctx->stream>>>(b);
-        ++ctx->launches;
-        CKC(cudaGetLastError());
-    }
-    lag_status st;
-    if ((st = lag_peer_signal(ctx, cm->peer, cm->prank, cm->pback, 0, seq)) != LAG_OK) return st;
-    if ((st = lag_peer_wait(ctx, cm->peer, cm->poff, seq, seq - 1)) != LAG_OK) return st;
-    if ((st = lag_peer_unpack(ctx, cm->peer, v0, v1, with_v0, q)) != LAG_OK) return st;
-    return launch_append(ctx, q ^ 1);
+    const AppendArgs ap = append_args(ctx, (int)((seq & 1) ^ 1));   // hand-offs of cycle seq-1
+    return lag_peer_exchange(ctx, cm->peer, cm->d_send_boxes, (int)cm->peers.size(), cm->halo_send_floats,
+                             v0, v1, with_v0, true, cm->poff, cm->pback, seq - 1, &ap);
 }
 
 lag_status lag_comm_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool v0_is_prev_v1) {
@@ -622,20 +553,23 @@ void lag_comm_fill_args(lag_ctx_s* ctx, AdvectArgs* a) {
         a->slot_capv[k] = cm->slot_capv[k];
         a->slot_ptr[k] = cm->slots + cm->slot_base[k];
     }
-    a->peer_fence = 0;
+    a->n_sig = 0;
     if (cm->peer) {
-        const int q = (int)(lag_peer_seq(cm->peer) & 1);
-        for (size_t i = 0; i < cm->peers.size(); ++i)
+        const unsigned long long seq = lag_peer_seq(cm->peer);
+        const int q = (int)(seq & 1);
+        for (size_t i = 0; i < cm->peers.size(); ++i) {
             a->slot_ptr[cm->peers[i].off] = lag_peer_remote_slot(cm->peer, (int)i, cm->peers[i].rank, cm->peers[i].back, q);
-        a->peer_fence = 1;
+            a->sig_flag[i] = lag_peer_remote_flag(cm->peer, (int)i, 1, cm->peers[i].back);
+        }
+        a->n_sig = (int)cm->peers.size();
+        a->sig_value = seq;
+        a->done_warps = lag_peer_done_counter(cm->peer);
     }
 }
 
 lag_status lag_comm_post_advect(lag_ctx_s* ctx) {
     Comm* cm = ctx->comm;
-    cm->pending = !cm->peers.empty();
-    if (cm->peer && !cm->peers.empty())
-        return lag_peer_signal(ctx, cm->peer, cm->prank, cm->pback, 1, lag_peer_seq(cm->peer));
+    cm->pending = !cm->peers.empty();       // peer transport: signalled by the advect kernel
     return LAG_OK;
 }
 
@@ -650,8 +584,9 @@ lag_status lag_comm_return_to_origin(lag_ctx_s* ctx) {
         lag_status st;
         if (cm->peer) {
             const unsigned long long seq = lag_peer_seq(cm->peer);
-            if ((st = lag_peer_wait(ctx, cm->peer, cm->poff, 0, seq)) != LAG_OK) return st;
-            st = launch_append(ctx, (int)(seq & 1));
+            const AppendArgs ap = append_args(ctx, (int)(seq & 1));
+            st = lag_peer_exchange(ctx, cm->peer, cm->d_send_boxes, (int)cm->peers.size(), 0,
+                                   nullptr, nullptr, false, false, cm->poff, cm->pback, seq, &ap);
         } else {
             st = exchange(ctx, nullptr, nullptr, false, false);
         }

@@ -78,7 +78,12 @@ struct AdvectArgs {
     int32_t slot_base[27];
     int32_t slot_capv[27];
     float4* slot_ptr[27];           // slot of offset k: local (NCCL) or the owner's inbox (peer)
-    int32_t peer_fence;             // peer exchange: fence remote stores system-wide
+    // peer transport: the last warp to retire signals "particles of cycle
+    // sig_value ready" into each neighbour's flag word
+    unsigned long long* sig_flag[26];
+    int32_t n_sig;
+    unsigned long long sig_value;
+    uint32_t* done_warps;
 };
 
 __device__ __forceinline__ void unpack_g(uint32_t w, const AdvectArgs& a, int g[3]) {
@@ -453,6 +458,7 @@ advect_kernel(const AdvectArgs a) {
 
     unsigned long long steps = 0, nterm = 0, nexit = 0, nsent = 0;
     uint32_t errbits = 0;
+    bool did_remote = false;
 
     // software pipeline: the next tile's count and records are in flight while
     // the current tile computes
@@ -640,7 +646,7 @@ advect_kernel(const AdvectArgs a) {
                     sb[1 + pos] = make_float4(dn[0], dn[1], dn[2], r.w);
                 else
                     errbits |= ERR_OVERFLOW;
-                if (a.peer_fence) __threadfence_system();   // remote stores before the ready flag
+                did_remote = true;
             }
             if (lane == 0) nsent += __popc(mmask);
         }
@@ -676,6 +682,22 @@ advect_kernel(const AdvectArgs a) {
     }
     errbits = __reduce_or_sync(0xffffffffu, errbits);
     if (lane == 0 && errbits) atomicOr(a.err, errbits);
+    if constexpr (!BTO) {
+        if (a.n_sig) {
+            if (did_remote) __threadfence_system();          // my remote hand-offs are performed
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t total = (gridDim.x * kThreads) >> 5;
+                if (atomicAdd(a.done_warps, 1u) == total - 1) {  // last warp of the grid
+                    *a.done_warps = 0u;
+                    __threadfence_system();
+                    for (int k = 0; k < a.n_sig; ++k)
+                        *reinterpret_cast<volatile unsigned long long*>(a.sig_flag[k]) = a.sig_value;
+                    __threadfence_system();
+                }
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -19,6 +19,7 @@
 // Two parities suffice: a neighbour reuses parity q at seq+2 only after it
 // waited for my halo(seq+1), which I signal after consuming parity q.
 #include "lag_internal.h"
+#include "lag_append.cuh"
 
 #include <nccl.h>
 
@@ -49,7 +50,7 @@ using namespace lag;
 
 namespace lag {
 
-constexpr int kOff = 27;
+constexpr int kOff = kMaxOff;
 constexpr int kMaxPeers = 26;
 // per-rank layout table published to every rank (int64 words)
 enum : int { T_INBOX = 0, T_INBOX_PAR = 1, T_OUTBOX = 2, T_HALO = 3, T_RECV = 4, T_SEND = 4 + kOff,
@@ -126,6 +127,80 @@ __global__ void peer_unpack_kernel(PeerUnpackArgs a) {
     }
 }
 
+// One CTA does the whole per-cycle exchange (one launch instead of five):
+// pack my ghost sources -> signal halo(seq) -> wait for the neighbours ->
+// pull their ghost sources into my ghost layers -> append the hand-offs of the
+// previous cycle.  The particle-ready signal comes from the advect kernel.
+struct XchgArgs {
+    float* v0;
+    float* v1;
+    const Box* send_boxes;
+    int nsend;
+    float* outbox;                                 // my outbox at parity q
+    int64_t sfl;                                   // floats to pack
+    int signal_halo;
+    unsigned long long* halo_flag[kMaxPeers];      // neighbour's halo flag word for me
+    int npeers;
+    const unsigned long long* my_flags;
+    int back[kMaxPeers];
+    unsigned long long need_halo, need_part;
+    long long timeout_cycles;
+    uint32_t* err;
+    const PeerBox* recv_boxes;
+    int nrecv;
+    int parity;
+    int64_t rtotal;                                // floats to pull
+    int sx, sxy, dim;
+    unsigned long long seq;
+    int do_append;
+};
+
+__global__ void __launch_bounds__(1024) peer_exchange_kernel(XchgArgs x, AppendArgs ap) {
+    const int tid = threadIdx.x;
+    for (int64_t i = tid; i < x.sfl; i += blockDim.x) {              // pack
+        int k = 0;
+        while (k + 1 < x.nsend && x.send_boxes[k + 1].off <= i) ++k;
+        const Box& b = x.send_boxes[k];
+        const int64_t j = i - b.off;
+        const int comp = (int)(j % x.dim);
+        const int64_t node = j / x.dim;
+        const int xx = (int)(node % b.nx), yy = (int)((node / b.nx) % b.ny), zz = (int)(node / ((int64_t)b.nx * b.ny));
+        const float* src = b.slice ? x.v1 : x.v0;
+        x.outbox[i] = src[(int64_t)x.dim * ((b.x0 + xx) + (int64_t)x.sx * (b.y0 + yy) + (int64_t)x.sxy * (b.z0 + zz)) + comp];
+    }
+    __syncthreads();
+    if (tid == 0 && x.signal_halo) {                                  // halo(seq) ready
+        __threadfence_system();
+        for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(x.halo_flag[p]) = x.seq;
+        __threadfence_system();
+    }
+    if (tid < x.npeers) {                                             // wait for every neighbour
+        const volatile unsigned long long* fh = x.my_flags + 0 * kOff + x.back[tid];
+        const volatile unsigned long long* fp = x.my_flags + 1 * kOff + x.back[tid];
+        const long long t0 = clock64();
+        while (*fh < x.need_halo || *fp < x.need_part) {
+            if (clock64() - t0 > x.timeout_cycles) { atomicOr(x.err, ERR_XCHG); break; }
+            __nanosleep(100);
+        }
+        __threadfence_system();
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < x.rtotal; i += blockDim.x) {            // pull ghosts
+        int k = 0;
+        while (k + 1 < x.nrecv && x.recv_boxes[k + 1].off <= i) ++k;
+        const PeerBox& b = x.recv_boxes[k];
+        const int64_t j = i - b.off;
+        const int comp = (int)(j % x.dim);
+        const int64_t node = j / x.dim;
+        const int xx = (int)(node % b.nx), yy = (int)((node / b.nx) % b.ny), zz = (int)(node / ((int64_t)b.nx * b.ny));
+        float* dst = b.slice ? x.v1 : x.v0;
+        dst[(int64_t)x.dim * ((b.x0 + xx) + (int64_t)x.sx * (b.y0 + yy) + (int64_t)x.sxy * (b.z0 + zz)) + comp] =
+            b.src[x.parity][b.slice][j];
+    }
+    __syncthreads();
+    if (x.do_append) append_body(ap);                                 // hand-offs of cycle seq-1
+}
+
 }  // namespace lag
 
 // ---------------------------------------------------------------------------
@@ -144,6 +219,7 @@ struct PeerState {
     int64_t halo_send_floats = 0;
     std::vector<int64_t> my_table;            // my own layout words
     unsigned long long seq = 0;
+    uint32_t* done_warps = nullptr;           // advect completion counter
 };
 
 lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>& prank,
@@ -228,6 +304,8 @@ lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>
             ps->boxes.push_back(b);
         }
     }
+    CKC(cudaMalloc(&ps->done_warps, sizeof(uint32_t)));
+    CKC(cudaMemset(ps->done_warps, 0, sizeof(uint32_t)));
     CKC(cudaMalloc(&ps->d_boxes, sizeof(PeerBox) * std::max<size_t>(1, ps->boxes.size())));
     if (!ps->boxes.empty())
         CKC(cudaMemcpy(ps->d_boxes, ps->boxes.data(), sizeof(PeerBox) * ps->boxes.size(), cudaMemcpyHostToDevice));
@@ -240,6 +318,7 @@ void lag_peer_destroy(PeerState* ps) {
     if (!ps) return;
     for (char* p : ps->remote) if (p) cudaIpcCloseMemHandle(p);
     cudaFree(ps->d_boxes);
+    cudaFree(ps->done_warps);
     cudaFree(ps->mem);
     delete ps;
 }
@@ -312,3 +391,52 @@ float4* lag_peer_inbox_slot(PeerState* ps, int q, int poff) {
 float* lag_peer_outbox(PeerState* ps, int q) { return ps->outbox + (size_t)q * 2 * ps->halo_send_floats; }
 
 unsigned long long& lag_peer_seq(PeerState* ps) { return ps->seq; }
+
+uint32_t* lag_peer_done_counter(PeerState* ps) { return ps->done_warps; }
+
+unsigned long long* lag_peer_remote_flag(PeerState* ps, int i, int kind, int pback) {
+    return reinterpret_cast<unsigned long long*>(ps->remote[i]) + kind * kOff + pback;
+}
+
+// The fused exchange (see peer_exchange_kernel).  pack/halo: this cycle's
+// ghost exchange; need_part: hand-offs to wait for; append_parity: inbox
+// parity to append (-1: none).
+lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_boxes, int nsend,
+                             int64_t sfl, float* v0, float* v1, bool with_v0, bool halo,
+                             const std::vector<int>& poff, const std::vector<int>& pback,
+                             unsigned long long need_part, const void* append_args) {
+    const int np = (int)poff.size();
+    XchgArgs x{};
+    const unsigned long long seq = ps->seq;
+    const int q = (int)(seq & 1);
+    x.v0 = v0; x.v1 = v1;
+    x.send_boxes = reinterpret_cast<const Box*>(send_boxes);
+    x.nsend = halo ? (with_v0 ? 2 * nsend : nsend) : 0;
+    x.outbox = ps->outbox + (size_t)q * 2 * ps->halo_send_floats;
+    x.sfl = halo ? (with_v0 ? 2 : 1) * sfl : 0;
+    x.signal_halo = halo ? 1 : 0;
+    x.npeers = np;
+    for (int i = 0; i < np; ++i) {
+        x.halo_flag[i] = lag_peer_remote_flag(ps, i, 0, pback[i]);
+        x.back[i] = poff[i];
+    }
+    x.my_flags = ps->flags;
+    x.need_halo = halo ? seq : 0;
+    x.need_part = need_part;
+    x.timeout_cycles = 8000000000LL;
+    x.err = ctx->words + W_ERR;
+    x.recv_boxes = ps->d_boxes;
+    const int nb = (int)ps->boxes.size() / 2;
+    x.nrecv = halo ? (with_v0 ? 2 * nb : nb) : 0;
+    x.parity = q;
+    x.rtotal = halo ? (with_v0 ? 2 : 1) * ps->halo_recv_floats : 0;
+    x.sx = ctx->ext[0]; x.sxy = ctx->ext[0] * ctx->ext[1]; x.dim = ctx->cfg.dim;
+    x.seq = seq;
+    x.do_append = append_args ? 1 : 0;
+    AppendArgs ap{};
+    if (append_args) ap = *reinterpret_cast<const AppendArgs*>(append_args);
+    peer_exchange_kernel<<<1, 1024, 0, ctx->stream>>>(x, ap);
+    ++ctx->launches;
+    CKC(cudaGetLastError());
+    return LAG_OK;
+}
