@@ -127,10 +127,13 @@ __global__ void peer_unpack_kernel(PeerUnpackArgs a) {
     }
 }
 
-// One CTA does the whole per-cycle exchange (one launch instead of five):
-// pack my ghost sources -> signal halo(seq) -> wait for the neighbours ->
-// pull their ghost sources into my ghost layers -> append the hand-offs of the
-// previous cycle.  The particle-ready signal comes from the advect kernel.
+// Per-cycle exchange in two multi-CTA kernels (the advect kernel signals the
+// hand-offs itself):
+//   A: pack my ghost sources (grid-stride); the last CTA to finish fences and
+//      signals halo(seq) to every neighbour;
+//   B: every CTA waits (bounded) for all neighbours' halo(seq) and
+//      particles(seq-1), then pulls its share of the ghost layers with remote
+//      loads; CTA 0 also appends the previous cycle's hand-offs.
 struct XchgArgs {
     float* v0;
     float* v1;
@@ -140,6 +143,7 @@ struct XchgArgs {
     int64_t sfl;                                   // floats to pack
     int signal_halo;
     unsigned long long* halo_flag[kMaxPeers];      // neighbour's halo flag word for me
+    uint32_t* done_ctas;                           // kernel A completion counter
     int npeers;
     const unsigned long long* my_flags;
     int back[kMaxPeers];
@@ -155,9 +159,9 @@ struct XchgArgs {
     int do_append;
 };
 
-__global__ void __launch_bounds__(1024) peer_exchange_kernel(XchgArgs x, AppendArgs ap) {
-    const int tid = threadIdx.x;
-    for (int64_t i = tid; i < x.sfl; i += blockDim.x) {              // pack
+__global__ void __launch_bounds__(256) peer_pack_signal_kernel(XchgArgs x) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < x.sfl;
+         i += (int64_t)gridDim.x * blockDim.x) {
         int k = 0;
         while (k + 1 < x.nsend && x.send_boxes[k + 1].off <= i) ++k;
         const Box& b = x.send_boxes[k];
@@ -168,15 +172,22 @@ __global__ void __launch_bounds__(1024) peer_exchange_kernel(XchgArgs x, AppendA
         const float* src = b.slice ? x.v1 : x.v0;
         x.outbox[i] = src[(int64_t)x.dim * ((b.x0 + xx) + (int64_t)x.sx * (b.y0 + yy) + (int64_t)x.sxy * (b.z0 + zz)) + comp];
     }
-    __syncthreads();
-    if (tid == 0 && x.signal_halo) {                                  // halo(seq) ready
-        __threadfence_system();
-        for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(x.halo_flag[p]) = x.seq;
-        __threadfence_system();
+    __syncthreads();                                  // the CTA's packs are visible to thread 0
+    if (threadIdx.x == 0 && x.signal_halo) {
+        __threadfence_system();                       // cumulative: orders the CTA's packs
+        if (atomicAdd(x.done_ctas, 1u) == gridDim.x - 1) {   // last CTA: halo(seq) ready
+            *x.done_ctas = 0u;
+            __threadfence_system();
+            for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(x.halo_flag[p]) = x.seq;
+            __threadfence_system();
+        }
     }
-    if (tid < x.npeers) {                                             // wait for every neighbour
-        const volatile unsigned long long* fh = x.my_flags + 0 * kOff + x.back[tid];
-        const volatile unsigned long long* fp = x.my_flags + 1 * kOff + x.back[tid];
+}
+
+__global__ void __launch_bounds__(256) peer_wait_pull_kernel(XchgArgs x, AppendArgs ap) {
+    if (threadIdx.x < x.npeers) {
+        const volatile unsigned long long* fh = x.my_flags + 0 * kOff + x.back[threadIdx.x];
+        const volatile unsigned long long* fp = x.my_flags + 1 * kOff + x.back[threadIdx.x];
         const long long t0 = clock64();
         while (*fh < x.need_halo || *fp < x.need_part) {
             if (clock64() - t0 > x.timeout_cycles) { atomicOr(x.err, ERR_XCHG); break; }
@@ -185,7 +196,8 @@ __global__ void __launch_bounds__(1024) peer_exchange_kernel(XchgArgs x, AppendA
         __threadfence_system();
     }
     __syncthreads();
-    for (int64_t i = tid; i < x.rtotal; i += blockDim.x) {            // pull ghosts
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < x.rtotal;
+         i += (int64_t)gridDim.x * blockDim.x) {
         int k = 0;
         while (k + 1 < x.nrecv && x.recv_boxes[k + 1].off <= i) ++k;
         const PeerBox& b = x.recv_boxes[k];
@@ -197,8 +209,7 @@ __global__ void __launch_bounds__(1024) peer_exchange_kernel(XchgArgs x, AppendA
         dst[(int64_t)x.dim * ((b.x0 + xx) + (int64_t)x.sx * (b.y0 + yy) + (int64_t)x.sxy * (b.z0 + zz)) + comp] =
             b.src[x.parity][b.slice][j];
     }
-    __syncthreads();
-    if (x.do_append) append_body(ap);                                 // hand-offs of cycle seq-1
+    if (blockIdx.x == 0 && x.do_append) append_body(ap);      // hand-offs of cycle seq-1
 }
 
 }  // namespace lag
@@ -220,6 +231,7 @@ struct PeerState {
     std::vector<int64_t> my_table;            // my own layout words
     unsigned long long seq = 0;
     uint32_t* done_warps = nullptr;           // advect completion counter
+    uint32_t* done_ctas = nullptr;            // pack-kernel completion counter
 };
 
 lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>& prank,
@@ -304,8 +316,9 @@ lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>
             ps->boxes.push_back(b);
         }
     }
-    CKC(cudaMalloc(&ps->done_warps, sizeof(uint32_t)));
-    CKC(cudaMemset(ps->done_warps, 0, sizeof(uint32_t)));
+    CKC(cudaMalloc(&ps->done_warps, 2 * sizeof(uint32_t)));
+    CKC(cudaMemset(ps->done_warps, 0, 2 * sizeof(uint32_t)));
+    ps->done_ctas = ps->done_warps + 1;
     CKC(cudaMalloc(&ps->d_boxes, sizeof(PeerBox) * std::max<size_t>(1, ps->boxes.size())));
     if (!ps->boxes.empty())
         CKC(cudaMemcpy(ps->d_boxes, ps->boxes.data(), sizeof(PeerBox) * ps->boxes.size(), cudaMemcpyHostToDevice));
@@ -433,9 +446,17 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
     x.sx = ctx->ext[0]; x.sxy = ctx->ext[0] * ctx->ext[1]; x.dim = ctx->cfg.dim;
     x.seq = seq;
     x.do_append = append_args ? 1 : 0;
+    x.done_ctas = ps->done_ctas;
     AppendArgs ap{};
     if (append_args) ap = *reinterpret_cast<const AppendArgs*>(append_args);
-    peer_exchange_kernel<<<1, 1024, 0, ctx->stream>>>(x, ap);
+    const int cap = ctx->num_sms * 2;
+    if (halo) {
+        const int ga = (int)std::max<int64_t>(1, std::min<int64_t>((x.sfl + 255) / 256, cap));
+        peer_pack_signal_kernel<<<ga, 256, 0, ctx->stream>>>(x);
+        ++ctx->launches;
+    }
+    const int gb = (int)std::max<int64_t>(1, std::min<int64_t>((x.rtotal + 255) / 256, cap));
+    peer_wait_pull_kernel<<<gb, 256, 0, ctx->stream>>>(x, ap);
     ++ctx->launches;
     CKC(cudaGetLastError());
     return LAG_OK;
