@@ -442,6 +442,7 @@ def main():
     # both transports; the BTO speed-up is quoted against the faster one
     comm = None
     if not args.no_comm:
+      try:
         comm = {}
         transports = [("nccl", P.LAG_XCHG_NCCL)] + ([("peer", P.LAG_XCHG_PEER)] if world > 1 else [])
         for tname, xch in transports:
@@ -466,18 +467,29 @@ def main():
                      "exchange": "per cycle: ghost layer (G=1, faces+edges+corners) of v_t1 + particle "
                                  "hand-offs; 'nccl' = one grouped NCCL send/recv, 'peer' = kernels read / "
                                  "write the neighbours' memory over NVLink (CUDA IPC); value/speedup = faster"})
+      except Exception as exc:        # the headline BTO line must still print
+        comm = {"error": repr(exc)[:300]}
 
     secondary = None
     if not args.no_secondary:
-        secondary = measure_secondary("C3", rank, world, max(2, args.steps // 2), 2, flush)
+        try:
+            secondary = measure_secondary("C3", rank, world, max(2, args.steps // 2), 2, flush)
+        except Exception as exc:
+            secondary = {"error": repr(exc)[:300]}
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(cfg, rank, world, max(2, args.steps // 2), 1)
+        try:
+            e2e = run_e2e(cfg, rank, world, max(2, args.steps // 2), 1)
+        except Exception as exc:
+            e2e = {"error": repr(exc)[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(cfg)
+        try:
+            cpu = cpu_baseline(cfg)
+        except Exception as exc:
+            cpu = {"error": repr(exc)[:300]}
 
     if rank == 0:
         out = {
