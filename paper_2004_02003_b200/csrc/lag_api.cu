@@ -345,6 +345,7 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
     AdvectArgs a{};
     a.v0 = d0; a.v1 = d1;
     a.frozen = d0 == d1 ? 1 : 0;
+    a.slice_nodes = (int32_t)(ctx->slice_floats / ctx->cfg.dim);
     a.state = ctx->state; a.tile_count = ctx->tile_count;
     a.n_tiles_dev = ctx->cfg.mode == LAG_COMM ? (const int32_t*)(ctx->words + W_NTILES) : nullptr;
     a.n_tiles = ctx->n_tiles;

@@ -59,6 +59,7 @@ struct AdvectArgs {
     int32_t bmin[3], bspan[3];
     int32_t gidx0;                  // node index of global cell gmin (local slice coordinates)
     int32_t frozen;                 // v0 == v1: one snapshot per cycle; load corners once
+    int32_t slice_nodes;            // nodes in one slice array (debug bounds checks)
     int32_t sx, sxy;                // slice pitch (nodes) of a row / a plane
     float hdth[3], qdth[3], sdth[3];// dt/h * (1/2, 1/4, 1/6)
     uint32_t bx, by;                // packed seed-node bit widths (x, y)
@@ -351,6 +352,18 @@ __device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
     return d;
 }
 
+// Debug build (-DLAG_DEBUG_BOUNDS): trap if a corner gather of cell origin
+// `idx` would leave the slice array (compute-sanitizer is unavailable here).
+#ifdef LAG_DEBUG_BOUNDS
+#define LAG_CHECK_GATHER(a, idx, live)                                                    \
+    do {                                                                                  \
+        const long long far_ = (long long)(idx) + 1 + (a).sx + (DIM == 3 ? (a).sxy : 0);  \
+        if ((live) && ((idx) < 0 || far_ >= (a).slice_nodes)) __trap();                  \
+    } while (0)
+#else
+#define LAG_CHECK_GATHER(a, idx, live) do { } while (0)
+#endif
+
 // number of corner pairs per slice: rows (2^(DIM-1)) x components (DIM)
 template <int DIM> struct Pairs { static constexpr int n = (1 << (DIM - 1)) * DIM; };
 
@@ -492,6 +505,7 @@ advect_kernel(const AdvectArgs a) {
         if (!cells_b<DIM>(gb, d, a.gspan, c, f) && live)
             classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);   // top-face clamp only
         int cur = vindex<DIM>(a, c);
+        LAG_CHECK_GATHER(a, cur, live);
         if (!live) cur = 0;
         gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
         if constexpr (FROZEN) {
@@ -512,6 +526,7 @@ advect_kernel(const AdvectArgs a) {
             st = classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);
         {
             const int idx = vindex<DIM>(a, c);
+            LAG_CHECK_GATHER(a, idx, live && st == ST_VALID);
 #ifdef LAG_EXP_NORELOAD
             if (false) {
 #else
@@ -539,6 +554,7 @@ advect_kernel(const AdvectArgs a) {
             st = classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);
         {
             const int idx = vindex<DIM>(a, c);
+            LAG_CHECK_GATHER(a, idx, live && st == ST_VALID);
 #ifdef LAG_EXP_NORELOAD
             if (false) {
 #else
@@ -566,6 +582,7 @@ advect_kernel(const AdvectArgs a) {
             st = classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);
         {
             const int idx = vindex<DIM>(a, c);
+            LAG_CHECK_GATHER(a, idx, live && st == ST_VALID);
 #ifndef LAG_EXP_NORELOAD
             if (live && st == ST_VALID && idx != cur) {
                 gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
