@@ -209,6 +209,28 @@ LAG_API lag_status lag_nccl_unique_id(void* out, int64_t out_bytes);
  * lag_init (instrumentation for the benchmark's gpu_launches claim). */
 LAG_API int64_t lag_kernel_launches(lag_ctx ctx);
 
+/* lag_gridfill — post hoc reconstruction of BTO holes on a dense seed
+ * lattice (paper P:229-233 §3.1 "interpolated ... post hoc"; Eq. 2,
+ * P:289-303 §3.3; GridFill; reading R12 in DESIGN.md).
+ *   dim      2 or 3.
+ *   dims     [dim] host array: lattice extent per axis (x fastest), each >= 1.
+ *   k        components per node (1..3), e.g. k = dim for end positions.
+ *   values   DEVICE [n][k] f64, n = prod(dims); entries of invalid nodes are
+ *            ignored (may hold anything, including NaN).
+ *   valid    DEVICE [n] u8, nonzero = the node's value is known.
+ *   out      DEVICE [n][k] f64 (caller-owned, must not alias values):
+ *            valid nodes copy their value; an invalid node gets the linear
+ *            interpolant (Eq. 1) between the nearest valid nodes on both
+ *            sides along the lattice axis with the shortest such bracket
+ *            (brackets of equal length averaged); NaN if no axis brackets it.
+ *   filled   DEVICE [n] u8: 1 where an invalid node was filled, else 0.
+ *   stream   cudaStream_t (NULL = legacy default); the call synchronises it.
+ * Arithmetic is round-to-nearest f64 without contraction, so results are
+ * bitwise reproducible.  Errors: LAG_EINVAL (bad sizes, NULL or non-device
+ * pointers), LAG_ECUDA (launch failure); message in lag_last_error(NULL). */
+LAG_API lag_status lag_gridfill(int32_t dim, const int64_t* dims, int32_t k, const double* values,
+                                const uint8_t* valid, double* out, uint8_t* filled, void* stream);
+
 /* lag_abi_version — LAG_ABI_VERSION the library was built with. */
 LAG_API int32_t lag_abi_version(void);
 

@@ -217,16 +217,21 @@ def grid_fill(lat: np.ndarray, values: np.ndarray, valid: np.ndarray, hole: np.n
 
 
 def agreement(grid, g_seeds, start, bto_end, bto_status, comm_end, comm_status, stride,
-              method: str = "delaunay"):
+              method: str = "delaunay", recon=None):
     """BTO-vs-comm flow-map agreement for one interval (§4.3):
     over seeds valid in the comm flow map, b = BTO end if valid, else its
     reconstruction (Delaunay + barycentric, P:267-274, or GridFill, Eq. 2);
     L = Eq. 5, accuracy = Eq. 6.  Seeds that cannot be reconstructed (outside
-    the hull / no bounding pair) are excluded and counted."""
+    the hull / no bounding pair) are excluded and counted.  `recon`
+    = (values [n, dim], filled mask [n]) supplies a reconstruction computed
+    elsewhere (e.g. the CUDA GridFill) instead of computing one here."""
     comm_ok = np.asarray(comm_status) == 0
     bto_ok = np.asarray(bto_status) == 0
     hole = comm_ok & ~bto_ok
-    if method == "gridfill":
+    if recon is not None:
+        recon, inside = recon
+        inside = np.asarray(inside, dtype=bool) & hole
+    elif method == "gridfill":
         lat = np.asarray(g_seeds)[:, :grid.dim] // stride
         recon, inside = grid_fill(lat, bto_end, bto_ok, hole)
     else:

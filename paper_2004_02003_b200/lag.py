@@ -29,7 +29,7 @@ STATUS_NAMES = {0: "LAG_OK", -1: "LAG_EINVAL", -2: "LAG_ESTATE", -3: "LAG_EEMPTY
 # every symbol include/lag.h declares
 EXPORTS = ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_extract_ex", "lag_stats",
            "lag_destroy", "lag_last_error", "lag_nccl_unique_id", "lag_kernel_launches",
-           "lag_abi_version")
+           "lag_abi_version", "lag_gridfill")
 
 
 class LagError(RuntimeError):
@@ -84,8 +84,10 @@ def load(path: str = LIB_PATH):
     lib.lag_kernel_launches.argtypes = [vp]
     lib.lag_kernel_launches.restype = ctypes.c_int64
     lib.lag_abi_version.restype = ctypes.c_int32
+    if hasattr(lib, "lag_gridfill"):
+        lib.lag_gridfill.argtypes = [ctypes.c_int32, P(ctypes.c_int64), ctypes.c_int32, vp, vp, vp, vp, vp]
     for name in ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_extract_ex", "lag_stats",
-                 "lag_destroy", "lag_nccl_unique_id"):
+                 "lag_destroy", "lag_nccl_unique_id", "lag_gridfill"):
         if hasattr(lib, name):
             getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -202,6 +204,30 @@ def lag_stats(ctx) -> dict:
 
 def lag_destroy(ctx) -> None:
     _check(load().lag_destroy(ctx))
+
+
+def lag_gridfill(values, valid, dims: Sequence[int], out=None, filled=None, stream=None):
+    """GridFill reconstruction on a dense lattice (include/lag.h).  `values`
+    [n, k] f64 and `valid` [n] u8 are device tensors in x-fastest lattice
+    order; returns (out, filled), allocating them if not given."""
+    import torch
+    dim = len(dims)
+    n = 1
+    for d in dims:
+        n *= int(d)
+    k = values.shape[1]
+    if out is None:
+        out = torch.empty_like(values)
+    if filled is None:
+        filled = torch.empty_like(valid)
+    if values.shape[0] != n or valid.shape[0] != n:
+        raise ValueError("values/valid must hold prod(dims) nodes")
+    d = (ctypes.c_int64 * 3)(*[int(x) for x in dims], *([1] * (3 - dim)))
+    if stream is None:                  # (host tensors are rejected by the library)
+        stream = torch.cuda.current_stream(values.device).cuda_stream if values.is_cuda else 0
+    s = stream
+    _check(load().lag_gridfill(dim, d, k, _addr(values), _addr(valid), _addr(out), _addr(filled), s))
+    return out, filled
 
 
 def lag_kernel_launches(ctx) -> int:

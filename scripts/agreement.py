@@ -42,7 +42,9 @@ def main():
     ap.add_argument("--stride", type=int, default=None)
     ap.add_argument("--interval", type=int, default=None)
     ap.add_argument("--save", action="store_true")
-    ap.add_argument("--recon", default="delaunay", choices=["delaunay", "gridfill"])
+    ap.add_argument("--recon", default="delaunay", choices=["delaunay", "gridfill", "gpu-gridfill"],
+                    help="gpu-gridfill: holes filled by lag_gridfill (CUDA), cross-checked bitwise "
+                         "against the oracle's GridFill on the first interval")
     ap.add_argument("--tag", default="")
     ap.add_argument("--layout", default=None, help="blocks per axis, e.g. 2,2,2 (default: the config's)")
     args = ap.parse_args()
@@ -72,7 +74,7 @@ def main():
         q = gg // stride
         return q[:, 0] + dims[0] * (q[:, 1] + dims[1] * q[:, 2])
     bidx = [gidx(lattice(b.lo, b.hi)) for b in blocks]
-    per, t_gpu, t_cpu = [], 0.0, 0.0
+    per, t_gpu, t_cpu, t_fill = [], 0.0, 0.0, 0.0
     for it in range(args.intervals):
         t0 = time.time()
         ext = [L.block_slice_extent(g, b, 0) for b in blocks]
@@ -99,9 +101,24 @@ def main():
             b_st[ix] = s_.cpu().numpy()
         torch.cuda.synchronize()
         t_gpu += time.time() - t0
+        recon = None
+        if args.recon == "gpu-gridfill":
+            # gall is x-fastest over the global seed lattice, so it is the dense
+            # lattice lag_gridfill expects
+            tg = time.time()
+            ok = torch.from_numpy(b_st == 0).to(torch.uint8).cuda()
+            vals = torch.from_numpy(np.where((b_st == 0)[:, None], b_end, 0.0)).cuda()
+            out, filled = P.lag_gridfill(vals, ok, dims[:g.dim])
+            recon = (out.cpu().numpy(), filled.cpu().numpy().astype(bool))
+            t_fill += time.time() - tg
+            if it == 0:
+                lat = gall[:, :g.dim] // stride
+                ref, ref_in = metrics.grid_fill(lat, b_end, b_st == 0, b_st != 0)
+                assert np.array_equal(recon[1] & (b_st != 0), ref_in), "gpu gridfill mask != oracle"
+                assert np.array_equal(recon[0][ref_in], ref[ref_in]), "gpu gridfill != oracle (bitwise)"
         t1 = time.time()
         r = metrics.agreement(g, gall, start.cpu().numpy(), b_end, b_st, m_end.cpu().numpy(),
-                              m_st.cpu().numpy(), stride, method=args.recon)
+                              m_st.cpu().numpy(), stride, method=args.recon, recon=recon)
         t_cpu += time.time() - t1
         r["interval"] = it
         per.append(r)
@@ -120,10 +137,12 @@ def main():
         "excluded_outside_hull": int(sum(r["excluded"] for r in per)),
         "compared": int(sum(r["compared"] for r in per)),
         "gpu_seconds": t_gpu, "cpu_seconds": t_cpu, "cpu_cores": os.cpu_count(),
+        "gpu_gridfill_seconds": t_fill if args.recon == "gpu-gridfill" else None,
         "method": "BTO: one context per block on one GPU; COMM map: single-block run (== decomposed COMM "
                   "bitwise); holes reconstructed by " + ("Qhull-QJ Delaunay + barycentric over valid seeds in "
                   "hole-band tiles (P:267-274)" if args.recon == "delaunay" else
-                  "GridFill along lattice axes (Eq. 2, SPEC.md:323-331)"),
+                  "GridFill along lattice axes (Eq. 2, SPEC.md:323-331)" +
+                  (" on the GPU (lag_gridfill)" if args.recon == "gpu-gridfill" else "")),
         "reconstruction": args.recon,
         "per_interval": [{k: r[k] for k in ("interval", "L", "max_l2", "accuracy", "discarded", "holes", "excluded")}
                          for r in per],

@@ -99,3 +99,13 @@ def test_product_never_imports_the_oracle():
             elif f.endswith((".cu", ".cuh", ".h", ".cpp")):
                 txt = open(path).read()
                 assert "lag_oracle" not in txt and "orc_" not in txt, path
+
+
+def test_gridfill_rejects_null_and_bad_sizes_without_a_gpu():
+    import ctypes
+    lib = P.load()
+    dims = (ctypes.c_int64 * 3)(4, 4, 1)
+    assert lib.lag_gridfill(2, dims, 2, None, None, None, None, None) == P.LAG_EINVAL
+    assert lib.lag_gridfill(4, dims, 2, 1, 1, 1, 1, None) == P.LAG_EINVAL
+    assert lib.lag_gridfill(2, dims, 0, 1, 1, 1, 1, None) == P.LAG_EINVAL
+    assert "gridfill" in P.lag_last_error(None)

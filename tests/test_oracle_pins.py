@@ -457,3 +457,23 @@ def test_grid_fill_affine_exact_and_eq2():
     lat1 = np.stack([np.arange(n), np.zeros(n, int)], 1)
     out1, fl1 = metrics.grid_fill(lat1, f[:, None], valid, ~valid)
     np.testing.assert_allclose(out1[~valid, 0], metrics.grid_fill_1d(f, valid, np.arange(n))[~valid], atol=1e-12)
+
+
+def test_agreement_accepts_an_external_reconstruction():
+    """metrics.agreement(recon=...) (used for the CUDA GridFill) gives the same
+    numbers as its own GridFill when handed that GridFill's output."""
+    import lag_inputs as L
+    from oracle import metrics
+    g = L.Grid(2, (12, 10, 1), (0.0, 0.0, 0.0), (0.1, 0.1, 1.0))
+    gy, gx = np.meshgrid(np.arange(10), np.arange(12), indexing="ij")
+    gs = np.stack([gx.ravel(), gy.ravel(), np.zeros(gx.size, int)], 1)
+    rng = np.random.default_rng(3)
+    end = gs[:, :2] * 0.1 + 0.01 * rng.standard_normal((gs.shape[0], 2))
+    bst = np.where((gs[:, 0] == 5) | (gs[:, 0] == 6), 1, 0).astype(np.uint8)
+    cst = np.zeros_like(bst)
+    cend = end + 1e-3
+    ref = metrics.agreement(g, gs, gs[:, :2] * 0.1, end, bst, cend, cst, 1, method="gridfill")
+    rec = metrics.grid_fill(gs[:, :2], end, bst == 0, bst != 0)
+    got = metrics.agreement(g, gs, gs[:, :2] * 0.1, end, bst, cend, cst, 1, recon=rec)
+    assert got == ref
+    assert ref["holes"] == 20 and ref["excluded"] == 0
