@@ -477,3 +477,77 @@ def test_agreement_accepts_an_external_reconstruction():
     got = metrics.agreement(g, gs, gs[:, :2] * 0.1, end, bst, cend, cst, 1, recon=rec)
     assert got == ref
     assert ref["holes"] == 20 and ref["excluded"] == 0
+
+
+# ---- FTLE (oracle/ftle.py) -----------------------
+
+def _lattice_pts(dims, spacing):
+    idx = np.indices(dims[::-1]).reshape(len(dims), -1)[::-1].T
+    return idx * np.asarray(spacing, dtype=np.float64)
+
+
+def test_ftle_identity_translation_and_rotation_are_zero():
+    from oracle.ftle import ftle
+    dims, sp = (7, 6, 5), (0.1, 0.2, 0.3)
+    X = _lattice_pts(dims, sp)
+    th = 0.7
+    R = np.array([[np.cos(th), -np.sin(th), 0], [np.sin(th), np.cos(th), 0], [0, 0, 1]])
+    for F in (X, X + np.array([0.3, -1.0, 2.0]), X @ R.T + 0.5):
+        out, nbad = ftle(F, dims, sp, 2.5)
+        assert nbad == 0
+        np.testing.assert_allclose(out, 0.0, atol=1e-14)
+
+
+def test_ftle_diagonal_stretch_is_ln2():
+    """SPEC.md:466 example: end = diag(2, 0.5) seed, T = 1 -> ln 2 (every
+    node: one-sided differences are exact on linear maps too)."""
+    from oracle.ftle import ftle
+    dims, sp = (9, 8), (0.25, 0.5)
+    X = _lattice_pts(dims, sp)
+    out, _ = ftle(X * np.array([2.0, 0.5]), dims, sp, 1.0)
+    np.testing.assert_allclose(out, np.log(2.0), rtol=0, atol=1e-14)
+    out, _ = ftle(X * np.array([2.0, 0.5]), dims, sp, -4.0)           # |T|
+    np.testing.assert_allclose(out, np.log(2.0) / 4.0, rtol=0, atol=1e-14)
+
+
+def test_ftle_shear_closed_form():
+    """F = (x + k y, y, z): lambda_max(C) = 1 + k^2/2 + k sqrt(1 + k^2/4)."""
+    from oracle.ftle import ftle
+    dims, sp, k, T = (6, 7, 5), (0.3, 0.2, 0.1), 1.7, 3.0
+    X = _lattice_pts(dims, sp)
+    F = X.copy()
+    F[:, 0] += k * X[:, 1]
+    out, _ = ftle(F, dims, sp, T)
+    lam = 1 + k * k / 2 + k * np.sqrt(1 + k * k / 4)
+    np.testing.assert_allclose(out, 0.5 * np.log(lam) / T, rtol=1e-13)
+
+
+def test_ftle_quadratic_map_interior_central_difference_is_exact():
+    """F = X + c X^2 per component: central differences are exact on
+    quadratics, so interior nodes match the analytic gradient 1 + 2 c x;
+    faces use one-sided differences (1 + c(2x + h))."""
+    from oracle.ftle import ftle
+    dims, sp, c, T = (8, 6), (0.2, 0.3), np.array([0.4, -0.3]), 1.5
+    X = _lattice_pts(dims, sp)
+    out, _ = ftle(X + c * X ** 2, dims, sp, T)
+    ix = X / np.array(sp)
+    g = 1 + 2 * c * X                                                  # interior: diagonal J
+    lo = ix == 0
+    hi = ix == np.array(dims) - 1
+    g = np.where(lo, 1 + c * (2 * X + np.array(sp)), g)
+    g = np.where(hi, 1 + c * (2 * X - np.array(sp)), g)
+    expect = np.log(np.abs(g).max(axis=1)) / T
+    np.testing.assert_allclose(out, expect, rtol=0, atol=1e-12)
+
+
+def test_ftle_degenerate_tensor_counted_and_nan_propagates():
+    from oracle.ftle import ftle
+    dims, sp = (4, 4), (1.0, 1.0)
+    F = np.zeros((16, 2))                                              # collapsed map: C = 0
+    out, nbad = ftle(F, dims, sp, 1.0)
+    assert nbad == 16 and (out == 0).all()
+    F = _lattice_pts(dims, sp)
+    F[5] = np.nan
+    out, nbad = ftle(F, dims, sp, 1.0)
+    # node 5 feeds the stencils of its 4 neighbours, not its own central difference
+    assert np.isnan(out[[1, 4, 6, 9]]).all() and np.isfinite(out[[0, 5, 15]]).all() and nbad == 0
