@@ -231,6 +231,26 @@ LAG_API int64_t lag_kernel_launches(lag_ctx ctx);
 LAG_API lag_status lag_gridfill(int32_t dim, const int64_t* dims, int32_t k, const double* values,
                                 const uint8_t* valid, double* out, uint8_t* filled, void* stream);
 
+/* lag_ftle — finite-time Lyapunov exponent of a flow map on a dense seed
+ * lattice (paper P:415-416 §4.3, FTLE fields from basis flows post hoc;
+ * operation as SPEC.md:460-468 states it).
+ *   dim        2 or 3.
+ *   dims       [dim] host array: lattice extent per axis (x fastest), each >= 1.
+ *   spacing    [dim] host array: seed spacing per axis (stride * h), > 0.
+ *   T          integration time of the flow map (nonzero, finite; |T| is used).
+ *   ends       DEVICE [n][dim] f64 end positions, n = prod(dims) (complete
+ *              lattice, e.g. after lag_gridfill).
+ *   ftle       DEVICE [n] f64 out: ln(sqrt(lambda_max(J^T J))) / |T| with J
+ *              the flow-map gradient by central differences (one-sided at
+ *              lattice faces; an axis of extent 1 contributes 0); 0 where
+ *              lambda_max <= 0; NaN where the stencil holds non-finite ends.
+ *   n_degenerate  host out (may be NULL): nodes with lambda_max <= 0.
+ *   stream     cudaStream_t (NULL = legacy default); the call synchronises it.
+ * Errors: LAG_EINVAL (bad sizes, spacing, T, NULL or non-device pointers),
+ * LAG_ENOMEM, LAG_ECUDA; message in lag_last_error(NULL). */
+LAG_API lag_status lag_ftle(int32_t dim, const int64_t* dims, const double* spacing, double T,
+                            const double* ends, double* ftle, int64_t* n_degenerate, void* stream);
+
 /* lag_abi_version — LAG_ABI_VERSION the library was built with. */
 LAG_API int32_t lag_abi_version(void);
 

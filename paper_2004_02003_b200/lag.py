@@ -29,7 +29,7 @@ STATUS_NAMES = {0: "LAG_OK", -1: "LAG_EINVAL", -2: "LAG_ESTATE", -3: "LAG_EEMPTY
 # every symbol include/lag.h declares
 EXPORTS = ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_extract_ex", "lag_stats",
            "lag_destroy", "lag_last_error", "lag_nccl_unique_id", "lag_kernel_launches",
-           "lag_abi_version", "lag_gridfill")
+           "lag_abi_version", "lag_gridfill", "lag_ftle")
 
 
 class LagError(RuntimeError):
@@ -84,10 +84,13 @@ def load(path: str = LIB_PATH):
     lib.lag_kernel_launches.argtypes = [vp]
     lib.lag_kernel_launches.restype = ctypes.c_int64
     lib.lag_abi_version.restype = ctypes.c_int32
+    if hasattr(lib, "lag_ftle"):
+        lib.lag_ftle.argtypes = [ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_double), ctypes.c_double,
+                                 vp, vp, P(ctypes.c_int64), vp]
     if hasattr(lib, "lag_gridfill"):
         lib.lag_gridfill.argtypes = [ctypes.c_int32, P(ctypes.c_int64), ctypes.c_int32, vp, vp, vp, vp, vp]
     for name in ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_extract_ex", "lag_stats",
-                 "lag_destroy", "lag_nccl_unique_id", "lag_gridfill"):
+                 "lag_destroy", "lag_nccl_unique_id", "lag_gridfill", "lag_ftle"):
         if hasattr(lib, name):
             getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -228,6 +231,22 @@ def lag_gridfill(values, valid, dims: Sequence[int], out=None, filled=None, stre
     s = stream
     _check(load().lag_gridfill(dim, d, k, _addr(values), _addr(valid), _addr(out), _addr(filled), s))
     return out, filled
+
+
+def lag_ftle(ends, dims: Sequence[int], spacing: Sequence[float], T: float, out=None, stream=None):
+    """FTLE of a flow map on a dense lattice (include/lag.h).  `ends` [n, dim]
+    f64 device tensor, x fastest.  Returns (ftle [n], n_degenerate)."""
+    import torch
+    dim = len(dims)
+    if out is None:
+        out = torch.empty((ends.shape[0],), dtype=torch.float64, device=ends.device)
+    d = (ctypes.c_int64 * 3)(*[int(x) for x in dims], *([1] * (3 - dim)))
+    sp = (ctypes.c_double * 3)(*[float(x) for x in spacing], *([1.0] * (3 - dim)))
+    nd = ctypes.c_int64(0)
+    if stream is None:
+        stream = torch.cuda.current_stream(ends.device).cuda_stream if ends.is_cuda else 0
+    _check(load().lag_ftle(dim, d, sp, float(T), _addr(ends), _addr(out), ctypes.byref(nd), stream))
+    return out, nd.value
 
 
 def lag_kernel_launches(ctx) -> int:

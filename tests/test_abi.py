@@ -109,3 +109,15 @@ def test_gridfill_rejects_null_and_bad_sizes_without_a_gpu():
     assert lib.lag_gridfill(4, dims, 2, 1, 1, 1, 1, None) == P.LAG_EINVAL
     assert lib.lag_gridfill(2, dims, 0, 1, 1, 1, 1, None) == P.LAG_EINVAL
     assert "gridfill" in P.lag_last_error(None)
+
+
+def test_ftle_rejects_bad_arguments_without_a_gpu():
+    import ctypes
+    lib = P.load()
+    dims = (ctypes.c_int64 * 3)(4, 4, 4)
+    sp = (ctypes.c_double * 3)(1.0, 1.0, 1.0)
+    assert lib.lag_ftle(3, dims, sp, 1.0, None, None, None, None) == P.LAG_EINVAL
+    assert lib.lag_ftle(3, dims, sp, 0.0, 1, 1, None, None) == P.LAG_EINVAL
+    assert lib.lag_ftle(1, dims, sp, 1.0, 1, 1, None, None) == P.LAG_EINVAL
+    bad = (ctypes.c_double * 3)(1.0, -1.0, 1.0)
+    assert lib.lag_ftle(3, dims, bad, 1.0, 1, 1, None, None) == P.LAG_EINVAL
