@@ -551,3 +551,100 @@ def test_ftle_degenerate_tensor_counted_and_nan_propagates():
     out, nbad = ftle(F, dims, sp, 1.0)
     # node 5 feeds the stencils of its 4 neighbours, not its own central difference
     assert np.isnan(out[[1, 4, 6, 9]]).all() and np.isfinite(out[[0, 5, 15]]).all() and nbad == 0
+
+
+# ---- pathline stitching (oracle/pathline.py; §3.2) -
+
+def _lat(dims, origin, sp):
+    idx = np.indices(dims[::-1]).reshape(len(dims), -1)[::-1].T
+    return np.asarray(origin) + idx * np.asarray(sp)
+
+
+def test_kuhn_weights_reproduce_the_point_and_are_convex():
+    from oracle.pathline import kuhn_weights
+    rng = np.random.default_rng(11)
+    for d in (2, 3):
+        f = rng.random((500, d))
+        f[:20, 0] = f[:20, 1]                               # ties
+        f[20:30] = np.round(f[20:30])                       # cube corners
+        off, w = kuhn_weights(f)
+        assert (w >= 0).all()
+        np.testing.assert_allclose(w.sum(1), 1.0, atol=1e-15)
+        np.testing.assert_allclose(np.einsum("mj,mjc->mc", w, off), f, atol=1e-15)
+        # consecutive vertices differ in exactly one axis (a Kuhn path 0 -> 1...1)
+        assert (np.abs(np.diff(off, axis=1)).sum(2) == 1).all()
+
+
+def test_stitched_affine_maps_compose_exactly():
+    """Barycentric interpolation is exact on affine maps, so stitching the
+    maps x -> M_k x + b_k equals their composition."""
+    from oracle.pathline import stitch
+    dims, o, sp = (9, 8, 7), (-1.0, 0.5, 2.0), (0.5, 0.25, 0.3)
+    X = _lat(dims, o, sp)
+    c = np.array(o) + (np.array(dims) - 1) * np.array(sp) / 2          # lattice centre
+    maps = [(np.array([[1.02, 0.05, 0.0], [-0.03, 0.98, 0.02], [0.01, 0.0, 1.01]]), np.array([0.02, -0.01, 0.03])),
+            (np.array([[0.99, -0.02, 0.01], [0.04, 1.01, 0.0], [0.0, 0.03, 0.97]]), np.array([-0.05, 0.02, 0.0])),
+            (np.eye(3) * 1.01, np.array([0.0, 0.0, -0.02]))]
+    ends = np.stack([(X - c) @ M.T + c + b for M, b in maps])
+    rng = np.random.default_rng(4)
+    q = c + (rng.random((200, 3)) - 0.5) * (np.array(dims) - 1) * np.array(sp) * 0.6
+    path, status, samples, _ = stitch(ends, None, dims, o, sp, q)
+    assert (status == 0).all() and (samples == 4).all()
+    x = q.copy()
+    for k, (M, b) in enumerate(maps):
+        x = (x - c) @ M.T + c + b
+        np.testing.assert_allclose(path[:, k + 1], x, rtol=0, atol=1e-13)
+
+
+def test_stitch_uniform_flow_example_and_hull_truncation():
+    """uniform v = (1,0,0), dt = 0.1, two intervals of 5 cycles,
+    seed (0.1, 0.5, 0.5) -> samples (0.6, .5, .5), (1.1, .5, .5); a third
+    interval from 1.1 on a [0, 1.5] lattice lands outside the hull and the
+    fourth is truncated."""
+    from oracle.pathline import stitch, OUT_OF_HULL
+    dims, o, sp = (16, 3, 3), (0.0, 0.0, 0.0), (0.1, 0.5, 0.5)
+    X = _lat(dims, o, sp)
+    ends = np.stack([X + np.array([0.5, 0.0, 0.0])] * 4)
+    path, status, samples, _ = stitch(ends, None, dims, o, sp, np.array([[0.1, 0.5, 0.5]]))
+    np.testing.assert_allclose(path[0, 1], [0.6, 0.5, 0.5], atol=1e-15)
+    np.testing.assert_allclose(path[0, 2], [1.1, 0.5, 0.5], atol=1e-15)
+    np.testing.assert_allclose(path[0, 3], [1.6, 0.5, 0.5], atol=1e-15)   # interpolated from inside
+    assert status[0] == OUT_OF_HULL and samples[0] == 4 and np.isnan(path[0, 4]).all()
+
+
+def test_stitch_identity_map_is_stationary_and_invalid_flows_truncate():
+    from oracle.pathline import stitch, INVALID_FLOW
+    dims, o, sp = (5, 4), (0.0, 0.0), (1.0, 1.0)
+    X = _lat(dims, o, sp)
+    ends = np.stack([X, X])
+    valid = np.ones((2, 20), bool)
+    valid[1, 6] = False                                        # node (1, 1)
+    q = np.array([[1.0, 2.0], [1.5, 1.25], [2.0, 2.0], [0.5, 2.5], [4.0, 3.0]])   # last: top corner
+    path, status, samples, _ = stitch(ends, valid, dims, o, sp, q)
+    # (1.5, 1.25) lies in the cube at (1, 1), whose simplex holds node (1, 1)
+    # with weight 0.5 > 0, so its second interval is truncated.  Nodes and
+    # points whose simplex gives (1, 1) weight 0 are unaffected.
+    assert list(status) == [0, INVALID_FLOW, 0, 0, 0]
+    np.testing.assert_array_equal(path[[0, 2, 3, 4], 2], q[[0, 2, 3, 4]])
+    assert samples[1] == 2
+
+
+def test_stitch_interpolant_is_continuous_across_simplices_and_cubes():
+    """Kuhn simplices conform: for a nonlinear map, the interpolant evaluated
+    just either side of simplex facets (f_a = f_b) and of cube faces differs
+    by O(eps)."""
+    from oracle.pathline import stitch
+    dims, o, sp = (6, 6, 6), (0.0, 0.0, 0.0), (1.0, 1.0, 1.0)
+    X = _lat(dims, o, sp)
+    ends = (X + 0.3 * np.sin(X[:, ::-1]) + 0.1 * X ** 2)[None]
+    rng = np.random.default_rng(8)
+    base = 1 + 3 * rng.random((300, 3))
+    base[:100, 1] = np.floor(base[:100, 1]) + (base[:100, 0] - np.floor(base[:100, 0]))   # f_x = f_y facet
+    base[100:200, 2] = np.round(base[100:200, 2])                                        # cube face
+    eps = 1e-9
+    for ax in range(3):
+        dv = np.zeros(3)
+        dv[ax] = eps
+        a = stitch(ends, None, dims, o, sp, base + dv)[0][:, 1]
+        b = stitch(ends, None, dims, o, sp, base - dv)[0][:, 1]
+        assert np.abs(a - b).max() < 50 * eps
