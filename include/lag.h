@@ -251,6 +251,29 @@ LAG_API lag_status lag_gridfill(int32_t dim, const int64_t* dims, int32_t k, con
 LAG_API lag_status lag_ftle(int32_t dim, const int64_t* dims, const double* spacing, double T,
                             const double* ends, double* ftle, int64_t* n_degenerate, void* stream);
 
+/* lag_stitch — pathlines stitched from the basis flows of K successive
+ * intervals (§3.2 "a trajectory can be stitched together by using basis
+ * flows of successive nonoverlapping intervals"; barycentric interpolation of
+ * end positions).  Reading R16: on the
+ * seed lattice the Delaunay ties are broken by the fixed Kuhn template (cube
+ * split along the descending order of the local coordinates).
+ *   dim, dims      2 or 3; [dim] host array, lattice extent per axis (>= 2).
+ *   origin, spacing [dim] host arrays: lattice node 0 and seed spacing (> 0).
+ *   K              number of intervals (>= 0).
+ *   ends           DEVICE [K][n][dim] f64 end positions per interval, x fastest.
+ *   valid          DEVICE [K][n] u8 (nonzero = valid basis flow) or NULL = all.
+ *   m, starts      number of pathlines; DEVICE [m][dim] f64 start points.
+ *   path           DEVICE [m][K+1][dim] f64 out: path[q][0] = start, then one
+ *                  sample per interval; NaN after a truncation.
+ *   status         DEVICE [m] u8 out: 0 complete, 1 left the lattice hull (no
+ *                  clamping), 2 needed an invalid basis flow
+ *                  (fill holes first, lag_gridfill).
+ *   stream         cudaStream_t (NULL = legacy default); the call synchronises it.
+ * Errors: LAG_EINVAL (sizes, spacing, NULL or non-device pointers), LAG_ECUDA. */
+LAG_API lag_status lag_stitch(int32_t dim, const int64_t* dims, const double* origin, const double* spacing,
+                              int32_t K, const double* ends, const uint8_t* valid, int64_t m,
+                              const double* starts, double* path, uint8_t* status, void* stream);
+
 /* lag_abi_version — LAG_ABI_VERSION the library was built with. */
 LAG_API int32_t lag_abi_version(void);
 

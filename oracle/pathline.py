@@ -19,9 +19,9 @@ conforming, so the interpolant is continuous across cubes and simplices.
 
 Per interval k and query x:
   * u = (x - origin) / spacing.
-  * Outside the lattice hull (some u_a < 0 or u_a > dims_a - 1): the pathline
-    is truncated (status OUT_OF_HULL) at its last sample. SPEC.md:358: no
-    clamping.
+  * Outside the lattice hull (some u_a < 0 or u_a > dims_a - 1, or not a
+    number): the pathline is truncated (status OUT_OF_HULL) at its last
+    sample. SPEC.md:358: no clamping.
   * Otherwise cube i = min(floor(u), dims - 2) and f = u - i.
   * If a vertex with weight > 0 has an invalid basis flow: status
     INVALID_FLOW, truncated. Fill the holes first (GridFill) to avoid this.
@@ -79,7 +79,7 @@ def stitch(ends: np.ndarray, valid: Optional[np.ndarray], dims: Sequence[int], o
         u = (x - origin) / spacing
         dist = np.minimum(u, (dims - 1) - u).min(axis=1)
         min_hull = np.where(alive, np.minimum(min_hull, np.abs(dist)), min_hull)
-        out = alive & ((u < 0) | (u > dims - 1)).any(axis=1)
+        out = alive & ~((u >= 0) & (u <= dims - 1)).all(axis=1)      # a NaN position is outside too
         status[out] = OUT_OF_HULL
         alive &= ~out
         idx = np.nonzero(alive)[0]

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblag.so")
-SOURCES = ["lag_api.cu", "lag_comm.cu", "lag_peer.cu", "lag_recon.cu", "lag_ftle.cu"]
+SOURCES = ["lag_api.cu", "lag_comm.cu", "lag_peer.cu", "lag_recon.cu", "lag_ftle.cu", "lag_pathline.cu"]
 HEADERS = ["lag_kernels.cuh", "lag_internal.h", "lag_append.cuh"]
 
 

@@ -29,7 +29,7 @@ STATUS_NAMES = {0: "LAG_OK", -1: "LAG_EINVAL", -2: "LAG_ESTATE", -3: "LAG_EEMPTY
 # every symbol include/lag.h declares
 EXPORTS = ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_extract_ex", "lag_stats",
            "lag_destroy", "lag_last_error", "lag_nccl_unique_id", "lag_kernel_launches",
-           "lag_abi_version", "lag_gridfill", "lag_ftle")
+           "lag_abi_version", "lag_gridfill", "lag_ftle", "lag_stitch")
 
 
 class LagError(RuntimeError):
@@ -84,13 +84,16 @@ def load(path: str = LIB_PATH):
     lib.lag_kernel_launches.argtypes = [vp]
     lib.lag_kernel_launches.restype = ctypes.c_int64
     lib.lag_abi_version.restype = ctypes.c_int32
+    if hasattr(lib, "lag_stitch"):
+        lib.lag_stitch.argtypes = [ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_double), P(ctypes.c_double),
+                                   ctypes.c_int32, vp, vp, ctypes.c_int64, vp, vp, vp, vp]
     if hasattr(lib, "lag_ftle"):
         lib.lag_ftle.argtypes = [ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_double), ctypes.c_double,
                                  vp, vp, P(ctypes.c_int64), vp]
     if hasattr(lib, "lag_gridfill"):
         lib.lag_gridfill.argtypes = [ctypes.c_int32, P(ctypes.c_int64), ctypes.c_int32, vp, vp, vp, vp, vp]
     for name in ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_extract_ex", "lag_stats",
-                 "lag_destroy", "lag_nccl_unique_id", "lag_gridfill", "lag_ftle"):
+                 "lag_destroy", "lag_nccl_unique_id", "lag_gridfill", "lag_ftle", "lag_stitch"):
         if hasattr(lib, name):
             getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -247,6 +250,28 @@ def lag_ftle(ends, dims: Sequence[int], spacing: Sequence[float], T: float, out=
         stream = torch.cuda.current_stream(ends.device).cuda_stream if ends.is_cuda else 0
     _check(load().lag_ftle(dim, d, sp, float(T), _addr(ends), _addr(out), ctypes.byref(nd), stream))
     return out, nd.value
+
+
+def lag_stitch(ends, starts, dims: Sequence[int], origin: Sequence[float], spacing: Sequence[float],
+               valid=None, path=None, status=None, stream=None):
+    """Stitch pathlines through K flow maps (include/lag.h).  `ends` [K, n, dim]
+    f64 and `starts` [m, dim] f64 device tensors, `valid` [K, n] u8 or None.
+    Returns (path [m, K+1, dim], status [m])."""
+    import torch
+    dim = len(dims)
+    K, m = int(ends.shape[0]), int(starts.shape[0])
+    if path is None:
+        path = torch.empty((m, K + 1, dim), dtype=torch.float64, device=starts.device)
+    if status is None:
+        status = torch.empty((m,), dtype=torch.uint8, device=starts.device)
+    d = (ctypes.c_int64 * 3)(*[int(x) for x in dims], *([1] * (3 - dim)))
+    o = (ctypes.c_double * 3)(*[float(x) for x in origin[:dim]], *([0.0] * (3 - dim)))
+    sp = (ctypes.c_double * 3)(*[float(x) for x in spacing[:dim]], *([1.0] * (3 - dim)))
+    if stream is None:
+        stream = torch.cuda.current_stream(starts.device).cuda_stream if starts.is_cuda else 0
+    _check(load().lag_stitch(dim, d, o, sp, K, _addr(ends), _addr(valid), m, _addr(starts), _addr(path),
+                             _addr(status), stream))
+    return path, status
 
 
 def lag_kernel_launches(ctx) -> int:

@@ -121,3 +121,16 @@ def test_ftle_rejects_bad_arguments_without_a_gpu():
     assert lib.lag_ftle(1, dims, sp, 1.0, 1, 1, None, None) == P.LAG_EINVAL
     bad = (ctypes.c_double * 3)(1.0, -1.0, 1.0)
     assert lib.lag_ftle(3, dims, bad, 1.0, 1, 1, None, None) == P.LAG_EINVAL
+
+
+def test_stitch_rejects_bad_arguments_without_a_gpu():
+    import ctypes
+    lib = P.load()
+    dims = (ctypes.c_int64 * 3)(4, 4, 4)
+    o = (ctypes.c_double * 3)(0.0, 0.0, 0.0)
+    sp = (ctypes.c_double * 3)(1.0, 1.0, 1.0)
+    assert lib.lag_stitch(3, dims, o, sp, 1, None, None, 5, 1, 1, 1, None) == P.LAG_EINVAL   # ends NULL
+    assert lib.lag_stitch(3, dims, o, sp, -1, 1, None, 5, 1, 1, 1, None) == P.LAG_EINVAL
+    one = (ctypes.c_int64 * 3)(4, 1, 4)
+    assert lib.lag_stitch(3, one, o, sp, 1, 1, None, 5, 1, 1, 1, None) == P.LAG_EINVAL    # extent < 2
+    assert lib.lag_stitch(3, dims, o, sp, 1, 1, None, 0, None, None, None, None) == P.LAG_OK  # no pathlines
