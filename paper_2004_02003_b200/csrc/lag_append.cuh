@@ -29,52 +29,59 @@ struct AppendArgs {
     int zero_recv;                  // peer transport: reset the consumed inbox headers instead
 };
 
-// one CTA: received particles become new tiles at the end of the list
+// Received particles become new tiles at the end of the list.  Every CTA of
+// the calling grid takes a grid-stride share of the records (one latency
+// round for a few thousand hand-offs instead of one per 256 records); each
+// CTA reads the headers and the old tile count first, and the last CTA to
+// finish resets the headers and publishes the new tile count.
 __device__ __forceinline__ void append_body(const AppendArgs& a) {
     __shared__ uint32_t pre[kMaxOff + 1];
-    __shared__ uint32_t old_tiles;
+    __shared__ uint32_t old_tiles, total_s;
     if (threadIdx.x == 0) {
         uint32_t s = 0;
         for (int p = 0; p < a.npeers; ++p) {
             pre[p] = s;
-            uint32_t c = *reinterpret_cast<const uint32_t*>(a.recv[p]);
+            uint32_t c = *reinterpret_cast<const volatile uint32_t*>(a.recv[p]);
             if (c > a.cap[p]) { c = a.cap[p]; atomicOr(a.words + W_ERR, ERR_OVERFLOW); }
             s += c;
         }
         pre[a.npeers] = s;
-        old_tiles = a.words[W_NTILES];
+        old_tiles = *reinterpret_cast<const volatile uint32_t*>(a.words + W_NTILES);
+        const uint32_t room = (uint32_t)(a.cap_tiles - (int)old_tiles) * kTile;
+        if (s > room) { atomicOr(a.words + W_ERR, ERR_OVERFLOW); s = room; }
+        total_s = s;
     }
     __syncthreads();
-    uint32_t total = pre[a.npeers];
-    const uint32_t room = (uint32_t)(a.cap_tiles - (int)old_tiles) * kTile;
-    if (total > room) {
-        if (threadIdx.x == 0) atomicOr(a.words + W_ERR, ERR_OVERFLOW);
-        total = room;
-    }
-    for (uint32_t j = threadIdx.x; j < total; j += blockDim.x) {
+    const uint32_t total = total_s;
+    const uint32_t nthr = gridDim.x * blockDim.x;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < total; j += nthr) {
         int p = 0;
         while (p + 1 < a.npeers && pre[p + 1] <= j) ++p;
         a.state[(size_t)old_tiles * kTile + j] = a.recv[p][1 + (j - pre[p])];
     }
     const uint32_t new_tiles = (total + kTile - 1) / kTile;
-    for (uint32_t t = threadIdx.x; t < new_tiles; t += blockDim.x) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < new_tiles; t += nthr) {
         const uint32_t rem = total - t * kTile;
         a.tile_count[old_tiles + t] = (uint8_t)(rem >= (uint32_t)kTile ? kTile : rem);
     }
-    __syncthreads();                 // every count read before any header reset
-    if (a.zero_recv) {
-        if (threadIdx.x < (unsigned)a.npeers) *reinterpret_cast<uint32_t*>(a.recv[threadIdx.x]) = 0u;
-    } else if (threadIdx.x < (unsigned)a.noff) {
-        *reinterpret_cast<uint32_t*>(a.slots + a.slot_base[threadIdx.x]) = 0u;
-    }
-    __syncthreads();
+    __syncthreads();                 // this CTA read every header and wrote its share
     if (threadIdx.x == 0) {
-        a.words[W_NTILES] = old_tiles + new_tiles;
-        if (total) atomicAdd(&a.counters[CNT_RECV], (unsigned long long)total);
+        __threadfence();
+        if (atomicAdd(a.words + W_APPEND_DONE, 1u) == gridDim.x - 1) {      // last CTA
+            a.words[W_APPEND_DONE] = 0u;
+            if (a.zero_recv) {
+                for (int p = 0; p < a.npeers; ++p) *reinterpret_cast<uint32_t*>(a.recv[p]) = 0u;
+            } else {
+                for (int k = 0; k < a.noff; ++k) *reinterpret_cast<uint32_t*>(a.slots + a.slot_base[k]) = 0u;
+            }
+            a.words[W_NTILES] = old_tiles + new_tiles;
+            if (total) atomicAdd(&a.counters[CNT_RECV], (unsigned long long)total);
+            __threadfence();
+        }
     }
 }
 
 
-static __global__ void __launch_bounds__(1024) append_kernel(AppendArgs a) { append_body(a); }
+static __global__ void __launch_bounds__(256) append_kernel(AppendArgs a) { append_body(a); }
 
 }  // namespace lag

@@ -46,6 +46,7 @@ lag_status lag_peer_wait(lag_ctx_s* ctx, PeerState* ps, const std::vector<int>& 
                          unsigned long long need_halo, unsigned long long need_part);
 lag_status lag_peer_unpack(lag_ctx_s* ctx, PeerState* ps, float* v0, float* v1, bool with_v0, int parity);
 uint32_t* lag_peer_done_counter(PeerState* ps);
+unsigned long long* lag_peer_timeline(PeerState* ps);
 unsigned long long* lag_peer_remote_flag(PeerState* ps, int i, int kind, int pback);
 lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_boxes, int nsend,
                              int64_t sfl, float* v0, float* v1, bool with_v0, bool halo,
@@ -456,7 +457,7 @@ static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity);
 
 static lag_status launch_append(lag_ctx_s* ctx, int peer_parity = -1) {
     AppendArgs a = append_args(ctx, peer_parity);
-    append_kernel<<<1, 1024, 0, ctx->stream>>>(a);
+    append_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(a);
     ++ctx->launches;
     CKC(cudaGetLastError());
     return LAG_OK;
@@ -564,6 +565,9 @@ void lag_comm_fill_args(lag_ctx_s* ctx, AdvectArgs* a) {
         a->n_sig = (int)cm->peers.size();
         a->sig_value = seq;
         a->done_warps = lag_peer_done_counter(cm->peer);
+#ifdef LAG_EXP_TIMELINE
+        a->tl = lag_peer_timeline(cm->peer);
+#endif
     }
 }
 

@@ -7,7 +7,7 @@
 #include <string>
 
 namespace lag {
-enum : int { W_DEAD = 0, W_ERR = 1, W_NTILES = 2, kWords = 8 };
+enum : int { W_DEAD = 0, W_ERR = 1, W_NTILES = 2, W_APPEND_DONE = 3, kWords = 8 };
 struct Comm;   // lag_comm.cu
 }
 

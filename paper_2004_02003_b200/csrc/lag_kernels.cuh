@@ -85,7 +85,18 @@ struct AdvectArgs {
     int32_t n_sig;
     unsigned long long sig_value;
     uint32_t* done_warps;
+#ifdef LAG_EXP_TIMELINE
+    unsigned long long* tl;         // experiment: per-cycle globaltimer stamps [64][8]
+#endif
 };
+
+#ifdef LAG_EXP_TIMELINE
+__device__ __forceinline__ unsigned long long lag_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 __device__ __forceinline__ void unpack_g(uint32_t w, const AdvectArgs& a, int g[3]) {
     g[0] = (int)(w & a.mx);
@@ -472,6 +483,9 @@ advect_kernel(const AdvectArgs a) {
     unsigned long long steps = 0, nterm = 0, nexit = 0, nsent = 0;
     uint32_t errbits = 0;
     bool did_remote = false;
+#ifdef LAG_EXP_TIMELINE
+    if (a.tl && blockIdx.x == 0 && threadIdx.x == 0) a.tl[(a.sig_value & 63) * 8 + 6] = lag_gtimer();
+#endif
 
     // software pipeline: the next tile's count and records are in flight while
     // the current tile computes
@@ -707,6 +721,9 @@ advect_kernel(const AdvectArgs a) {
                 const uint32_t total = (gridDim.x * kThreads) >> 5;
                 if (atomicAdd(a.done_warps, 1u) == total - 1) {  // last warp of the grid
                     *a.done_warps = 0u;
+#ifdef LAG_EXP_TIMELINE
+                    if (a.tl) a.tl[(a.sig_value & 63) * 8 + 7] = lag_gtimer();
+#endif
                     __threadfence_system();
                     for (int k = 0; k < a.n_sig; ++k)
                         *reinterpret_cast<volatile unsigned long long*>(a.sig_flag[k]) = a.sig_value;

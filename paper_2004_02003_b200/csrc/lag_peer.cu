@@ -24,6 +24,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <unistd.h>
 #include <cstring>
 #include <vector>
 
@@ -157,9 +160,18 @@ struct XchgArgs {
     int sx, sxy, dim;
     unsigned long long seq;
     int do_append;
+#ifdef LAG_EXP_TIMELINE
+    unsigned long long* tl;
+#endif
 };
 
 __global__ void __launch_bounds__(256) peer_pack_signal_kernel(XchgArgs x) {
+#ifdef LAG_EXP_TIMELINE
+    if (x.tl && blockIdx.x == 0 && threadIdx.x == 0) x.tl[(x.seq & 63) * 8 + 0] = lag_gtimer();
+#endif
+#ifdef LAG_EXP_NOPACK
+    if (false)
+#endif
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < x.sfl;
          i += (int64_t)gridDim.x * blockDim.x) {
         int k = 0;
@@ -177,6 +189,9 @@ __global__ void __launch_bounds__(256) peer_pack_signal_kernel(XchgArgs x) {
         __threadfence_system();                       // cumulative: orders the CTA's packs
         if (atomicAdd(x.done_ctas, 1u) == gridDim.x - 1) {   // last CTA: halo(seq) ready
             *x.done_ctas = 0u;
+#ifdef LAG_EXP_TIMELINE
+            if (x.tl) x.tl[(x.seq & 63) * 8 + 1] = lag_gtimer();
+#endif
             __threadfence_system();
             for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(x.halo_flag[p]) = x.seq;
             __threadfence_system();
@@ -185,6 +200,10 @@ __global__ void __launch_bounds__(256) peer_pack_signal_kernel(XchgArgs x) {
 }
 
 __global__ void __launch_bounds__(256) peer_wait_pull_kernel(XchgArgs x, AppendArgs ap) {
+#ifdef LAG_EXP_TIMELINE
+    if (x.tl && blockIdx.x == 0 && threadIdx.x == 0) x.tl[(x.seq & 63) * 8 + 2] = lag_gtimer();
+#endif
+#ifndef LAG_EXP_NOWAIT
     if (threadIdx.x < x.npeers) {
         const volatile unsigned long long* fh = x.my_flags + 0 * kOff + x.back[threadIdx.x];
         const volatile unsigned long long* fp = x.my_flags + 1 * kOff + x.back[threadIdx.x];
@@ -195,7 +214,14 @@ __global__ void __launch_bounds__(256) peer_wait_pull_kernel(XchgArgs x, AppendA
         }
         __threadfence_system();
     }
+#endif
     __syncthreads();
+#ifdef LAG_EXP_TIMELINE
+    if (x.tl && threadIdx.x == 0) atomicMax(x.tl + (x.seq & 63) * 8 + 3, lag_gtimer());
+#endif
+#ifdef LAG_EXP_NOPULL
+    if (false)
+#endif
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < x.rtotal;
          i += (int64_t)gridDim.x * blockDim.x) {
         int k = 0;
@@ -209,7 +235,15 @@ __global__ void __launch_bounds__(256) peer_wait_pull_kernel(XchgArgs x, AppendA
         dst[(int64_t)x.dim * ((b.x0 + xx) + (int64_t)x.sx * (b.y0 + yy) + (int64_t)x.sxy * (b.z0 + zz)) + comp] =
             b.src[x.parity][b.slice][j];
     }
-    if (blockIdx.x == 0 && x.do_append) append_body(ap);      // hand-offs of cycle seq-1
+#ifdef LAG_EXP_TIMELINE
+    __syncthreads();
+    if (x.tl && threadIdx.x == 0) atomicMax(x.tl + (x.seq & 63) * 8 + 4, lag_gtimer());
+#endif
+    if (x.do_append) append_body(ap);                         // hand-offs of cycle seq-1 (all CTAs)
+#ifdef LAG_EXP_TIMELINE
+    __syncthreads();
+    if (x.tl && threadIdx.x == 0) atomicMax(x.tl + (x.seq & 63) * 8 + 5, lag_gtimer());
+#endif
 }
 
 }  // namespace lag
@@ -232,6 +266,7 @@ struct PeerState {
     unsigned long long seq = 0;
     uint32_t* done_warps = nullptr;           // advect completion counter
     uint32_t* done_ctas = nullptr;            // pack-kernel completion counter
+    unsigned long long* tl = nullptr;         // experiment timeline [64][8]
 };
 
 lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>& prank,
@@ -319,6 +354,10 @@ lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>
     CKC(cudaMalloc(&ps->done_warps, 2 * sizeof(uint32_t)));
     CKC(cudaMemset(ps->done_warps, 0, 2 * sizeof(uint32_t)));
     ps->done_ctas = ps->done_warps + 1;
+#ifdef LAG_EXP_TIMELINE
+    CKC(cudaMalloc(&ps->tl, 64 * 8 * sizeof(unsigned long long)));
+    CKC(cudaMemset(ps->tl, 0, 64 * 8 * sizeof(unsigned long long)));
+#endif
     CKC(cudaMalloc(&ps->d_boxes, sizeof(PeerBox) * std::max<size_t>(1, ps->boxes.size())));
     if (!ps->boxes.empty())
         CKC(cudaMemcpy(ps->d_boxes, ps->boxes.data(), sizeof(PeerBox) * ps->boxes.size(), cudaMemcpyHostToDevice));
@@ -329,6 +368,27 @@ lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>
 
 void lag_peer_destroy(PeerState* ps) {
     if (!ps) return;
+#ifdef LAG_EXP_TIMELINE
+    if (ps->tl) {
+        unsigned long long h[64 * 8];
+        cudaDeviceSynchronize();
+        cudaMemcpy(h, ps->tl, sizeof(h), cudaMemcpyDeviceToHost);
+        // per cycle, µs relative to the pack start: pack_end wp_start wait_done pull_done append_done adv_start adv_end
+        char fn[256];
+        const char* dir = getenv("LAG_TL_DIR");
+        snprintf(fn, sizeof(fn), "%s/tl_%d.txt", dir ? dir : ".", (int)getpid());
+        FILE* f = fopen(fn, "a");
+        for (int c = 0; f && c < 64; ++c) {
+            const unsigned long long* r = h + c * 8;
+            if (!r[0] || !r[7]) continue;
+            fprintf(f, "TL %d %llu", c, r[0]);
+            for (int k = 1; k < 8; ++k) fprintf(f, " %.1f", r[k] ? (double)(long long)(r[k] - r[0]) * 1e-3 : -1.0);
+            fprintf(f, "\n");
+        }
+        if (f) fclose(f);
+        cudaFree(ps->tl);
+    }
+#endif
     for (char* p : ps->remote) if (p) cudaIpcCloseMemHandle(p);
     cudaFree(ps->d_boxes);
     cudaFree(ps->done_warps);
@@ -406,6 +466,7 @@ float* lag_peer_outbox(PeerState* ps, int q) { return ps->outbox + (size_t)q * 2
 unsigned long long& lag_peer_seq(PeerState* ps) { return ps->seq; }
 
 uint32_t* lag_peer_done_counter(PeerState* ps) { return ps->done_warps; }
+unsigned long long* lag_peer_timeline(PeerState* ps) { return ps->tl; }
 
 unsigned long long* lag_peer_remote_flag(PeerState* ps, int i, int kind, int pback) {
     return reinterpret_cast<unsigned long long*>(ps->remote[i]) + kind * kOff + pback;
@@ -447,6 +508,10 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
     x.seq = seq;
     x.do_append = append_args ? 1 : 0;
     x.done_ctas = ps->done_ctas;
+#ifdef LAG_EXP_TIMELINE
+    x.tl = ps->tl;
+    if (ps->tl) cudaMemsetAsync(ps->tl + (seq & 63) * 8, 0, 8 * sizeof(unsigned long long), ctx->stream);
+#endif
     AppendArgs ap{};
     if (append_args) ap = *reinterpret_cast<const AppendArgs*>(append_args);
     const int cap = ctx->num_sms * 2;
