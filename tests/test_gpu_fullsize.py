@@ -98,3 +98,16 @@ def test_c4_full_size_block_sampled(interval):
     assert res["exit"] > 0                    # seeds on the global faces leave the domain
     # (at this CFL a stride-4 seed needs > 50 cycles to cross the 4 nodes to
     # an internal face; the termination path is covered by the C3/C5/C2 cases)
+
+
+@pytest.mark.parametrize("rank", [0, 7])
+def test_c2_full_size_block_sampled(rank):
+    """C2: ABC 128^3 over 2x2x2 blocks at stride 1 (262 144 particles per
+    block), interval 25; blocks 0 and 7 (opposite corners, three internal
+    faces each). Half of the sample lies within 4 nodes of an internal face,
+    so BTO terminations are checked at full size."""
+    cfg = L.make_config("C2")
+    b = L.decompose(cfg["grid"], cfg["layout"])[rank]
+    res, st, n = _lockstep(cfg, b, 1, cfg["interval"], near=4)
+    assert n == 64 ** 3
+    assert res["term"] > 100
