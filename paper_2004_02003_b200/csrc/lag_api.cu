@@ -155,7 +155,17 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     ctx->max_seeds = owned;
     // COMM: particles migrate in; keep room for 2x the owned nodes (+ tail tiles)
     ctx->cap = cfg->mode == LAG_COMM ? 2 * owned + 64 * kTile : owned;
-    ctx->cap_tiles = (ctx->cap + kTile - 1) / kTile;
+    // seed tiles in brick order (ragged bricks leave partial tiles; stride 1
+    // bounds every stride) + COMM room for appended tiles
+    ctx->brick[0] = D == 3 ? kBrickRows : 1;
+    ctx->brick[1] = D == 3 ? kBrickRows : 1;
+    {
+        int32_t o[3] = {1, 1, 1};
+        for (int a = 0; a < D; ++a) o[a] = (int32_t)(cfg->block_hi[a] - cfg->block_lo[a]);
+        const int64_t seed_tiles = brick_tiles(o, ctx->brick[0], ctx->brick[1]);
+        const int64_t extra = cfg->mode == LAG_COMM ? (ctx->cap - owned + kTile - 1) / kTile : 0;
+        ctx->cap_tiles = (int)(seed_tiles + extra);
+    }
 
     auto fail = [&](lag_status s) {
         std::string m = ctx->msg;
@@ -168,6 +178,7 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     if ((st = dmalloc(ctx, &ctx->dead_rec, (size_t)ctx->cap)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->dead_info, (size_t)ctx->cap)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->words, (size_t)kWords)) != LAG_OK) return fail(st);
+    if ((st = dmalloc(ctx, &ctx->bbox, (size_t)(ctx->cap_tiles / kBrickTiles + 1) * kBBoxInts)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->counters, (size_t)CNT_N)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->out_start, (size_t)owned * D)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->out_end, (size_t)owned * D)) != LAG_OK) return fail(st);
@@ -189,6 +200,14 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<2, true, false> : advect_kernel<2, false, false>, kThreads, 0);
     ctx->advect_blocks_per_sm = occ > 0 ? occ : 1;
+    if (D == 3) {
+        cudaFuncSetAttribute(advect_brick_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBoxBytes);
+        cudaFuncSetAttribute(advect_brick_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBoxBytes);
+    }
+    if (const char* o = getenv("LAG_ADV_OCC")) {       // experiment hook: fewer resident CTAs per SM
+        const int v = atoi(o);
+        if (v > 0 && v < ctx->advect_blocks_per_sm) ctx->advect_blocks_per_sm = v;
+    }
     {
         const char* pt = getenv("LAG_PHASE_TIMING");
         ctx->phase_timing = pt && pt[0] == '1';
@@ -206,7 +225,7 @@ extern "C" lag_status lag_destroy(lag_ctx ctx) {
     if (ctx->stream_synced_needed) cudaStreamSynchronize(ctx->stream);
     lag_comm_destroy(ctx);
     dfree(ctx->state); dfree(ctx->tile_count); dfree(ctx->dead_rec); dfree(ctx->dead_info);
-    dfree(ctx->words); dfree(ctx->counters); dfree(ctx->out_start); dfree(ctx->out_end);
+    dfree(ctx->words); dfree(ctx->counters); dfree(ctx->bbox); dfree(ctx->out_start); dfree(ctx->out_end);
     if (ctx->phase_timing)
         for (int i = 0; i < 64; ++i)
             for (int j = 0; j < 4; ++j) cudaEventDestroy(ctx->ph_ev[i][j]);
@@ -253,7 +272,7 @@ extern "C" lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out
     if (st != LAG_OK) return st;
     ctx->stride = stride;
     ctx->n_seeds = n;
-    ctx->n_tiles = (int)((n + kTile - 1) / kTile);
+    ctx->n_tiles = (int)brick_tiles(ctx->ns, ctx->brick[0], ctx->brick[1]);
     if (ctx->cfg.mode == LAG_COMM) {
         // tail tiles past the seeds are empty; n_tiles lives on the device (appends)
         CK(cudaMemsetAsync(ctx->tile_count, 0, (size_t)ctx->cap_tiles, ctx->stream));
@@ -261,14 +280,30 @@ extern "C" lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out
         if (st != LAG_OK) return st;
     }
     SeedArgs sa{};
-    sa.state = ctx->state; sa.tile_count = ctx->tile_count; sa.n = n; sa.stride = stride;
+    sa.state = ctx->state; sa.tile_count = ctx->tile_count; sa.n_tiles = ctx->n_tiles; sa.stride = stride;
     sa.n_tiles_word = ctx->cfg.mode == LAG_COMM ? ctx->words + W_NTILES : nullptr;
     for (int a = 0; a < 3; ++a) { sa.first[a] = ctx->first[a]; sa.ns[a] = ctx->ns[a]; }
-    sa.bx = ctx->bits[0]; sa.by = ctx->bits[1];
+    sa.by = ctx->brick[0]; sa.bz = ctx->brick[1];
+    sa.bx = ctx->bits[0]; sa.by_bits = ctx->bits[1];
     const int64_t total = (int64_t)ctx->n_tiles * kTile;
     seed_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(sa);
     ++ctx->launches;
     CK(cudaGetLastError());
+    // experiment (LAG_BRICK=1): stride-1 3-D intervals advect brick by brick
+    // with the velocity box staged in shared memory (lag_brick.cuh; slower
+    // than advect_kernel on B200); the seeds' cell boxes start it
+    {
+        const char* eb = getenv("LAG_BRICK");
+        ctx->use_brick = D == 3 && stride == 1 && eb && eb[0] == '1';
+    }
+    if (ctx->use_brick) {
+        BBoxInitArgs ba{};
+        ba.bbox = ctx->bbox; ba.n_bricks = ctx->n_tiles / kBrickTiles; ba.stride = stride;
+        for (int a = 0; a < 3; ++a) { ba.first[a] = ctx->first[a]; ba.ns[a] = ctx->ns[a]; }
+        brick_bbox_kernel<<<(unsigned)((ba.n_bricks + 127) / 128), 128, 0, ctx->stream>>>(ba);
+        ++ctx->launches;
+        CK(cudaGetLastError());
+    }
     ctx->seeded = true;
     ctx->cycles_in_interval = 0;
     ctx->active_host = n;
@@ -395,7 +430,18 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
 #endif
     if (blocks < 1) blocks = 1;
     const bool bto = ctx->cfg.mode == LAG_BTO;
-    if (D == 3) {
+    if (ctx->use_brick && !a.frozen) {
+        BrickArgs b{};
+        b.a = a;
+        b.bbox = ctx->bbox;
+        b.n_seed_bricks = ctx->n_tiles / kBrickTiles;
+        b.slice_bytes = ctx->slice_floats * (int64_t)sizeof(float);
+        // persistent: one CTA per SM (two box buffers fill its shared memory)
+        const int bricks = (tiles + kBrickTiles - 1) / kBrickTiles;
+        const unsigned grid = (unsigned)std::max(1, std::min(bricks, ctx->num_sms));
+        if (bto) advect_brick_kernel<true><<<grid, kBrickThreads, 4 * kBoxBytes, ctx->stream>>>(b);
+        else advect_brick_kernel<false><<<grid, kBrickThreads, 4 * kBoxBytes, ctx->stream>>>(b);
+    } else if (D == 3) {
         if (a.frozen) {
             if (bto) advect_kernel<3, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
             else advect_kernel<3, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a);

@@ -2,6 +2,7 @@
 #pragma once
 #include "lag.h"
 #include "lag_kernels.cuh"
+#include "lag_brick.cuh"
 
 #include <cuda_runtime.h>
 #include <string>
@@ -26,6 +27,9 @@ struct lag_ctx_s {
     int64_t max_seeds = 0, cap = 0;
     int cap_tiles = 0;
     int n_tiles = 0;                 // tiles holding seeds
+    int brick[2] = {1, 1};           // seed brick rows (y, z) of 32-seed tiles
+    int32_t* bbox = nullptr;         // stride-1 3-D: cell box per seed brick (advect_brick_kernel)
+    bool use_brick = false;          // this interval advects with advect_brick_kernel
     int64_t n_seeds = 0, active_host = 0;
     int first[3] = {0, 0, 0}, ns[3] = {1, 1, 1};
     int stride = 1;

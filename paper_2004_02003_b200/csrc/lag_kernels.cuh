@@ -34,6 +34,9 @@ constexpr int kTilesPerWarp = LAG_ADV_TPW;    // contiguous 32-particle tiles pe
 #ifndef LAG_ADV_PERSIST
 #define LAG_ADV_PERSIST 1
 #endif
+#ifndef LAG_PREFETCH
+#define LAG_PREFETCH 0   // 1: L2, 2: L1 prefetch of the next tile's stage-1 corner rows
+#endif
 #ifndef LAG_POLY
 #define LAG_POLY 0       // 1: polynomial-form trilinear (coefficients per corner set)
 #endif
@@ -326,6 +329,42 @@ __device__ __forceinline__ uint8_t classify_slow_v(const AdvectArgs& a, int v[3]
     return st;
 }
 
+// Stage sample s >= 2 relative to the stage-1 cell: fs = f1 + beta dt k (cell
+// units from the stage-1 cell origin).  fs in [0, 1) on every axis (one
+// unsigned compare of the float bits per axis: negatives have the sign bit)
+// means the stage-1 cell, which the committed position already validated, so
+// nothing else is tested.  Otherwise the sample's cell v1 + floor(fs) takes
+// the fast-range test and, outside it, the full classification.  Returns the
+// node index of the cell to interpolate in (f = fractions inside it).
+template <int DIM, bool BTO>
+__device__ __forceinline__ int stage_cell(const AdvectArgs& a, const int v1[3], int idx1,
+                                          const float fs[3], bool test, uint8_t& st,
+                                          bool& ghost_bad, float f[3]) {
+    bool same = true;
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) {
+        f[ax] = fs[ax];
+        same &= __float_as_uint(fs[ax]) < 0x3F800000u;
+    }
+    if constexpr (DIM == 2) f[2] = 0.f;
+    int idx = idx1;
+    if (!same && test) {
+        int v[3];
+        bool ok = true;
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax) {
+            const float fl = floorf(fs[ax]);
+            f[ax] = fs[ax] - fl;                                   // exact
+            v[ax] = v1[ax] + (__float_as_int(fl + 12582912.0f) - 0x4B400000);
+            ok &= (unsigned)v[ax] <= (unsigned)a.gspan[ax];
+        }
+        if constexpr (DIM == 2) v[2] = 0;
+        if (!ok) st = classify_slow_v<DIM, BTO>(a, v, f, ghost_bad);
+        idx = vindex<DIM>(a, v);
+    }
+    return idx;
+}
+
 template <int DIM>
 __device__ __forceinline__ int node_index(const AdvectArgs& a, const int c[3]) {
     const int lx = c[0] - a.base[0], ly = c[1] - a.base[1];
@@ -521,6 +560,9 @@ advect_kernel(const AdvectArgs a) {
         int cur = vindex<DIM>(a, c);
         LAG_CHECK_GATHER(a, cur, live);
         if (!live) cur = 0;
+        const int idx1 = cur;                 // stage-1 cell: offsets, fractions
+        const int v1c[3] = {c[0], c[1], c[2]};
+        const float f1[3] = {f[0], f[1], f[2]};
         gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
         if constexpr (FROZEN) {
 #pragma unroll
@@ -535,11 +577,9 @@ advect_kernel(const AdvectArgs a) {
 
         // ---- stage 2: q2 = x + dt/2 k1, alpha = 1/2 ----
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], k1[ax], d[ax]);
-        if (!cells_b<DIM>(gb, e, a.gspan, c, f) && live)
-            st = classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);
+        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], k1[ax], f1[ax]);
         {
-            const int idx = vindex<DIM>(a, c);
+            const int idx = stage_cell<DIM, BTO>(a, v1c, idx1, e, live, st, ghost_bad, f);
             LAG_CHECK_GATHER(a, idx, live && st == ST_VALID);
 #ifdef LAG_EXP_NORELOAD
             if (false) {
@@ -560,14 +600,43 @@ advect_kernel(const AdvectArgs a) {
         }
         float T2[3];
         interp_pairs<DIM>(S, f, T2);                          // T2 = 2 k2
+#if LAG_PREFETCH
+        // the next tile's stage-1 corner rows (its record arrived by now): one
+        // prefetch per row and slice, so its gathers hit the cache
+        if (ntile < n_tiles && lane < ncnt) {
+            int gn[3];
+            unpack_g(__float_as_uint(nr.w), a, gn);
+            const float dn0[3] = {nr.x, nr.y, DIM == 3 ? nr.z : 0.f};
+            int vn[3];
+            bool okn = true;
+#pragma unroll
+            for (int ax = 0; ax < DIM; ++ax) {
+                vn[ax] = gn[ax] - a.gmin[ax] + (__float_as_int(floorf(dn0[ax]) + 12582912.0f) - kMagicBits);
+                okn &= (unsigned)vn[ax] <= (unsigned)a.gspan[ax];
+            }
+            if constexpr (DIM == 2) vn[2] = 0;
+            if (okn) {
+                const int in = vindex<DIM>(a, vn);
+#pragma unroll
+                for (int r = 0; r < (1 << (DIM - 1)); ++r) {
+                    const int o = DIM * (in + (r & 1) * a.sx + (r >> 1) * a.sxy);
+#if LAG_PREFETCH == 1
+                    asm volatile("prefetch.global.L2 [%0];" :: "l"(a.v0 + o));
+                    if constexpr (!FROZEN) asm volatile("prefetch.global.L2 [%0];" :: "l"(a.v1 + o));
+#else
+                    asm volatile("prefetch.global.L1 [%0];" :: "l"(a.v0 + o));
+                    if constexpr (!FROZEN) asm volatile("prefetch.global.L1 [%0];" :: "l"(a.v1 + o));
+#endif
+                }
+            }
+        }
+#endif
 
         // ---- stage 3: q3 = x + dt/2 k2 = x + dt/4 T2, alpha = 1/2 ----
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.qdth[ax], T2[ax], d[ax]);
-        if (!cells_b<DIM>(gb, e, a.gspan, c, f) && live && st == ST_VALID)
-            st = classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);
+        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.qdth[ax], T2[ax], f1[ax]);
         {
-            const int idx = vindex<DIM>(a, c);
+            const int idx = stage_cell<DIM, BTO>(a, v1c, idx1, e, live && st == ST_VALID, st, ghost_bad, f);
             LAG_CHECK_GATHER(a, idx, live && st == ST_VALID);
 #ifdef LAG_EXP_NORELOAD
             if (false) {
@@ -591,11 +660,9 @@ advect_kernel(const AdvectArgs a) {
 
         // ---- stage 4: q4 = x + dt k3 = x + dt/2 T3, alpha = 1 ----
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], T3[ax], d[ax]);
-        if (!cells_b<DIM>(gb, e, a.gspan, c, f) && live && st == ST_VALID)
-            st = classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);
+        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], T3[ax], f1[ax]);
         {
-            const int idx = vindex<DIM>(a, c);
+            const int idx = stage_cell<DIM, BTO>(a, v1c, idx1, e, live && st == ST_VALID, st, ghost_bad, f);
             LAG_CHECK_GATHER(a, idx, live && st == ST_VALID);
 #ifndef LAG_EXP_NORELOAD
             if (live && st == ST_VALID && idx != cur) {
@@ -735,37 +802,65 @@ advect_kernel(const AdvectArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// seeding: lattice nodes g = first + stride * (ix, iy, iz), x fastest
+// seeding: lattice nodes g = first + stride * (ix, iy, iz).
+// Tile order: bricks of (32 x by x bz) seeds, x fastest inside a tile, tiles
+// of a brick consecutive (rows ry fastest, then rz), bricks x-fastest.  A CTA
+// of by*bz warps then advects one brick at a time, so the node rows its
+// corner gathers share stay in that SM's L1 (a row of nodes serves the
+// particle rows on both sides of it).  Tiles past a ragged edge are partial
+// or empty (count 0).  by = bz = 1 is plain x-fastest row order.
+#ifndef LAG_BRICK_Y
+#define LAG_BRICK_Y 1
+#endif
+#ifndef LAG_BRICK_Z
+#define LAG_BRICK_Z 1
+#endif
 struct SeedArgs {
     float4* state;
     uint8_t* tile_count;
     uint32_t* n_tiles_word;         // COMM: device-side tile count to initialise (or nullptr)
-    int64_t n;
+    int64_t n_tiles;                // tiles of the brick layout (>= ceil(n / 32))
     int32_t first[3], stride, ns[3];
-    uint32_t bx, by;
+    int32_t by, bz;                 // brick rows (y, z) of 32-seed tiles
+    uint32_t bx, by_bits;
 };
+
+// tile t -> seed lattice coordinates of its lane 0 (ix0, iy, iz)
+__host__ __device__ inline void brick_tile(int64_t t, const int32_t ns[3], int by, int bz,
+                                           int64_t& ix0, int64_t& iy, int64_t& iz) {
+    const int64_t tb = (int64_t)by * bz;
+    const int64_t brick = t / tb, j = t % tb;
+    const int64_t nbx = (ns[0] + kTile - 1) / kTile, nby = (ns[1] + by - 1) / by;
+    ix0 = (brick % nbx) * kTile;
+    const int64_t r = brick / nbx;
+    iy = (r % nby) * by + j % by;
+    iz = (r / nby) * bz + j / by;
+}
+
+__host__ __device__ inline int64_t brick_tiles(const int32_t ns[3], int by, int bz) {
+    const int64_t nbx = (ns[0] + kTile - 1) / kTile, nby = (ns[1] + by - 1) / by, nbz = (ns[2] + bz - 1) / bz;
+    return nbx * nby * nbz * by * bz;
+}
 
 static __global__ void seed_kernel(const SeedArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t n_tiles = (a.n + kTile - 1) / kTile;
-    if (i == 0 && a.n_tiles_word) *a.n_tiles_word = (uint32_t)n_tiles;
-    if (i < n_tiles * kTile) {
-        if (i < a.n) {
-            const int64_t ix = i % a.ns[0];
-            const int64_t t = i / a.ns[0];
-            const int64_t iy = t % a.ns[1];
-            const int64_t iz = t / a.ns[1];
-            const uint32_t gx = (uint32_t)(a.first[0] + a.stride * ix);
-            const uint32_t gy = (uint32_t)(a.first[1] + a.stride * iy);
-            const uint32_t gz = (uint32_t)(a.first[2] + a.stride * iz);
-            const uint32_t w = gx | (gy << a.bx) | (gz << (a.bx + a.by));
-            a.state[i] = make_float4(0.f, 0.f, 0.f, __uint_as_float(w));
-        }
-        if ((i % kTile) == 0) {
-            const int64_t rem = a.n - i;
-            a.tile_count[i / kTile] = (uint8_t)(rem >= kTile ? kTile : rem);
-        }
+    if (i == 0 && a.n_tiles_word) *a.n_tiles_word = (uint32_t)a.n_tiles;
+    if (i >= a.n_tiles * kTile) return;
+    const int64_t t = i / kTile;
+    const int lane = (int)(i % kTile);
+    int64_t ix0, iy, iz;
+    brick_tile(t, a.ns, a.by, a.bz, ix0, iy, iz);
+    const bool row = iy < a.ns[1] && iz < a.ns[2];
+    const int64_t cnt = row ? (a.ns[0] - ix0 < kTile ? a.ns[0] - ix0 : kTile) : 0;
+    if (lane < cnt) {
+        const int64_t ix = ix0 + lane;
+        const uint32_t gx = (uint32_t)(a.first[0] + a.stride * ix);
+        const uint32_t gy = (uint32_t)(a.first[1] + a.stride * iy);
+        const uint32_t gz = (uint32_t)(a.first[2] + a.stride * iz);
+        const uint32_t w = gx | (gy << a.bx) | (gz << (a.bx + a.by_bits));
+        a.state[i] = make_float4(0.f, 0.f, 0.f, __uint_as_float(w));
     }
+    if (lane == 0) a.tile_count[t] = (uint8_t)cnt;
 }
 
 // ---------------------------------------------------------------------------
