@@ -89,6 +89,10 @@ typedef enum {
 
 /* lag_extract flags */
 #define LAG_NO_RESEED 1u    /* do not reseed after extracting */
+#define LAG_ASYNC     2u    /* do not synchronise: outputs must be device pointers of the
+                               ctx's device (or NULL), complete when ctx->stream passes
+                               this call's work; latched errors are reported by the next
+                               synchronous lag_extract (or seen in lag_stats) */
 
 typedef struct {
     int32_t dim;                 /* 2 or 3                                                */
@@ -173,9 +177,13 @@ LAG_API lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, double d
  * status may be NULL (skipped); each may be a host or device pointer with
  * room for `capacity` entries.  Synchronises the stream and reports latched
  * asynchronous errors (LAG_EOVERFLOW, LAG_EGHOST, LAG_ENONFINITE) after
- * writing the outputs.  Then reseeds with the same stride unless
- * flags & LAG_NO_RESEED.
- * Errors: LAG_ESTATE (no lag_seed), LAG_EINVAL (capacity < n).
+ * writing the outputs; a reported error is cleared.  Then reseeds with the
+ * same stride unless flags & LAG_NO_RESEED.  With flags & LAG_ASYNC the call
+ * only enqueues (no host synchronisation, for a simulation that must not
+ * stall on the write cycle): BTO only needs device outputs; errors stay
+ * latched across the reseed until a synchronous lag_extract reports them.
+ * Errors: LAG_ESTATE (no lag_seed), LAG_EINVAL (capacity < n; LAG_ASYNC with
+ * a host output pointer).
  */
 LAG_API lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8_t* status,
                        int64_t capacity, int64_t* n_out, uint32_t flags);

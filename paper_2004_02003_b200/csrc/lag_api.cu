@@ -201,6 +201,11 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<2, true, false> : advect_kernel<2, false, false>, kThreads, 0);
     ctx->advect_blocks_per_sm = occ > 0 ? occ : 1;
     if (D == 3) {
+        int occ2 = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, cfg->mode == LAG_BTO ? advect2_kernel<true> : advect2_kernel<false>, kThreads, 0);
+        ctx->advect2_blocks_per_sm = occ2 > 0 ? occ2 : 1;
+        const char* e2 = getenv("LAG_ADV2");
+        ctx->use_adv2 = e2 && e2[0] == '1';
         cudaFuncSetAttribute(advect_brick_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBoxBytes);
         cudaFuncSetAttribute(advect_brick_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBoxBytes);
     }
@@ -237,8 +242,11 @@ extern "C" lag_status lag_destroy(lag_ctx ctx) {
 // ---------------------------------------------------------------------------
 
 lag_status lag_reset_interval(lag_ctx_s* ctx) {
-    // device words: [W_DEAD] dead count, [W_ERR] error bits, [W_NTILES] tile count (COMM)
-    CK(cudaMemsetAsync(ctx->words, 0, kWords * sizeof(uint32_t), ctx->stream));
+    // device words: [W_DEAD] dead count, [W_ERR] error bits, [W_NTILES] tile count (COMM);
+    // error bits stay latched until a synchronous lag_extract reports them
+    static_assert(W_DEAD == 0 && W_ERR == 1, "word layout");
+    CK(cudaMemsetAsync(ctx->words + W_DEAD, 0, sizeof(uint32_t), ctx->stream));
+    CK(cudaMemsetAsync(ctx->words + W_ERR + 1, 0, (kWords - W_ERR - 1) * sizeof(uint32_t), ctx->stream));
     CK(cudaMemsetAsync(ctx->counters + CNT_TERM, 0, 4 * sizeof(unsigned long long), ctx->stream));
     return LAG_OK;
 }
@@ -441,6 +449,12 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
         const unsigned grid = (unsigned)std::max(1, std::min(bricks, ctx->num_sms));
         if (bto) advect_brick_kernel<true><<<grid, kBrickThreads, 4 * kBoxBytes, ctx->stream>>>(b);
         else advect_brick_kernel<false><<<grid, kBrickThreads, 4 * kBoxBytes, ctx->stream>>>(b);
+    } else if (D == 3 && ctx->use_adv2 && !a.frozen) {
+        const int groups = (tiles + kNpt - 1) / kNpt;
+        int nb = (groups + warps_per_block - 1) / warps_per_block;
+        nb = std::max(1, std::min(nb, ctx->num_sms * ctx->advect2_blocks_per_sm));
+        if (bto) advect2_kernel<true><<<nb, kThreads, 0, ctx->stream>>>(a);
+        else advect2_kernel<false><<<nb, kThreads, 0, ctx->stream>>>(a);
     } else if (D == 3) {
         if (a.frozen) {
             if (bto) advect_kernel<3, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
@@ -542,6 +556,13 @@ extern "C" lag_status lag_extract_ex(lag_ctx ctx, double* start, double* end, ui
     e.end = out_target(ctx, end, ctx->out_end);
     e.status = out_target(ctx, status, ctx->out_status);
     e.term_cycle = term_cycle ? out_target(ctx, term_cycle, ctx->out_cycle) : nullptr;
+    const bool async = (flags & LAG_ASYNC) != 0;
+    if (async && ((start && (void*)e.start != (void*)start) || (end && (void*)e.end != (void*)end) ||
+                  (status && (void*)e.status != (void*)status) ||
+                  (term_cycle && (void*)e.term_cycle != (void*)term_cycle))) {
+        lag_set_error(ctx, "LAG_ASYNC needs device output pointers on device %d", ctx->cfg.device);
+        return LAG_EINVAL;
+    }
     const unsigned nb_seed = (unsigned)((ctx->n_seeds + 255) / 256);
     extract_start_kernel<<<nb_seed, 256, 0, ctx->stream>>>(e);
     ++ctx->launches;
@@ -559,10 +580,15 @@ extern "C" lag_status lag_extract_ex(lag_ctx ctx, double* start, double* end, ui
     if ((st = copy_out(ctx, end, e.end, n * D * sizeof(double))) != LAG_OK) return st;
     if ((st = copy_out(ctx, status, e.status, n)) != LAG_OK) return st;
     if ((st = copy_out(ctx, term_cycle, e.term_cycle, n * sizeof(int32_t))) != LAG_OK) return st;
-    CK(cudaMemcpyAsync(&ctx->host_words[0], ctx->words, kWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));      // the only host sync of the write cycle
+    lag_status err = LAG_OK;
+    if (!async) {
+        CK(cudaMemcpyAsync(&ctx->host_words[0], ctx->words, kWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));  // the only host sync of the write cycle
+        err = latched(ctx, ctx->host_words[W_ERR]);
+        if (ctx->host_words[W_ERR])              // reported: clear the latch
+            CK(cudaMemsetAsync(ctx->words + W_ERR, 0, sizeof(uint32_t), ctx->stream));
+    }
     if (n_out) *n_out = ctx->n_seeds;
-    const lag_status err = latched(ctx, ctx->host_words[W_ERR]);
     if (!(flags & LAG_NO_RESEED)) {
         st = lag_seed(ctx, ctx->stride, nullptr);
         if (st != LAG_OK) return st;

@@ -3,6 +3,7 @@
 #include "lag.h"
 #include "lag_kernels.cuh"
 #include "lag_brick.cuh"
+#include "lag_advect2.cuh"
 
 #include <cuda_runtime.h>
 #include <string>
@@ -23,6 +24,8 @@ struct lag_ctx_s {
     int64_t slice_floats = 0;
     int num_sms = 148;
     int advect_blocks_per_sm = 1;
+    int advect2_blocks_per_sm = 1;
+    bool use_adv2 = false;           // 3-D two-slice cycles advect with advect2_kernel
     // particles
     int64_t max_seeds = 0, cap = 0;
     int cap_tiles = 0;

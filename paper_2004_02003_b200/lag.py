@@ -22,6 +22,7 @@ LAG_BTO, LAG_COMM = 0, 1
 LAG_XCHG_NCCL, LAG_XCHG_PEER = 0, 1
 LAG_VALID, LAG_TERM_BOUNDARY, LAG_EXIT_DOMAIN = 0, 1, 2
 LAG_NO_RESEED = 1
+LAG_ASYNC = 2
 STATUS_NAMES = {0: "LAG_OK", -1: "LAG_EINVAL", -2: "LAG_ESTATE", -3: "LAG_EEMPTY",
                 -4: "LAG_ENOMEM", -5: "LAG_ECUDA", -6: "LAG_ENCCL", -7: "LAG_EOVERFLOW",
                 -8: "LAG_EGHOST", -9: "LAG_ENONFINITE"}

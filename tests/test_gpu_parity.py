@@ -324,3 +324,39 @@ def test_brick_kernel_opt_in(case, monkeypatch):
         cfg = L.make_config("C2", scale=29)
         b = L.Block(0, (0, 0, 0), (3, 2, 5), (26, 23, 19))
         _run_config(cfg, 8, stride=1, blocks=[b])
+
+
+def test_async_extract_matches_sync_and_keeps_errors_latched():
+    """LAG_ASYNC enqueues the write cycle without a host sync: same bits as the
+    synchronous extract; a latched device error survives the asynchronous
+    write cycle and its reseed and is reported by the next synchronous one;
+    host outputs are refused."""
+    import torch
+    import paper_2004_02003_b200 as P
+    cfg = L.make_config("C2", scale=21)
+    sl = global_slices(cfg, 4)
+    b = L.decompose(cfg["grid"], cfg["layout"])[0]
+    ref = gpu_block(cfg, b, sl, 1)
+    got = gpu_block(cfg, b, sl, 1, extract_flags=P.LAG_ASYNC)
+    for x, y in zip(ref[:3], got[:3]):
+        assert np.array_equal(x, y)
+
+    g = L.Grid(3, (8, 8, 8), (0, 0, 0), (1, 1, 1))
+    ctx = P.Context(P.make_config(3, g.nodes, g.origin, g.spacing, (0, 0, 0), g.nodes))
+    n = ctx.seed(1)
+    bad = torch.zeros((8, 8, 8, 3), device="cuda")
+    bad[4, 4, 4, 0] = float("nan")
+    good = torch.zeros_like(bad)
+    end = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    with pytest.raises(P.LagError) as e:
+        ctx.extract(end=torch.empty((n, 3), dtype=torch.float64).pin_memory(), flags=P.LAG_ASYNC)
+    assert e.value.status == P.LAG_EINVAL
+    ctx.advect(bad, bad, 0.1)
+    ctx.extract(end=end, flags=P.LAG_ASYNC)                  # enqueued, reseeded, error kept
+    ctx.advect(good, good, 0.1)
+    with pytest.raises(P.LagError) as e:
+        ctx.extract(end=end)
+    assert e.value.status == P.LAG_ENONFINITE
+    ctx.advect(good, good, 0.1)                              # reported -> cleared
+    assert ctx.extract(end=end) == n
+    ctx.close()
