@@ -59,12 +59,6 @@ static lag_status dmalloc(lag_ctx_s* ctx, T** p, size_t count) {
 
 static void dfree(void* p) { if (p) cudaFree(p); }
 
-// dynamic shared memory of advect_kernel: the stage-1 corner pipeline buffer
-static size_t adv_smem_bytes(int dim) {
-    if (!LAG_SMEM_PIPE) return 0;
-    return (size_t)(kThreads / 32) * 32 * sizeof(float) * (dim == 3 ? PipeF<3>::n : PipeF<2>::n);
-}
-
 // ---------------------------------------------------------------------------
 
 extern "C" int32_t lag_abi_version(void) { return LAG_ABI_VERSION; }
@@ -202,9 +196,9 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     // occupancy-sized persistent grid for the advect kernel
     int occ = 1;
     if (D == 3)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<3, true, false> : advect_kernel<3, false, false>, kThreads, adv_smem_bytes(3));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<3, true, false> : advect_kernel<3, false, false>, kThreads, 0);
     else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<2, true, false> : advect_kernel<2, false, false>, kThreads, adv_smem_bytes(2));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<2, true, false> : advect_kernel<2, false, false>, kThreads, 0);
     ctx->advect_blocks_per_sm = occ > 0 ? occ : 1;
     if (D == 3) {
         int occ2 = 1;
@@ -463,19 +457,19 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
         else advect2_kernel<false><<<nb, kThreads, 0, ctx->stream>>>(a);
     } else if (D == 3) {
         if (a.frozen) {
-            if (bto) advect_kernel<3, true, true><<<blocks, kThreads, adv_smem_bytes(3), ctx->stream>>>(a);
-            else advect_kernel<3, false, true><<<blocks, kThreads, adv_smem_bytes(3), ctx->stream>>>(a);
+            if (bto) advect_kernel<3, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
+            else advect_kernel<3, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
         } else {
-            if (bto) advect_kernel<3, true, false><<<blocks, kThreads, adv_smem_bytes(3), ctx->stream>>>(a);
-            else advect_kernel<3, false, false><<<blocks, kThreads, adv_smem_bytes(3), ctx->stream>>>(a);
+            if (bto) advect_kernel<3, true, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
+            else advect_kernel<3, false, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
         }
     } else {
         if (a.frozen) {
-            if (bto) advect_kernel<2, true, true><<<blocks, kThreads, adv_smem_bytes(2), ctx->stream>>>(a);
-            else advect_kernel<2, false, true><<<blocks, kThreads, adv_smem_bytes(2), ctx->stream>>>(a);
+            if (bto) advect_kernel<2, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
+            else advect_kernel<2, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
         } else {
-            if (bto) advect_kernel<2, true, false><<<blocks, kThreads, adv_smem_bytes(2), ctx->stream>>>(a);
-            else advect_kernel<2, false, false><<<blocks, kThreads, adv_smem_bytes(2), ctx->stream>>>(a);
+            if (bto) advect_kernel<2, true, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
+            else advect_kernel<2, false, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
         }
     }
     ++ctx->launches;

@@ -497,65 +497,6 @@ __device__ __forceinline__ void gather_idx(const float* __restrict__ v, int idx,
     }
 }
 
-// ---------------------------------------------------------------------------
-// Stage-1 corner pipeline (LAG_SMEM_PIPE): while a warp advects tile k, the
-// stage-1 corners of tile k+1 travel global -> shared memory with cp.async
-// (no registers held); tile k+1 then reads them with conflict-free LDS.
-// Buffer per warp: [slice][row][2*DIM floats][32 lanes]; every lane writes
-// and reads only its own column, so no warp synchronisation is needed.
-#ifndef LAG_SMEM_PIPE
-#define LAG_SMEM_PIPE 0
-#endif
-template <int DIM> struct PipeF { static constexpr int n = 2 * (1 << (DIM - 1)) * 2 * DIM; };   // floats per lane
-
-template <int DIM, bool BTO>
-__device__ __forceinline__ int stage1_index(const AdvectArgs& a, float4 r, bool live) {
-    int g[3];
-    unpack_g(__float_as_uint(r.w), a, g);
-    const float d[3] = {r.x, r.y, DIM == 3 ? r.z : 0.f};
-    int gb[3], c[3];
-    float f[3];
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) gb[ax] = g[ax] - a.gmin[ax] - kMagicBits;
-    bool gdummy = false;
-    if (!cells_b<DIM>(gb, d, a.gspan, c, f) && live) classify_slow_v<DIM, BTO>(a, c, f, gdummy);
-    return live ? vindex<DIM>(a, c) : 0;
-}
-
-template <int DIM, bool FROZEN>
-__device__ __forceinline__ void pipe_issue(const AdvectArgs& a, int idx, float* wbuf, int lane) {
-    constexpr int R = 1 << (DIM - 1), W = 2 * DIM;
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(wbuf) + 4u * lane;
-#pragma unroll
-    for (int sl = 0; sl < (FROZEN ? 1 : 2); ++sl) {
-        const float* p = (sl ? a.v1 : a.v0) + DIM * idx;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const float* q = p + DIM * ((r & 1) * a.sx + (r >> 1) * a.sxy);
-#pragma unroll
-            for (int k = 0; k < W; ++k)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;"
-                             :: "r"(sb + 128u * (uint32_t)((sl * R + r) * W + k)), "l"(q + k) : "memory");
-        }
-    }
-}
-
-__device__ __forceinline__ void pipe_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void pipe_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-template <int DIM>
-__device__ __forceinline__ void pipe_read(const float* wbuf, int lane, int sl, f2_t* P) {
-    constexpr int R = 1 << (DIM - 1), W = 2 * DIM;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        float e[W];
-#pragma unroll
-        for (int k = 0; k < W; ++k) e[k] = wbuf[((sl * R + r) * W + k) * 32 + lane];
-#pragma unroll
-        for (int c = 0; c < DIM; ++c) P[r * DIM + c] = f2_pack(e[c], e[DIM + c]);
-    }
-}
-
 template <int DIM, bool BTO, bool FROZEN>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 advect_kernel(const AdvectArgs a) {
@@ -590,26 +531,13 @@ advect_kernel(const AdvectArgs a) {
     int tile = tile0;
     int cnt = tile < n_tiles ? a.tile_count[tile] : 0;
     float4 r = tile < n_tiles ? a.state[(size_t)tile * kTile + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-#if LAG_SMEM_PIPE
-    extern __shared__ float pipe_smem[];
-    float* wbuf = pipe_smem + (threadIdx.x >> 5) * PipeF<DIM>::n * 32;
-    if (tile < n_tiles && lane < cnt) pipe_issue<DIM, FROZEN>(a, stage1_index<DIM, BTO>(a, r, true), wbuf, lane);
-    pipe_commit();
-#endif
 
     while (tile < n_tiles) {
         const int ntile = tile + tstride;
         const int ncnt = ntile < n_tiles ? a.tile_count[ntile] : 0;
         const float4 nr = ntile < n_tiles ? a.state[(size_t)ntile * kTile + lane]
                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (cnt == 0) {
-#if LAG_SMEM_PIPE
-            pipe_wait();
-            if (ntile < n_tiles && lane < ncnt) pipe_issue<DIM, FROZEN>(a, stage1_index<DIM, BTO>(a, nr, true), wbuf, lane);
-            pipe_commit();
-#endif
-            tile = ntile; cnt = ncnt; r = nr; continue;
-        }
+        if (cnt == 0) { tile = ntile; cnt = ncnt; r = nr; continue; }
         const bool live = lane < cnt;
         float4* trec = a.state + (size_t)tile * kTile;
         int g[3];
@@ -635,16 +563,6 @@ advect_kernel(const AdvectArgs a) {
         const int idx1 = cur;                 // stage-1 cell: offsets, fractions
         const int v1c[3] = {c[0], c[1], c[2]};
         const float f1[3] = {f[0], f[1], f[2]};
-#if LAG_SMEM_PIPE
-        pipe_wait();
-        pipe_read<DIM>(wbuf, lane, 0, S);
-        if constexpr (FROZEN) {
-#pragma unroll
-            for (int i = 0; i < NP; ++i) B[i] = S[i];
-        } else {
-            pipe_read<DIM>(wbuf, lane, 1, B);
-        }
-#else
         gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
         if constexpr (FROZEN) {
 #pragma unroll
@@ -652,7 +570,6 @@ advect_kernel(const AdvectArgs a) {
         } else {
             gather_pairs<DIM>(a.v1, cur, a.sx, a.sxy, B);
         }
-#endif
         float k1[3];
         interp_pairs<DIM>(S, f, k1);
 #pragma unroll
@@ -683,11 +600,6 @@ advect_kernel(const AdvectArgs a) {
         }
         float T2[3];
         interp_pairs<DIM>(S, f, T2);                          // T2 = 2 k2
-#if LAG_SMEM_PIPE
-        // the next tile's stage-1 corners (its record arrived by now) -> shared memory
-        if (ntile < n_tiles && lane < ncnt) pipe_issue<DIM, FROZEN>(a, stage1_index<DIM, BTO>(a, nr, true), wbuf, lane);
-        pipe_commit();
-#endif
 #if LAG_PREFETCH
         // the next tile's stage-1 corner rows (its record arrived by now): one
         // prefetch per row and slice, so its gathers hit the cache
