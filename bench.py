@@ -328,6 +328,79 @@ def measure_secondary(name, rank, world, steps, warmup, flush):
     return out
 
 
+def measure_c2(steps, warmup, flush):
+    """configs[1] on one GPU: C2 = ABC 128^3 as 8 blocks (2x2x2), stride 1,
+    interval 25, BTO — the 8 block contexts share the GPU, each on its own
+    stream, launched cycle by cycle.  Device time per cycle = a window from an
+    event after the L2 flush to the join of the 8 streams (max over blocks)."""
+    import torch
+    import lag_inputs as L
+    import paper_2004_02003_b200 as P
+    cfg = L.make_config("C2")
+    g = cfg["grid"]
+    blocks = L.decompose(g, cfg["layout"])
+    main_s = torch.cuda.current_stream()
+    arms = []
+    for b in blocks:
+        st = torch.cuda.Stream()
+        ext = L.block_slice_extent(g, b, 0)
+        hi = [b.lo[a] + ext[a] for a in range(3)]
+        sl = [L.field_at_nodes(cfg["field"], g, k * cfg["dt"], lo=b.lo, hi=hi, device="cuda",
+                               backend="torch").contiguous() for k in range(cfg["interval"] + 1)]
+        ctx = P.Context(P.make_config(g.dim, g.nodes, g.origin, g.spacing, b.lo, b.hi,
+                                      stream=st.cuda_stream))
+        n = ctx.seed(cfg["stride"])
+        out = [torch.empty((n, 3), dtype=torch.float64, device="cuda"), None,
+               torch.empty((n,), dtype=torch.uint8, device="cuda")]
+        out[1] = torch.empty_like(out[0])
+        arms.append((st, sl, ctx, out))
+    torch.cuda.synchronize()
+
+    def window(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(main_s)
+        for st, sl, ctx, out in arms:
+            st.wait_event(e0)
+        for i, (st, sl, ctx, out) in enumerate(arms):
+            fn(i, st, sl, ctx, out)
+        for st, *_ in arms:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            main_s.wait_event(ev)
+        e1.record(main_s)
+        return (e0, e1)
+
+    def run(nsteps):
+        wins = []
+        for _ in range(nsteps):
+            if flush is not None:
+                flush.zero_()
+            wins.append(window(lambda i, st, sl, ctx, out: ctx.seed(cfg["stride"])))
+            for c in range(cfg["interval"]):
+                if flush is not None:
+                    flush.zero_()
+                wins.append(window(lambda i, st, sl, ctx, out: ctx.advect(sl[c], sl[c + 1], cfg["dt"])))
+            wins.append(window(lambda i, st, sl, ctx, out: ctx.extract(
+                out[0], out[1], out[2], flags=P.LAG_NO_RESEED | P.LAG_ASYNC)))
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in wins)
+
+    run(warmup)
+    ps0 = sum(ctx.stats()["particle_steps"] for _, _, ctx, _ in arms)
+    ms = run(steps)
+    stats = [ctx.stats() for _, _, ctx, _ in arms]
+    if any(s["device_error"] for s in stats):
+        raise RuntimeError("latched device error in the C2 leg")
+    ps = sum(s["particle_steps"] for s in stats) - ps0
+    for _, _, ctx, _ in arms:
+        ctx.close()
+    return {"workload": "C2 (configs[1]): ABC 128^3 as 8 blocks (2x2x2) on one GPU, one context and "
+                        "stream per block, stride 1 (2097152 particles), interval 25, BTO",
+            "value": ps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps,
+            "discarded_last_interval": int(sum(s["term_boundary"] + s["exit_domain"] for s in stats)),
+            "comm": "not measured on one GPU (one NCCL rank per device); see the C5 'comm' arm at N >= 2"}
+
+
 def measured_peak():
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -482,6 +555,13 @@ def main():
         except Exception as exc:
             secondary = {"error": repr(exc)[:300]}
 
+    c2 = None
+    if world == 1 and not args.no_secondary:
+        try:
+            c2 = measure_c2(max(2, args.steps // 2), 2, flush)
+        except Exception as exc:
+            c2 = {"error": repr(exc)[:300]}
+
     e2e = None
     if not args.no_e2e:
         try:
@@ -520,6 +600,7 @@ def main():
                          "kernel_share_of_step": adv_ms / dev_ms},
             "comm": comm,
             "secondary": secondary,
+            "c2": c2,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
