@@ -563,17 +563,22 @@ extern "C" lag_status lag_extract_ex(lag_ctx ctx, double* start, double* end, ui
         lag_set_error(ctx, "LAG_ASYNC needs device output pointers on device %d", ctx->cfg.device);
         return LAG_EINVAL;
     }
+    e.write_start = ctx->cfg.mode == LAG_BTO ? 1 : 0;
     const unsigned nb_seed = (unsigned)((ctx->n_seeds + 255) / 256);
-    extract_start_kernel<<<nb_seed, 256, 0, ctx->stream>>>(e);
-    ++ctx->launches;
-    extract_live_kernel<<<(unsigned)(((int64_t)e.n_tiles * kTile + 255) / 256), 256, 0, ctx->stream>>>(e);
-    ++ctx->launches;
-    extract_dead_kernel<<<(unsigned)std::max(1, ctx->num_sms * 2), 256, 0, ctx->stream>>>(e);
-    ++ctx->launches;
-    if (e.n_ret > 0) {
-        extract_returned_kernel<<<(e.n_ret + 255) / 256, 256, 0, ctx->stream>>>(e);
-        ++ctx->launches;
+    const unsigned nb_live = (unsigned)(((int64_t)e.n_tiles * kTile + 255) / 256);
+    const unsigned nb_dead = (unsigned)std::max(1, ctx->num_sms * 2);
+    if (D == 3) {
+        if (!e.write_start) { extract_start_kernel<3><<<nb_seed, 256, 0, ctx->stream>>>(e); ++ctx->launches; }
+        extract_live_kernel<3><<<nb_live, 256, 0, ctx->stream>>>(e);
+        extract_dead_kernel<3><<<nb_dead, 256, 0, ctx->stream>>>(e);
+        if (e.n_ret > 0) { extract_returned_kernel<3><<<(e.n_ret + 255) / 256, 256, 0, ctx->stream>>>(e); ++ctx->launches; }
+    } else {
+        if (!e.write_start) { extract_start_kernel<2><<<nb_seed, 256, 0, ctx->stream>>>(e); ++ctx->launches; }
+        extract_live_kernel<2><<<nb_live, 256, 0, ctx->stream>>>(e);
+        extract_dead_kernel<2><<<nb_dead, 256, 0, ctx->stream>>>(e);
+        if (e.n_ret > 0) { extract_returned_kernel<2><<<(e.n_ret + 255) / 256, 256, 0, ctx->stream>>>(e); ++ctx->launches; }
     }
+    ctx->launches += 2;
     CK(cudaGetLastError());
     const size_t n = (size_t)ctx->n_seeds;
     if ((st = copy_out(ctx, start, e.start, n * D * sizeof(double))) != LAG_OK) return st;

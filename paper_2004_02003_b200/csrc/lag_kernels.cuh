@@ -843,18 +843,23 @@ __host__ __device__ inline int64_t brick_tiles(const int32_t ns[3], int by, int 
 }
 
 static __global__ void seed_kernel(const SeedArgs a) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // 32-bit index math: tiles * 32 < 2^31 (lag_init bounds the slice)
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0 && a.n_tiles_word) *a.n_tiles_word = (uint32_t)a.n_tiles;
-    if (i >= a.n_tiles * kTile) return;
-    const int64_t t = i / kTile;
-    const int lane = (int)(i % kTile);
-    int64_t ix0, iy, iz;
-    brick_tile(t, a.ns, a.by, a.bz, ix0, iy, iz);
+    if (i >= (int)a.n_tiles * kTile) return;
+    const int t = i >> 5, lane = i & 31;
+    const int tb = a.by * a.bz;
+    const int brick = t / tb, j = t - brick * tb;
+    const int nbx = (a.ns[0] + kTile - 1) / kTile, nby = (a.ns[1] + a.by - 1) / a.by;
+    const int bq = brick / nbx;
+    const int ix0 = (brick - bq * nbx) * kTile;
+    const int jz = j / a.by;
+    const int iy = (bq % nby) * a.by + (j - jz * a.by);
+    const int iz = (bq / nby) * a.bz + jz;
     const bool row = iy < a.ns[1] && iz < a.ns[2];
-    const int64_t cnt = row ? (a.ns[0] - ix0 < kTile ? a.ns[0] - ix0 : kTile) : 0;
+    const int cnt = row ? min(a.ns[0] - ix0, kTile) : 0;
     if (lane < cnt) {
-        const int64_t ix = ix0 + lane;
-        const uint32_t gx = (uint32_t)(a.first[0] + a.stride * ix);
+        const uint32_t gx = (uint32_t)(a.first[0] + a.stride * (ix0 + lane));
         const uint32_t gy = (uint32_t)(a.first[1] + a.stride * iy);
         const uint32_t gz = (uint32_t)(a.first[2] + a.stride * iz);
         const uint32_t w = gx | (gy << a.bx) | (gz << (a.bx + a.by_bits));
@@ -886,6 +891,7 @@ struct ExtractArgs {
     double* end;                    // [n][dim]
     uint8_t* status;                // [n]
     int32_t* term_cycle;            // [n] or nullptr: cycle of termination, -1 if valid
+    int32_t write_start;            // scatter kernels write start (BTO); else extract_start_kernel
 };
 
 __device__ __forceinline__ bool own_seed(const ExtractArgs& a, uint32_t w) {
@@ -895,25 +901,46 @@ __device__ __forceinline__ bool own_seed(const ExtractArgs& a, uint32_t w) {
     return in;
 }
 
-__device__ __forceinline__ int64_t seed_index(const ExtractArgs& a, uint32_t w, int g[3]) {
+// Seed index (x fastest) of packed seed node w; 32-bit: n < 2^31 (lag_init).
+__device__ __forceinline__ int seed_index(const ExtractArgs& a, uint32_t w, int g[3]) {
     g[0] = (int)(w & a.mx);
     g[1] = (int)((w >> a.bx) & a.my);
     g[2] = (int)(w >> (a.bx + a.by));
-    const int64_t ix = (g[0] - a.first[0]) / a.stride;
-    const int64_t iy = (g[1] - a.first[1]) / a.stride;
-    const int64_t iz = (g[2] - a.first[2]) / a.stride;
+    int ix = g[0] - a.first[0], iy = g[1] - a.first[1], iz = g[2] - a.first[2];
+    if (a.stride != 1) { ix /= a.stride; iy /= a.stride; iz /= a.stride; }
     return ix + a.ns[0] * (iy + a.ns[1] * iz);
 }
 
+// One basis flow in seed order: end = o + (g + d) h in fp64; start = o + g h
+// when the scatter kernels cover every seed (BTO: each seed is live or dead);
+// COMM writes starts with extract_start_kernel (hand-offs may be in flight
+// on another rank when a slot overflowed).
+template <int DIM>
+__device__ __forceinline__ void write_flow(const ExtractArgs& a, int s, const int g[3], const float4 r,
+                                           uint8_t status, int32_t tc) {
+    const float d[3] = {r.x, r.y, r.z};
+    const int64_t o = (int64_t)s * DIM;
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) {
+        a.end[o + ax] = a.o[ax] + ((double)g[ax] + (double)d[ax]) * a.h[ax];
+        if (a.write_start) a.start[o + ax] = a.o[ax] + (double)g[ax] * a.h[ax];
+    }
+    a.status[s] = status;
+    if (a.term_cycle) a.term_cycle[s] = tc;
+}
+
+template <int DIM>
 static __global__ void extract_start_kernel(const ExtractArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n) return;
     const int64_t idx[3] = {i % a.ns[0], (i / a.ns[0]) % a.ns[1], i / ((int64_t)a.ns[0] * a.ns[1])};
-    for (int ax = 0; ax < a.dim; ++ax)
-        a.start[i * a.dim + ax] = a.o[ax] + (double)(a.first[ax] + a.stride * idx[ax]) * a.h[ax];
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax)
+        a.start[i * DIM + ax] = a.o[ax] + (double)(a.first[ax] + a.stride * idx[ax]) * a.h[ax];
     if (a.term_cycle) a.term_cycle[i] = -1;
 }
 
+template <int DIM>
 static __global__ void extract_live_kernel(const ExtractArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t tile = i / kTile;
@@ -923,13 +950,11 @@ static __global__ void extract_live_kernel(const ExtractArgs a) {
     const float4 r = a.state[i];
     if (!own_seed(a, __float_as_uint(r.w))) return;
     int g[3];
-    const int64_t s = seed_index(a, __float_as_uint(r.w), g);
-    const float d[3] = {r.x, r.y, r.z};
-    for (int ax = 0; ax < a.dim; ++ax)
-        a.end[s * a.dim + ax] = a.o[ax] + ((double)g[ax] + (double)d[ax]) * a.h[ax];
-    a.status[s] = ST_VALID;
+    const int s = seed_index(a, __float_as_uint(r.w), g);
+    write_flow<DIM>(a, s, g, r, ST_VALID, -1);
 }
 
+template <int DIM>
 static __global__ void extract_dead_kernel(const ExtractArgs a) {
     const uint32_t n_dead = min(*a.n_dead_dev, a.dead_cap);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_dead;
@@ -937,27 +962,22 @@ static __global__ void extract_dead_kernel(const ExtractArgs a) {
         const float4 r = a.dead_rec[i];
         if (!own_seed(a, __float_as_uint(r.w))) continue;
         int g[3];
-        const int64_t s = seed_index(a, __float_as_uint(r.w), g);
-        const float d[3] = {r.x, r.y, r.z};
-        for (int ax = 0; ax < a.dim; ++ax)
-            a.end[s * a.dim + ax] = a.o[ax] + ((double)g[ax] + (double)d[ax]) * a.h[ax];
-        a.status[s] = (uint8_t)(a.dead_info[i] >> 24);
-        if (a.term_cycle) a.term_cycle[s] = (int32_t)(a.dead_info[i] & 0xffffffu);
+        const int s = seed_index(a, __float_as_uint(r.w), g);
+        const uint32_t info = a.dead_info[i];
+        write_flow<DIM>(a, s, g, r, (uint8_t)(info >> 24), (int32_t)(info & 0xffffffu));
     }
 }
 
+template <int DIM>
 static __global__ void extract_returned_kernel(const ExtractArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n_ret) return;
     const float4 r = a.ret[2 * i];
     const uint32_t info = __float_as_uint(a.ret[2 * i + 1].x);
     int g[3];
-    const int64_t s = seed_index(a, __float_as_uint(r.w), g);
-    const float d[3] = {r.x, r.y, r.z};
-    for (int ax = 0; ax < a.dim; ++ax)
-        a.end[s * a.dim + ax] = a.o[ax] + ((double)g[ax] + (double)d[ax]) * a.h[ax];
-    a.status[s] = (uint8_t)(info >> 24);
-    if (a.term_cycle && (info >> 24) != ST_VALID) a.term_cycle[s] = (int32_t)(info & 0xffffffu);
+    const int s = seed_index(a, __float_as_uint(r.w), g);
+    const uint8_t st = (uint8_t)(info >> 24);
+    write_flow<DIM>(a, s, g, r, st, st != ST_VALID ? (int32_t)(info & 0xffffffu) : -1);
 }
 
 }  // namespace lag
