@@ -41,8 +41,11 @@
  *     Element (0,0,0) is global node block_lo - ghost.
  *   - Pointers passed to lag_advect_cycle / lag_extract may be device pointers
  *     (used in place, stream-ordered on cfg.stream) or host pointers (the
- *     library stages them through device buffers with cudaMemcpyAsync; this is
- *     the end-to-end path).
+ *     library stages them through three device buffers with cudaMemcpyAsync on
+ *     its own copy stream, so the next cycle's copy overlaps this cycle's
+ *     kernels; pinned host memory makes the copy asynchronous; this is the
+ *     end-to-end path).  The previous call's host v_t1 passed again as v_t is
+ *     not copied twice, so it must not change between those two calls.
  *   - Not thread-safe per context.  Several contexts may share a device.
  */
 #ifndef LAG_H
@@ -78,7 +81,15 @@ typedef enum {
 } lag_status;
 
 typedef enum { LAG_BTO = 0, LAG_COMM = 1 } lag_mode;
-typedef enum { LAG_XCHG_NCCL = 0, LAG_XCHG_PEER = 1 } lag_exchange;
+typedef enum {
+    LAG_XCHG_NCCL = 0,          /* grouped NCCL send/recv before the advect kernel            */
+    LAG_XCHG_PEER = 1,          /* the kernels read/write the neighbours' memory (CUDA IPC)   */
+    LAG_XCHG_PEER_OVERLAP = 2   /* LAG_XCHG_PEER fused with the advection: the first CTAs of
+                                   the advect kernel run the exchange while the others
+                                   advect the tiles whose stage samples cannot reach a ghost
+                                   node; the rest (and the particles received this cycle)
+                                   advect in a second pass.  Bitwise equal to the others.  */
+} lag_exchange;
 
 /* Per-basis-flow status returned by lag_extract. */
 typedef enum {
@@ -108,9 +119,7 @@ typedef struct {
     int32_t rank;                /* COMM: this block's rank (x-fastest in layout)         */
     int32_t nranks;              /* COMM: number of ranks = prod(layout)                  */
     int32_t layout[3];           /* COMM: blocks per axis                                 */
-    int32_t exchange;            /* COMM transport: LAG_XCHG_NCCL (grouped NCCL send/recv)
-                                    or LAG_XCHG_PEER (the kernels read/write the
-                                    neighbours' memory over NVLink, CUDA IPC)             */
+    int32_t exchange;            /* COMM transport: lag_exchange                          */
     const void* nccl_id;         /* COMM: 128-byte ncclUniqueId shared by all ranks (from
                                     lag_nccl_unique_id on one rank); NULL for BTO         */
     void*   stream;              /* cudaStream_t the library enqueues on (borrowed);

@@ -5,6 +5,7 @@
 // the kernels below; host code only validates, allocates and enqueues.
 #include "lag.h"
 #include "lag_internal.h"
+#include "lag_xchg.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -18,6 +19,22 @@
 using namespace lag;
 
 static thread_local std::string g_init_error = "no error";
+
+// COMM overlap pass 1 (LAG_XCHG_PEER_OVERLAP): CTAs [0, xf.ncta) run this
+// cycle's peer exchange (pack + signal, wait + ghost pull + append of the
+// previous cycle's hand-offs, lag_xchg.cuh) while the other CTAs advect the
+// tiles whose stage samples cannot reach a ghost node (a.pass = 1).  The grid
+// is the resident capacity, so the exchange CTAs never wait for a slot.
+template <int DIM, bool FROZEN>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+advect_xchg_kernel(const AdvectArgs a, const XchgFused xf) {
+    if ((int)blockIdx.x < xf.ncta) {
+        xchg_pack_signal(xf.x, blockIdx.x, xf.ncta);
+        xchg_wait_pull(xf.x, xf.ap, blockIdx.x, xf.ncta);
+        return;
+    }
+    advect_body<DIM, false, FROZEN>(a, blockIdx.x - xf.ncta, gridDim.x - xf.ncta);
+}
 
 int lag_set_error(lag_ctx_s* ctx, const char* fmt, ...) {
     char buf[512];
@@ -106,7 +123,10 @@ static lag_status validate(const lag_config* c) {
         }
         if (prod != c->nranks || c->rank < 0 || c->rank >= c->nranks) { lag_set_error(ctx, "rank/nranks/layout mismatch"); return LAG_EINVAL; }
         if (c->nranks > 1 && !c->nccl_id) { lag_set_error(ctx, "COMM mode with nranks > 1 needs nccl_id"); return LAG_EINVAL; }
-        if (c->exchange != LAG_XCHG_NCCL && c->exchange != LAG_XCHG_PEER) { lag_set_error(ctx, "exchange must be LAG_XCHG_NCCL or LAG_XCHG_PEER"); return LAG_EINVAL; }
+        if (c->exchange != LAG_XCHG_NCCL && c->exchange != LAG_XCHG_PEER && c->exchange != LAG_XCHG_PEER_OVERLAP) {
+            lag_set_error(ctx, "exchange must be LAG_XCHG_NCCL, LAG_XCHG_PEER or LAG_XCHG_PEER_OVERLAP");
+            return LAG_EINVAL;
+        }
     }
     // slice extent must fit 32-bit element offsets
     int64_t nodes = 1;
@@ -192,6 +212,9 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     if (cfg->mode == LAG_COMM) {
         st = lag_comm_init(ctx);
         if (st != LAG_OK) return fail(st);
+        if (lag_comm_overlap(ctx)) {
+            if ((st = dmalloc(ctx, &ctx->defer_list, (size_t)ctx->cap_tiles)) != LAG_OK) return fail(st);
+        }
     }
     // occupancy-sized persistent grid for the advect kernel
     int occ = 1;
@@ -229,12 +252,19 @@ extern "C" lag_status lag_destroy(lag_ctx ctx) {
     cudaSetDevice(ctx->cfg.device);
     if (ctx->stream_synced_needed) cudaStreamSynchronize(ctx->stream);
     lag_comm_destroy(ctx);
+    dfree(ctx->defer_list);
     dfree(ctx->state); dfree(ctx->tile_count); dfree(ctx->dead_rec); dfree(ctx->dead_info);
     dfree(ctx->words); dfree(ctx->counters); dfree(ctx->bbox); dfree(ctx->out_start); dfree(ctx->out_end);
     if (ctx->phase_timing)
         for (int i = 0; i < 64; ++i)
             for (int j = 0; j < 4; ++j) cudaEventDestroy(ctx->ph_ev[i][j]);
-    dfree(ctx->out_status); dfree(ctx->out_cycle); dfree(ctx->stage[0]); dfree(ctx->stage[1]);
+    dfree(ctx->out_status); dfree(ctx->out_cycle);
+    for (int k = 0; k < lag_ctx_s::kStage; ++k) {
+        dfree(ctx->stage[k]);
+        if (ctx->stage_ready[k]) cudaEventDestroy(ctx->stage_ready[k]);
+        if (ctx->stage_free[k]) cudaEventDestroy(ctx->stage_free[k]);
+    }
+    if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
     delete ctx;
     return LAG_OK;
 }
@@ -322,8 +352,8 @@ extern "C" lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out
 
 // Device-resident velocity for a caller pointer: device memory is used in
 // place; host memory is copied into one of two staging buffers (end-to-end
-// path).  A host pointer already staged (the previous call's v_t1 passed as
-// this call's v_t) is reused: host slices must not change between those calls.
+// path).  Only the previous call's v_t1 passed again as v_t is reused; it must
+// not change between those two calls.
 static lag_status resolve_slice(lag_ctx_s* ctx, void* p, int avoid, float** out, int* slot_out) {
     *slot_out = -1;
     cudaPointerAttributes at{};
@@ -337,18 +367,36 @@ static lag_status resolve_slice(lag_ctx_s* ctx, void* p, int avoid, float** out,
         *out = (float*)p;
         return LAG_OK;
     }
-    for (int s = 0; s < 2; ++s)
-        if (ctx->stage[s] && ctx->stage_src[s] == p && s != avoid) {
-            *out = ctx->stage[s]; *slot_out = s;
-            return LAG_OK;
+    // only the previous call's v_t1, passed again as this call's v_t, is reused
+    // (the in situ sequence); any other host slice is copied afresh
+    if (avoid < 0 && ctx->last_v1_slot >= 0 && ctx->stage_src[ctx->last_v1_slot] == p) {
+        const int s = ctx->last_v1_slot;
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->stage_ready[s], 0));
+        *out = ctx->stage[s]; *slot_out = s;
+        return LAG_OK;
+    }
+    // least recently read buffer (never the one this call already uses); its
+    // copy waits only for that buffer's last reader, so it overlaps the
+    // kernels of the cycle in flight
+    int s = -1;
+    for (int k = 0; k < lag_ctx_s::kStage; ++k)
+        if (k != avoid && (s < 0 || ctx->stage_use[k] < ctx->stage_use[s])) s = k;
+    if (!ctx->cstream) {
+        CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+        for (int k = 0; k < lag_ctx_s::kStage; ++k) {
+            CK(cudaEventCreateWithFlags(&ctx->stage_ready[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->stage_free[k], cudaEventDisableTiming));
         }
-    const int s = avoid == 0 ? 1 : 0;
+    }
     if (!ctx->stage[s]) {
         lag_status st = dmalloc(ctx, &ctx->stage[s], (size_t)ctx->slice_floats);
         if (st != LAG_OK) return st;
     }
+    if (ctx->stage_use[s] >= 0) CK(cudaStreamWaitEvent(ctx->cstream, ctx->stage_free[s], 0));
     CK(cudaMemcpyAsync(ctx->stage[s], p, (size_t)ctx->slice_floats * sizeof(float),
-                       cudaMemcpyHostToDevice, ctx->stream));
+                       cudaMemcpyHostToDevice, ctx->cstream));
+    CK(cudaEventRecord(ctx->stage_ready[s], ctx->cstream));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->stage_ready[s], 0));
     ctx->stage_src[s] = p;
     *out = ctx->stage[s]; *slot_out = s;
     return LAG_OK;
@@ -359,6 +407,8 @@ static void fold_phases(lag_ctx_s* ctx) {
     for (int i = 0; i < ctx->ph_n; ++i) {
         float ms;
         for (int j = 0; j < 3; ++j)
+            // overlap (LAG_XCHG_PEER_OVERLAP): snapshot, pass 1 (exchange CTAs +
+            // ghost-free tiles), pass 2 + signal
             if (cudaEventElapsedTime(&ms, ctx->ph_ev[i][j], ctx->ph_ev[i][j + 1]) == cudaSuccess) ctx->ph_ms[j] += ms;
     }
     ctx->ph_n = 0;
@@ -380,11 +430,24 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
     if (ctx->phase_timing && ctx->ph_n == 64) fold_phases(ctx);
     cudaEvent_t* ev = ctx->phase_timing ? ctx->ph_ev[ctx->ph_n++] : nullptr;
     if (ev) cudaEventRecord(ev[0], ctx->stream);
-    if (ctx->cfg.mode == LAG_COMM) {
+    const bool overlap = ctx->cfg.mode == LAG_COMM && lag_comm_overlap(ctx);
+    XchgFused xf{};
+    if (overlap) {
+        // tile count before this cycle's append, empty deferral list; the
+        // exchange is not launched here: pass 1's first CTAs run it
+        CK(cudaMemcpyAsync(ctx->words + W_NTILES_B, ctx->words + W_NTILES, sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+        CK(cudaMemsetAsync(ctx->words + W_DEFER, 0, sizeof(uint32_t), ctx->stream));
+        ctx->xchg_fused = &xf;
+        st = lag_comm_pre_advect(ctx, d0, d1, v_t == ctx->last_v1);
+        ctx->xchg_fused = nullptr;
+        if (st != LAG_OK) return st;
+        xf.ncta = kXchgCtas;
+    } else if (ctx->cfg.mode == LAG_COMM) {
         st = lag_comm_pre_advect(ctx, d0, d1, v_t == ctx->last_v1);
         if (st != LAG_OK) return st;
     }
-    if (ev) cudaEventRecord(ev[1], ctx->stream);
+    if (ev && !overlap) cudaEventRecord(ev[1], ctx->stream);
     AdvectArgs a{};
     a.v0 = d0; a.v1 = d1;
     a.frozen = d0 == d1 ? 1 : 0;
@@ -424,6 +487,21 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
     a.counters = ctx->counters; a.err = ctx->words + W_ERR;
     a.cycle = ctx->cycles_in_interval;
     if (ctx->cfg.mode == LAG_COMM) lag_comm_fill_args(ctx, &a);
+    if (overlap) {
+        // ghost-free cells: a stage sample (within one cell of the stage-1 cell,
+        // CFL < 1) never needs node lo-1 (lower neighbour) or hi+1 (upper one)
+        for (int ax = 0; ax < 3; ++ax) {
+            const int N = (int)ctx->cfg.global_nodes[ax], lo = (int)ctx->cfg.block_lo[ax], hi = (int)ctx->cfg.block_hi[ax];
+            const int cmin = lo > 0 ? lo + 1 : a.gmin[ax];
+            const int cmax = hi < N ? hi - 2 : a.gmin[ax] + a.gspan[ax];
+            if (ax >= D) { a.smin[ax] = 0; a.sspan[ax] = 0; }
+            else if (cmax < cmin) { a.smin[ax] = 1 << 29; a.sspan[ax] = 0; }      // nothing ghost-free
+            else { a.smin[ax] = cmin - a.gmin[ax]; a.sspan[ax] = cmax - cmin; }
+        }
+        a.n_tiles_b = ctx->words + W_NTILES_B;
+        a.defer_list = ctx->defer_list;
+        a.defer_count = ctx->words + W_DEFER;
+    }
 
     const int tiles = ctx->cfg.mode == LAG_COMM ? ctx->cap_tiles : ctx->n_tiles;
     const int warps_per_block = kThreads / 32;
@@ -438,7 +516,46 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
 #endif
     if (blocks < 1) blocks = 1;
     const bool bto = ctx->cfg.mode == LAG_BTO;
-    if (ctx->use_brick && !a.frozen) {
+    auto launch = [&](const AdvectArgs& aa, int nb) {
+        if (D == 3) {
+            if (aa.frozen) {
+                if (bto) advect_kernel<3, true, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
+                else advect_kernel<3, false, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
+            } else {
+                if (bto) advect_kernel<3, true, false><<<nb, kThreads, 0, ctx->stream>>>(aa);
+                else advect_kernel<3, false, false><<<nb, kThreads, 0, ctx->stream>>>(aa);
+            }
+        } else {
+            if (aa.frozen) {
+                if (bto) advect_kernel<2, true, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
+                else advect_kernel<2, false, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
+            } else {
+                if (bto) advect_kernel<2, true, false><<<nb, kThreads, 0, ctx->stream>>>(aa);
+                else advect_kernel<2, false, false><<<nb, kThreads, 0, ctx->stream>>>(aa);
+            }
+        }
+    };
+    if (overlap) {
+        // pass 1: exchange CTAs + ghost-free tiles; pass 2 (stream-ordered after
+        // it): deferred tiles and this cycle's arrivals; its last warp signals
+        AdvectArgs a1 = a;
+        a1.pass = 1;
+        a1.n_sig = 0;
+        const int nb1 = std::max(blocks, kXchgCtas + 1);
+        if (ev) cudaEventRecord(ev[1], ctx->stream);
+        if (D == 3) {
+            if (a.frozen) advect_xchg_kernel<3, true><<<nb1, kThreads, 0, ctx->stream>>>(a1, xf);
+            else advect_xchg_kernel<3, false><<<nb1, kThreads, 0, ctx->stream>>>(a1, xf);
+        } else {
+            if (a.frozen) advect_xchg_kernel<2, true><<<nb1, kThreads, 0, ctx->stream>>>(a1, xf);
+            else advect_xchg_kernel<2, false><<<nb1, kThreads, 0, ctx->stream>>>(a1, xf);
+        }
+        ++ctx->launches;
+        if (ev) cudaEventRecord(ev[2], ctx->stream);
+        AdvectArgs a2 = a;
+        a2.pass = 2;
+        launch(a2, blocks);
+    } else if (ctx->use_brick && !a.frozen) {
         BrickArgs b{};
         b.a = a;
         b.bbox = ctx->bbox;
@@ -455,32 +572,24 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
         nb = std::max(1, std::min(nb, ctx->num_sms * ctx->advect2_blocks_per_sm));
         if (bto) advect2_kernel<true><<<nb, kThreads, 0, ctx->stream>>>(a);
         else advect2_kernel<false><<<nb, kThreads, 0, ctx->stream>>>(a);
-    } else if (D == 3) {
-        if (a.frozen) {
-            if (bto) advect_kernel<3, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
-            else advect_kernel<3, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
-        } else {
-            if (bto) advect_kernel<3, true, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
-            else advect_kernel<3, false, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
-        }
     } else {
-        if (a.frozen) {
-            if (bto) advect_kernel<2, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
-            else advect_kernel<2, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a);
-        } else {
-            if (bto) advect_kernel<2, true, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
-            else advect_kernel<2, false, false><<<blocks, kThreads, 0, ctx->stream>>>(a);
-        }
+        launch(a, blocks);
     }
     ++ctx->launches;
     CK(cudaGetLastError());
-    if (ev) cudaEventRecord(ev[2], ctx->stream);
+    if (ev && !overlap) cudaEventRecord(ev[2], ctx->stream);
     if (ctx->cfg.mode == LAG_COMM) {
         st = lag_comm_post_advect(ctx);
         if (st != LAG_OK) return st;
     }
     if (ev) cudaEventRecord(ev[3], ctx->stream);
+    for (int k : {s0, s1})                  // staged host slices: read up to here
+        if (k >= 0) {
+            CK(cudaEventRecord(ctx->stage_free[k], ctx->stream));
+            ctx->stage_use[k] = ctx->cycles_total;
+        }
     ctx->last_v1 = v_t1;
+    ctx->last_v1_slot = s1;
     ++ctx->cycles_in_interval;
     ++ctx->cycles_total;
     return LAG_OK;

@@ -34,7 +34,7 @@ struct AppendArgs {
 // round for a few thousand hand-offs instead of one per 256 records); each
 // CTA reads the headers and the old tile count first, and the last CTA to
 // finish resets the headers and publishes the new tile count.
-__device__ __forceinline__ void append_body(const AppendArgs& a) {
+__device__ __forceinline__ void append_body(const AppendArgs& a, int cta, int ncta) {
     __shared__ uint32_t pre[kMaxOff + 1];
     __shared__ uint32_t old_tiles, total_s;
     if (threadIdx.x == 0) {
@@ -53,21 +53,21 @@ __device__ __forceinline__ void append_body(const AppendArgs& a) {
     }
     __syncthreads();
     const uint32_t total = total_s;
-    const uint32_t nthr = gridDim.x * blockDim.x;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < total; j += nthr) {
+    const uint32_t nthr = ncta * blockDim.x;
+    for (uint32_t j = cta * blockDim.x + threadIdx.x; j < total; j += nthr) {
         int p = 0;
         while (p + 1 < a.npeers && pre[p + 1] <= j) ++p;
         a.state[(size_t)old_tiles * kTile + j] = a.recv[p][1 + (j - pre[p])];
     }
     const uint32_t new_tiles = (total + kTile - 1) / kTile;
-    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < new_tiles; t += nthr) {
+    for (uint32_t t = cta * blockDim.x + threadIdx.x; t < new_tiles; t += nthr) {
         const uint32_t rem = total - t * kTile;
         a.tile_count[old_tiles + t] = (uint8_t)(rem >= (uint32_t)kTile ? kTile : rem);
     }
     __syncthreads();                 // this CTA read every header and wrote its share
     if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(a.words + W_APPEND_DONE, 1u) == gridDim.x - 1) {      // last CTA
+        if (atomicAdd(a.words + W_APPEND_DONE, 1u) == (uint32_t)ncta - 1) {      // last CTA
             a.words[W_APPEND_DONE] = 0u;
             if (a.zero_recv) {
                 for (int p = 0; p < a.npeers; ++p) *reinterpret_cast<uint32_t*>(a.recv[p]) = 0u;
@@ -82,6 +82,6 @@ __device__ __forceinline__ void append_body(const AppendArgs& a) {
 }
 
 
-static __global__ void __launch_bounds__(256) append_kernel(AppendArgs a) { append_body(a); }
+static __global__ void __launch_bounds__(256) append_kernel(AppendArgs a) { append_body(a, blockIdx.x, gridDim.x); }
 
 }  // namespace lag

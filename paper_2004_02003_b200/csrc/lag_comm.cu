@@ -411,7 +411,7 @@ lag_status lag_comm_init(lag_ctx_s* ctx) {
     CKC(cudaMalloc(&cm->route, sizeof(RouteRec) * std::max<int64_t>(1, cm->route_cap)));
     CKC(cudaMalloc(&cm->route_recv, sizeof(RouteRec) * std::max<int64_t>(1, cm->route_cap)));
     for (const Peer& p : cm->peers) { cm->prank.push_back(p.rank); cm->poff.push_back(p.off); cm->pback.push_back(p.back); }
-    if (c.exchange == LAG_XCHG_PEER && !cm->peers.empty()) {
+    if ((c.exchange == LAG_XCHG_PEER || c.exchange == LAG_XCHG_PEER_OVERLAP) && !cm->peers.empty()) {
         std::vector<uint32_t> caps;
         std::vector<int64_t> send_off, send_by_off(kMaxOff, 0);
         std::vector<int> rbox;
@@ -535,6 +535,11 @@ static lag_status peer_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool wit
     const AppendArgs ap = append_args(ctx, (int)((seq & 1) ^ 1));   // hand-offs of cycle seq-1
     return lag_peer_exchange(ctx, cm->peer, cm->d_send_boxes, (int)cm->peers.size(), cm->halo_send_floats,
                              v0, v1, with_v0, true, cm->poff, cm->pback, seq - 1, &ap);
+}
+
+bool lag_comm_overlap(lag_ctx_s* ctx) {
+    return ctx->comm && ctx->comm->peer && !ctx->comm->peers.empty() &&
+           ctx->cfg.exchange == LAG_XCHG_PEER_OVERLAP;
 }
 
 lag_status lag_comm_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool v0_is_prev_v1) {

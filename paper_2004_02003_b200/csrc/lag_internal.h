@@ -9,7 +9,7 @@
 #include <string>
 
 namespace lag {
-enum : int { W_DEAD = 0, W_ERR = 1, W_NTILES = 2, W_APPEND_DONE = 3, kWords = 8 };
+enum : int { W_DEAD = 0, W_ERR = 1, W_NTILES = 2, W_APPEND_DONE = 3, W_NTILES_B = 4, W_DEFER = 5, kWords = 8 };
 struct Comm;   // lag_comm.cu
 }
 
@@ -54,11 +54,24 @@ struct lag_ctx_s {
     uint8_t* out_status = nullptr;
     int32_t* out_cycle = nullptr;
     // host-pointer staging (end-to-end path)
-    float* stage[2] = {nullptr, nullptr};
-    const void* stage_src[2] = {nullptr, nullptr};
+    // three staging buffers on their own copy stream: the H2D copy of the
+    // next cycle's slice overlaps the current cycle's kernels
+    static constexpr int kStage = 3;
+    float* stage[kStage] = {nullptr, nullptr, nullptr};
+    const void* stage_src[kStage] = {nullptr, nullptr, nullptr};
+    int64_t stage_use[kStage] = {-1, -1, -1};     // cycle that last read the buffer
+    cudaEvent_t stage_ready[kStage] = {};         // copy done (copy stream)
+    cudaEvent_t stage_free[kStage] = {};          // last reader done (ctx->stream)
+    cudaStream_t cstream = nullptr;
+    int last_v1_slot = -1;                        // buffer holding the previous call's host v_t1
     const void* last_v1 = nullptr;
     // COMM
     lag::Comm* comm = nullptr;
+    // LAG_XCHG_PEER_OVERLAP: the exchange runs in the first CTAs of the advect
+    // pass 1 while the ghost-free tiles advect; deferred tile ids in defer_list
+    cudaStream_t xstream = nullptr;            // exchange launches on this stream when set (default: stream)
+    void* xchg_fused = nullptr;                // non-null: lag_peer_exchange fills this XchgFused, no launch
+    uint32_t* defer_list = nullptr;
     // phase timing (LAG_PHASE_TIMING=1): events around pre-exchange / advect / post
     bool phase_timing = false;
     cudaEvent_t ph_ev[64][4] = {};
@@ -76,5 +89,6 @@ lag_status lag_comm_reset(lag_ctx_s* ctx);
 lag_status lag_comm_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool v0_is_prev_v1);
 void lag_comm_fill_args(lag_ctx_s* ctx, lag::AdvectArgs* a);
 lag_status lag_comm_post_advect(lag_ctx_s* ctx);
+bool lag_comm_overlap(lag_ctx_s* ctx);        // LAG_XCHG_PEER_OVERLAP with neighbours
 lag_status lag_comm_return_to_origin(lag_ctx_s* ctx);
 void lag_comm_returned(lag_ctx_s* ctx, const float4** rec, int64_t* stride_f4, uint32_t* n);

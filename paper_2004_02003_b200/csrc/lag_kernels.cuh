@@ -88,6 +88,15 @@ struct AdvectArgs {
     int32_t n_sig;
     unsigned long long sig_value;
     uint32_t* done_warps;
+    // COMM exchange overlap (LAG_XCHG_PEER_OVERLAP): pass 1 advects tiles
+    // [0, *n_tiles_b) whose stage samples cannot reach a ghost node and defers
+    // the others; pass 2 advects the deferred tiles and the tiles appended by
+    // this cycle's exchange.  pass 0: every tile.
+    int32_t pass;
+    const uint32_t* n_tiles_b;      // tile count before this cycle's append
+    uint32_t* defer_list;
+    uint32_t* defer_count;
+    int32_t smin[3], sspan[3];      // ghost-free cells (gather offsets): samples stay off ghost nodes
 #ifdef LAG_EXP_TIMELINE
     unsigned long long* tl;         // experiment: per-cycle globaltimer stamps [64][8]
 #endif
@@ -497,13 +506,32 @@ __device__ __forceinline__ void gather_idx(const float* __restrict__ v, int idx,
     }
 }
 
+// The advect loop over a virtual grid of `ncta` CTAs (this CTA = `cta`):
+// advect_kernel runs it on the whole grid; the COMM overlap pass 1
+// (advect_xchg_kernel, lag_api.cu) on the CTAs after its exchange CTAs.
 template <int DIM, bool BTO, bool FROZEN>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
-advect_kernel(const AdvectArgs a) {
+__device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, const int ncta) {
     constexpr int NC = (1 << DIM) * DIM;             // corner floats per slice
     const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
-    const int n_tiles_all = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
+    const int warp = (cta * kThreads + threadIdx.x) >> 5;
+    int n_tiles_all = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
+    // overlap passes (COMM): loop over virtual tile indices, map to real tiles
+    int n_def = 0, n_b = 0;
+    if constexpr (!BTO) {
+        if (a.pass == 1) {
+            n_tiles_all = (int)*a.n_tiles_b;
+        } else if (a.pass == 2) {
+            n_def = (int)*a.defer_count;
+            n_b = (int)*a.n_tiles_b;
+            n_tiles_all = n_def + (n_tiles_all - n_b);
+        }
+    }
+    auto real_tile = [&](int v) -> int {
+        if constexpr (!BTO) {
+            if (a.pass == 2) return v < n_def ? (int)a.defer_list[v] : n_b + (v - n_def);
+        }
+        return v;
+    };
     // non-persistent grid: warp w owns tiles [w*tpw, (w+1)*tpw) (contiguous, so
     // a CTA's particles are spatial neighbours); the block scheduler balances
     // the load across SMs
@@ -511,7 +539,7 @@ advect_kernel(const AdvectArgs a) {
     // persistent grid: warp w owns tiles w, w + W, w + 2W, ... (W = all warps),
     // so the GPU sweeps the particle list as one compact window
     const int tile0 = warp;
-    const int tstride = (gridDim.x * kThreads) >> 5;
+    const int tstride = (ncta * kThreads) >> 5;
     const int n_tiles = n_tiles_all;
 #else
     const int tile0 = warp * a.tiles_per_warp;
@@ -523,23 +551,25 @@ advect_kernel(const AdvectArgs a) {
     uint32_t errbits = 0;
     bool did_remote = false;
 #ifdef LAG_EXP_TIMELINE
-    if (a.tl && blockIdx.x == 0 && threadIdx.x == 0) a.tl[(a.sig_value & 63) * 8 + 6] = lag_gtimer();
+    if (a.tl && cta == 0 && threadIdx.x == 0) a.tl[(a.sig_value & 63) * 8 + 6] = lag_gtimer();
 #endif
 
     // software pipeline: the next tile's count and records are in flight while
     // the current tile computes
-    int tile = tile0;
-    int cnt = tile < n_tiles ? a.tile_count[tile] : 0;
-    float4 r = tile < n_tiles ? a.state[(size_t)tile * kTile + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    int tile = tile0;                         // virtual index (== real outside overlap pass 2)
+    int rtile = tile < n_tiles ? real_tile(tile) : 0;
+    int cnt = tile < n_tiles ? a.tile_count[rtile] : 0;
+    float4 r = tile < n_tiles ? a.state[(size_t)rtile * kTile + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
 
     while (tile < n_tiles) {
         const int ntile = tile + tstride;
-        const int ncnt = ntile < n_tiles ? a.tile_count[ntile] : 0;
-        const float4 nr = ntile < n_tiles ? a.state[(size_t)ntile * kTile + lane]
+        const int nrtile = ntile < n_tiles ? real_tile(ntile) : 0;
+        const int ncnt = ntile < n_tiles ? a.tile_count[nrtile] : 0;
+        const float4 nr = ntile < n_tiles ? a.state[(size_t)nrtile * kTile + lane]
                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (cnt == 0) { tile = ntile; cnt = ncnt; r = nr; continue; }
+        if (cnt == 0) { tile = ntile; rtile = nrtile; cnt = ncnt; r = nr; continue; }
         const bool live = lane < cnt;
-        float4* trec = a.state + (size_t)tile * kTile;
+        float4* trec = a.state + (size_t)rtile * kTile;
         int g[3];
         unpack_g(__float_as_uint(r.w), a, g);
         const float d[3] = {r.x, r.y, DIM == 3 ? r.z : 0.f};
@@ -557,6 +587,18 @@ advect_kernel(const AdvectArgs a) {
         for (int ax = 0; ax < 3; ++ax) gb[ax] = g[ax] - a.gmin[ax] - kMagicBits;
         if (!cells_b<DIM>(gb, d, a.gspan, c, f) && live)
             classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);   // top-face clamp only
+        if constexpr (!BTO) {
+            if (a.pass == 1) {                // a sample could reach a ghost node: after the exchange
+                bool safe = true;
+#pragma unroll
+                for (int ax = 0; ax < DIM; ++ax) safe &= (unsigned)(c[ax] - a.smin[ax]) <= (unsigned)a.sspan[ax];
+                if (__any_sync(0xffffffffu, live && !safe)) {
+                    if (lane == 0) a.defer_list[atomicAdd(a.defer_count, 1u)] = (uint32_t)rtile;
+                    tile = ntile; rtile = nrtile; cnt = ncnt; r = nr;
+                    continue;
+                }
+            }
+        }
         int cur = vindex<DIM>(a, c);
         LAG_CHECK_GATHER(a, cur, live);
         if (!live) cur = 0;
@@ -763,12 +805,12 @@ advect_kernel(const AdvectArgs a) {
             }
         }
         if (lane == 0) {
-            a.tile_count[tile] = (uint8_t)__popc(kmask);
+            a.tile_count[rtile] = (uint8_t)__popc(kmask);
             steps += (unsigned long long)cnt;
             nterm += __popc(tmask);
             nexit += __popc(dmask) - __popc(tmask);
         }
-        tile = ntile; cnt = ncnt; r = nr;
+        tile = ntile; rtile = nrtile; cnt = ncnt; r = nr;
     }
 
     // one atomic per warp per counter (no CTA barrier: finished warps retire)
@@ -785,7 +827,7 @@ advect_kernel(const AdvectArgs a) {
             if (did_remote) __threadfence_system();          // my remote hand-offs are performed
             __syncwarp();
             if (lane == 0) {
-                const uint32_t total = (gridDim.x * kThreads) >> 5;
+                const uint32_t total = (ncta * kThreads) >> 5;
                 if (atomicAdd(a.done_warps, 1u) == total - 1) {  // last warp of the grid
                     *a.done_warps = 0u;
 #ifdef LAG_EXP_TIMELINE
@@ -799,6 +841,12 @@ advect_kernel(const AdvectArgs a) {
             }
         }
     }
+}
+
+template <int DIM, bool BTO, bool FROZEN>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+advect_kernel(const AdvectArgs a) {
+    advect_body<DIM, BTO, FROZEN>(a, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------

@@ -20,6 +20,7 @@
 // waited for my halo(seq+1), which I signal after consuming parity q.
 #include "lag_internal.h"
 #include "lag_append.cuh"
+#include "lag_xchg.cuh"
 
 #include <nccl.h>
 
@@ -53,18 +54,9 @@ using namespace lag;
 
 namespace lag {
 
-constexpr int kOff = kMaxOff;
-constexpr int kMaxPeers = 26;
 // per-rank layout table published to every rank (int64 words)
 enum : int { T_INBOX = 0, T_INBOX_PAR = 1, T_OUTBOX = 2, T_HALO = 3, T_RECV = 4, T_SEND = 4 + kOff,
              T_WORDS = 4 + 2 * kOff };
-
-struct PeerBox {            // one ghost box to fill from a remote outbox
-    int x0, y0, z0, nx, ny, nz;
-    int64_t off;            // float offset of this box in the flattened copy
-    const float* src[2][2]; // [parity][slice 0 = v_t, 1 = v_t1] remote source
-    int slice;
-};
 
 struct PeerArgs {
     // wait
@@ -130,120 +122,12 @@ __global__ void peer_unpack_kernel(PeerUnpackArgs a) {
     }
 }
 
-// Per-cycle exchange in two multi-CTA kernels (the advect kernel signals the
-// hand-offs itself):
-//   A: pack my ghost sources (grid-stride); the last CTA to finish fences and
-//      signals halo(seq) to every neighbour;
-//   B: every CTA waits (bounded) for all neighbours' halo(seq) and
-//      particles(seq-1), then pulls its share of the ghost layers with remote
-//      loads; CTA 0 also appends the previous cycle's hand-offs.
-struct XchgArgs {
-    float* v0;
-    float* v1;
-    const Box* send_boxes;
-    int nsend;
-    float* outbox;                                 // my outbox at parity q
-    int64_t sfl;                                   // floats to pack
-    int signal_halo;
-    unsigned long long* halo_flag[kMaxPeers];      // neighbour's halo flag word for me
-    uint32_t* done_ctas;                           // kernel A completion counter
-    int npeers;
-    const unsigned long long* my_flags;
-    int back[kMaxPeers];
-    unsigned long long need_halo, need_part;
-    long long timeout_cycles;
-    uint32_t* err;
-    const PeerBox* recv_boxes;
-    int nrecv;
-    int parity;
-    int64_t rtotal;                                // floats to pull
-    int sx, sxy, dim;
-    unsigned long long seq;
-    int do_append;
-#ifdef LAG_EXP_TIMELINE
-    unsigned long long* tl;
-#endif
-};
-
 __global__ void __launch_bounds__(256) peer_pack_signal_kernel(XchgArgs x) {
-#ifdef LAG_EXP_TIMELINE
-    if (x.tl && blockIdx.x == 0 && threadIdx.x == 0) x.tl[(x.seq & 63) * 8 + 0] = lag_gtimer();
-#endif
-#ifdef LAG_EXP_NOPACK
-    if (false)
-#endif
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < x.sfl;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int k = 0;
-        while (k + 1 < x.nsend && x.send_boxes[k + 1].off <= i) ++k;
-        const Box& b = x.send_boxes[k];
-        const int64_t j = i - b.off;
-        const int comp = (int)(j % x.dim);
-        const int64_t node = j / x.dim;
-        const int xx = (int)(node % b.nx), yy = (int)((node / b.nx) % b.ny), zz = (int)(node / ((int64_t)b.nx * b.ny));
-        const float* src = b.slice ? x.v1 : x.v0;
-        x.outbox[i] = src[(int64_t)x.dim * ((b.x0 + xx) + (int64_t)x.sx * (b.y0 + yy) + (int64_t)x.sxy * (b.z0 + zz)) + comp];
-    }
-    __syncthreads();                                  // the CTA's packs are visible to thread 0
-    if (threadIdx.x == 0 && x.signal_halo) {
-        __threadfence_system();                       // cumulative: orders the CTA's packs
-        if (atomicAdd(x.done_ctas, 1u) == gridDim.x - 1) {   // last CTA: halo(seq) ready
-            *x.done_ctas = 0u;
-#ifdef LAG_EXP_TIMELINE
-            if (x.tl) x.tl[(x.seq & 63) * 8 + 1] = lag_gtimer();
-#endif
-            __threadfence_system();
-            for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(x.halo_flag[p]) = x.seq;
-            __threadfence_system();
-        }
-    }
+    xchg_pack_signal(x, blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(256) peer_wait_pull_kernel(XchgArgs x, AppendArgs ap) {
-#ifdef LAG_EXP_TIMELINE
-    if (x.tl && blockIdx.x == 0 && threadIdx.x == 0) x.tl[(x.seq & 63) * 8 + 2] = lag_gtimer();
-#endif
-#ifndef LAG_EXP_NOWAIT
-    if (threadIdx.x < x.npeers) {
-        const volatile unsigned long long* fh = x.my_flags + 0 * kOff + x.back[threadIdx.x];
-        const volatile unsigned long long* fp = x.my_flags + 1 * kOff + x.back[threadIdx.x];
-        const long long t0 = clock64();
-        while (*fh < x.need_halo || *fp < x.need_part) {
-            if (clock64() - t0 > x.timeout_cycles) { atomicOr(x.err, ERR_XCHG); break; }
-            __nanosleep(100);
-        }
-        __threadfence_system();
-    }
-#endif
-    __syncthreads();
-#ifdef LAG_EXP_TIMELINE
-    if (x.tl && threadIdx.x == 0) atomicMax(x.tl + (x.seq & 63) * 8 + 3, lag_gtimer());
-#endif
-#ifdef LAG_EXP_NOPULL
-    if (false)
-#endif
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < x.rtotal;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int k = 0;
-        while (k + 1 < x.nrecv && x.recv_boxes[k + 1].off <= i) ++k;
-        const PeerBox& b = x.recv_boxes[k];
-        const int64_t j = i - b.off;
-        const int comp = (int)(j % x.dim);
-        const int64_t node = j / x.dim;
-        const int xx = (int)(node % b.nx), yy = (int)((node / b.nx) % b.ny), zz = (int)(node / ((int64_t)b.nx * b.ny));
-        float* dst = b.slice ? x.v1 : x.v0;
-        dst[(int64_t)x.dim * ((b.x0 + xx) + (int64_t)x.sx * (b.y0 + yy) + (int64_t)x.sxy * (b.z0 + zz)) + comp] =
-            b.src[x.parity][b.slice][j];
-    }
-#ifdef LAG_EXP_TIMELINE
-    __syncthreads();
-    if (x.tl && threadIdx.x == 0) atomicMax(x.tl + (x.seq & 63) * 8 + 4, lag_gtimer());
-#endif
-    if (x.do_append) append_body(ap);                         // hand-offs of cycle seq-1 (all CTAs)
-#ifdef LAG_EXP_TIMELINE
-    __syncthreads();
-    if (x.tl && threadIdx.x == 0) atomicMax(x.tl + (x.seq & 63) * 8 + 5, lag_gtimer());
-#endif
+    xchg_wait_pull(x, ap, blockIdx.x, gridDim.x);
 }
 
 }  // namespace lag
@@ -480,6 +364,7 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
                              const std::vector<int>& poff, const std::vector<int>& pback,
                              unsigned long long need_part, const void* append_args) {
     const int np = (int)poff.size();
+    cudaStream_t st = ctx->xstream ? ctx->xstream : ctx->stream;   // overlap: the side stream
     XchgArgs x{};
     const unsigned long long seq = ps->seq;
     const int q = (int)(seq & 1);
@@ -510,18 +395,24 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
     x.done_ctas = ps->done_ctas;
 #ifdef LAG_EXP_TIMELINE
     x.tl = ps->tl;
-    if (ps->tl) cudaMemsetAsync(ps->tl + (seq & 63) * 8, 0, 8 * sizeof(unsigned long long), ctx->stream);
+    if (ps->tl) cudaMemsetAsync(ps->tl + (seq & 63) * 8, 0, 8 * sizeof(unsigned long long), st);
 #endif
     AppendArgs ap{};
     if (append_args) ap = *reinterpret_cast<const AppendArgs*>(append_args);
+    if (ctx->xchg_fused && halo) {           // overlap: the advect kernel's first CTAs run it
+        XchgFused* f = reinterpret_cast<XchgFused*>(ctx->xchg_fused);
+        f->x = x;
+        f->ap = ap;
+        return LAG_OK;
+    }
     const int cap = ctx->num_sms * 2;
     if (halo) {
         const int ga = (int)std::max<int64_t>(1, std::min<int64_t>((x.sfl + 255) / 256, cap));
-        peer_pack_signal_kernel<<<ga, 256, 0, ctx->stream>>>(x);
+        peer_pack_signal_kernel<<<ga, 256, 0, st>>>(x);
         ++ctx->launches;
     }
     const int gb = (int)std::max<int64_t>(1, std::min<int64_t>((x.rtotal + 255) / 256, cap));
-    peer_wait_pull_kernel<<<gb, 256, 0, ctx->stream>>>(x, ap);
+    peer_wait_pull_kernel<<<gb, 256, 0, st>>>(x, ap);
     ++ctx->launches;
     CKC(cudaGetLastError());
     return LAG_OK;

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("LAG_LIB") or os.path.join(HERE, "liblag.so")
 LAG_OK, LAG_EINVAL, LAG_ESTATE, LAG_EEMPTY, LAG_ENOMEM = 0, -1, -2, -3, -4
 LAG_ECUDA, LAG_ENCCL, LAG_EOVERFLOW, LAG_EGHOST, LAG_ENONFINITE = -5, -6, -7, -8, -9
 LAG_BTO, LAG_COMM = 0, 1
-LAG_XCHG_NCCL, LAG_XCHG_PEER = 0, 1
+LAG_XCHG_NCCL, LAG_XCHG_PEER, LAG_XCHG_PEER_OVERLAP = 0, 1, 2
 LAG_VALID, LAG_TERM_BOUNDARY, LAG_EXIT_DOMAIN = 0, 1, 2
 LAG_NO_RESEED = 1
 LAG_ASYNC = 2

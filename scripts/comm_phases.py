@@ -25,7 +25,8 @@ def main():
     flush = None if "--no-flush" in sys.argv else torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     out = {}
     for name, mode, xch in [("bto", P.LAG_BTO, 0), ("comm_nccl", P.LAG_COMM, P.LAG_XCHG_NCCL),
-                            ("comm_peer", P.LAG_COMM, P.LAG_XCHG_PEER)]:
+                            ("comm_peer", P.LAG_COMM, P.LAG_XCHG_PEER),
+                            ("comm_peer_overlap", P.LAG_COMM, P.LAG_XCHG_PEER_OVERLAP)]:
         nid = bench.broadcast_bytes(P.lag_nccl_unique_id() if rank == 0 else None, world, rank)
         arm = bench.Arm(cfg, rank, world, mode, nccl_id=nid, exchange=xch)
         bench.run_arm(arm, 2, flush)
@@ -34,8 +35,13 @@ def main():
         st1 = arm.ctx.stats()
         cyc = 4 * arm.interval
         ph = [(b - a) * 1e3 / cyc for a, b in zip(st0["phase_ms"], st1["phase_ms"])]
-        r = {"us_per_cycle_event": 1e3 * sum(t_adv) / cyc, "pre_exchange_us": ph[0], "advect_us": ph[1],
-             "post_us": ph[2], "sent": st1["sent"]}
+        if xch == P.LAG_XCHG_PEER_OVERLAP and mode == P.LAG_COMM:   # phases of the fused cycle
+            r = {"us_per_cycle_event": 1e3 * sum(t_adv) / cyc, "snapshot_us": ph[0],
+                 "pass1_exchange_and_ghost_free_us": ph[1], "pass2_deferred_and_arrivals_us": ph[2],
+                 "sent": st1["sent"]}
+        else:
+            r = {"us_per_cycle_event": 1e3 * sum(t_adv) / cyc, "pre_exchange_us": ph[0], "advect_us": ph[1],
+                 "post_us": ph[2], "sent": st1["sent"]}
         allr = [None] * world
         dist.all_gather_object(allr, r)
         out[name] = {k: max(x[k] for x in allr) for k in r}

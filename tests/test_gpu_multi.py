@@ -1,6 +1,8 @@
 """Multi-GPU parity (needs >= 2 GPUs; launched through torchrun).  The COMM
 baseline over NCCL must equal the single-block run bitwise (decomposition
-invariance) and match the fp64 oracle; BTO per rank vs the oracle."""
+invariance) and match the fp64 oracle; the peer-memory transports
+(plain and overlapped) must equal it bitwise with the ghost layers poisoned
+until the exchange fills them; BTO per rank vs the oracle."""
 import json
 import os
 import subprocess
@@ -31,3 +33,6 @@ def test_mgpu_comm_and_bto(nproc, config, scale):
     rep = json.loads(lines[-1])
     assert rep["ok"] and rep["sent"] > 0 and rep["comm_vs_single_bitwise_mismatching_arrays"] == 0
     assert rep["peer_vs_nccl_bitwise_mismatching_arrays"] == 0 and rep["peer_sent"] == rep["sent"]
+    # exchange overlapped with the ghost-free tiles (ghosts poisoned with NaN
+    # until the exchange fills them): bitwise the NCCL result
+    assert rep["overlap_vs_nccl_bitwise_mismatching_arrays"] == 0 and rep["overlap_sent"] == rep["sent"]
