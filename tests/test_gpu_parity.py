@@ -85,6 +85,37 @@ def test_host_pointers_match_device_pointers_bitwise():
         assert np.array_equal(x, y)
 
 
+def test_host_buffers_reused_by_the_caller():
+    """End-to-end path when the caller cycles two pinned host buffers and
+    refills them: only the previous v_t1 passed again as v_t may be taken from
+    the library's staging; a refilled buffer is copied afresh (same bits as
+    the device path)."""
+    import torch
+    import paper_2004_02003_b200 as P
+    cfg = L.make_config("C2", scale=21)
+    sl = global_slices(cfg, 6)
+    b = L.decompose(cfg["grid"], cfg["layout"])[3]
+    ref = gpu_block(cfg, b, sl, 1, host=False)
+    g = cfg["grid"]
+    cut = [np.ascontiguousarray(L.cut_block_slice(V, g, b, 0), dtype=np.float32) for V in sl]
+    bufs = [torch.from_numpy(cut[0].copy()).pin_memory(), torch.from_numpy(cut[1].copy()).pin_memory()]
+    ctx = P.Context(P.make_config(g.dim, g.nodes, g.origin, g.spacing, b.lo, b.hi,
+                                  stream=torch.cuda.current_stream().cuda_stream))
+    n = ctx.seed(1)
+    for k in range(len(sl) - 1):
+        cur, nxt = bufs[k % 2], bufs[(k + 1) % 2]
+        if k > 0:                                  # refill the buffer that becomes v_t1
+            torch.cuda.synchronize()
+            nxt.copy_(torch.from_numpy(cut[k + 1]))
+        ctx.advect(cur, nxt, cfg["dt"])
+    start = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    end, status = torch.empty_like(start), torch.empty((n,), dtype=torch.uint8, device="cuda")
+    ctx.extract(start, end, status)
+    ctx.close()
+    for x, y in zip(ref[:3], (start.cpu().numpy(), end.cpu().numpy(), status.cpu().numpy())):
+        assert np.array_equal(x, y)
+
+
 def test_single_rank_comm_equals_bto_bitwise():
     """R = 1 equivalence: COMM and BTO on one block agree bitwise."""
     cfg = L.make_config("C2", scale=21)
