@@ -80,9 +80,10 @@ __device__ __forceinline__ bool brick_cell(const int v1[3], const float fs[3], c
     bool ok = true;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-        const float fl = floorf(fs[ax]);
+        int tb;
+        const float fl = floor_fma(fs[ax], tb);
         f[ax] = fs[ax] - fl;                                             // exact
-        v[ax] = v1[ax] + (__float_as_int(fl + 12582912.0f) - kMagicBits);
+        v[ax] = v1[ax] + (tb - kMagicBits);
         ok &= (unsigned)v[ax] <= (unsigned)span[ax];
     }
     return ok;

@@ -245,17 +245,25 @@ __device__ __forceinline__ void poly_eval(const float* P, const float f[3], floa
 // Cell of a stage sample e (displacement from g, cell units):
 // c = g + floor(e), f = e - floor(e) (exact).  Fast path: every axis inside
 // the range [lo_, lo_ + span_] (one unsigned compare per axis).
+// floor(e) on the FMA pipe (no FRND): for |e| < 2^22, e + 1.5*2^23 rounded
+// toward -inf is 1.5*2^23 + floor(e) exactly, so its bits hold floor(e) in
+// the low mantissa (bits - 0x4B400000 = floor(e)) and t - 1.5*2^23 is floor(e).
+__device__ __forceinline__ float floor_fma(float e, int& bits) {
+    const float t = __fadd_rd(e, 12582912.0f);
+    bits = __float_as_int(t);
+    return t - 12582912.0f;
+}
+
 template <int DIM>
 __device__ __forceinline__ bool cells(const int g[3], const float e[3], const int32_t* rmin,
                                       const int32_t* rspan, int c[3], float f[3]) {
     bool ok = true;
 #pragma unroll
     for (int ax = 0; ax < DIM; ++ax) {
-        const float fl = floorf(e[ax]);
+        int tb;
+        const float fl = floor_fma(e[ax], tb);
         f[ax] = e[ax] - fl;                              // exact
-        // int(fl) without the XU pipe: |fl| < 2^22, so fl + 1.5*2^23 is exact
-        // and its low mantissa bits are the two's-complement integer
-        c[ax] = g[ax] + (__float_as_int(fl + 12582912.0f) - 0x4B400000);
+        c[ax] = g[ax] + (tb - 0x4B400000);
         ok &= (unsigned)(c[ax] - rmin[ax]) <= (unsigned)rspan[ax];
     }
     if constexpr (DIM == 2) { c[2] = 0; f[2] = 0.f; }
@@ -305,9 +313,10 @@ __device__ __forceinline__ bool cells_b(const int gb[3], const float e[3], const
     bool ok = true;
 #pragma unroll
     for (int ax = 0; ax < DIM; ++ax) {
-        const float fl = floorf(e[ax]);
+        int tb;
+        const float fl = floor_fma(e[ax], tb);
         f[ax] = e[ax] - fl;                              // exact
-        v[ax] = gb[ax] + __float_as_int(fl + 12582912.0f);   // = c - rmin (|fl| < 2^22)
+        v[ax] = gb[ax] + tb;                             // = c - rmin (|e| < 2^22)
         ok &= (unsigned)v[ax] <= (unsigned)rspan[ax];
     }
     if constexpr (DIM == 2) { v[2] = 0; f[2] = 0.f; }
@@ -362,9 +371,10 @@ __device__ __forceinline__ int stage_cell(const AdvectArgs& a, const int v1[3], 
         bool ok = true;
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) {
-            const float fl = floorf(fs[ax]);
+            int tb;
+            const float fl = floor_fma(fs[ax], tb);
             f[ax] = fs[ax] - fl;                                   // exact
-            v[ax] = v1[ax] + (__float_as_int(fl + 12582912.0f) - 0x4B400000);
+            v[ax] = v1[ax] + (tb - 0x4B400000);
             ok &= (unsigned)v[ax] <= (unsigned)a.gspan[ax];
         }
         if constexpr (DIM == 2) v[2] = 0;
