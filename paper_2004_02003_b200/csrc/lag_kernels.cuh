@@ -853,277 +853,9 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
     }
 }
 
-// ---------------------------------------------------------------------------
-// advect_body_pipe: the same per-particle steps as advect_body, with the tile
-// loop software-pipelined one tile deep.  Right after a tile's update (its
-// corner registers are dead), the next tile's stage-1 cell is located and its
-// 48 corner loads are issued into the same registers; the current tile's
-// compaction, termination records and counters then run while those loads
-// are in flight.  Overlap passes (COMM pass 1/2) use advect_body.
-#ifndef LAG_EPI_PIPE
-#define LAG_EPI_PIPE 1
-#endif
-template <int DIM>
-struct TileSetup {
-    int tile, rtile, cnt;
-    float4 r;
-    bool live, gbad;
-    int g[3], gb[3], v1c[3], idx1;
-    float f1[3];
-};
-
-template <int DIM, bool BTO, bool FROZEN>
-__device__ __forceinline__ bool pipe_setup(const AdvectArgs& a, int t, int c, float4 rr, int n_tiles,
-                                           int tstride, int lane, TileSetup<DIM>& s, f2_t* S, f2_t* B) {
-    while (t < n_tiles) {
-        if (c == 0) {                                    // empty tile: next one (rare, synchronous)
-            t += tstride;
-            if (t >= n_tiles) break;
-            c = a.tile_count[t];
-            rr = a.state[(size_t)t * kTile + lane];
-            continue;
-        }
-        s.tile = t; s.rtile = t; s.cnt = c; s.r = rr;
-        s.live = lane < c;
-        s.gbad = false;
-        unpack_g(__float_as_uint(rr.w), a, s.g);
-        const float d[3] = {rr.x, rr.y, DIM == 3 ? rr.z : 0.f};
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) s.gb[ax] = s.g[ax] - a.gmin[ax] - kMagicBits;
-        int cc[3];
-        float ff[3];
-        if (!cells_b<DIM>(s.gb, d, a.gspan, cc, ff) && s.live)
-            classify_slow_v<DIM, BTO>(a, cc, ff, s.gbad);   // top-face clamp only
-        int cur = vindex<DIM>(a, cc);
-        LAG_CHECK_GATHER(a, cur, s.live);
-        if (!s.live) cur = 0;
-        s.idx1 = cur;
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) { s.v1c[ax] = cc[ax]; s.f1[ax] = ff[ax]; }
-        gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
-        if constexpr (FROZEN) {
-#pragma unroll
-            for (int i = 0; i < Pairs<DIM>::n; ++i) B[i] = S[i];
-        } else {
-            gather_pairs<DIM>(a.v1, cur, a.sx, a.sxy, B);
-        }
-        return true;
-    }
-    return false;
-}
-
-template <int DIM, bool BTO, bool FROZEN>
-__device__ __forceinline__ void advect_body_pipe(const AdvectArgs& a, const int cta, const int ncta) {
-    constexpr int NP = Pairs<DIM>::n;
-    const int lane = threadIdx.x & 31;
-    const int warp = (cta * kThreads + threadIdx.x) >> 5;
-    const int n_tiles = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
-    const int tstride = (ncta * kThreads) >> 5;          // persistent: tiles warp, warp + W, ...
-
-    unsigned long long steps = 0, nterm = 0, nexit = 0, nsent = 0;
-    uint32_t errbits = 0;
-    bool did_remote = false;
-
-    f2_t S[NP], B[NP];
-    TileSetup<DIM> cs;
-    bool have = false;
-    {
-        const int t = warp;
-        const int c = t < n_tiles ? a.tile_count[t] : 0;
-        const float4 rr = t < n_tiles ? a.state[(size_t)t * kTile + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-        have = pipe_setup<DIM, BTO, FROZEN>(a, t, c, rr, n_tiles, tstride, lane, cs, S, B);
-    }
-    while (have) {
-        // the next tile's count and record are in flight while this one computes
-        const int ntile = cs.tile + tstride;
-        const int ncnt = ntile < n_tiles ? a.tile_count[ntile] : 0;
-        const float4 nr = ntile < n_tiles ? a.state[(size_t)ntile * kTile + lane]
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
-        const bool live = cs.live;
-        const float d[3] = {cs.r.x, cs.r.y, DIM == 3 ? cs.r.z : 0.f};
-        bool ghost_bad = cs.gbad;
-        uint8_t st = ST_VALID;
-        int cur = cs.idx1;
-        float f[3], e[3];
-
-        // ---- stage 1 (corners gathered by pipe_setup) ----
-        float k1[3];
-        interp_pairs<DIM>(S, cs.f1, k1);
-#pragma unroll
-        for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);   // S = v0 + v1 (stages 2, 3)
-
-        // ---- stages 2, 3 (alpha = 1/2: S) ----
-        float T2[3], T3[3];
-#pragma unroll
-        for (int sg = 2; sg <= 3; ++sg) {
-#pragma unroll
-            for (int ax = 0; ax < DIM; ++ax)
-                e[ax] = sg == 2 ? fmaf(a.hdth[ax], k1[ax], cs.f1[ax]) : fmaf(a.qdth[ax], T2[ax], cs.f1[ax]);
-            const int idx = stage_cell<DIM, BTO>(a, cs.v1c, cs.idx1, e, live && st == ST_VALID, st, ghost_bad, f);
-            LAG_CHECK_GATHER(a, idx, live && st == ST_VALID);
-            if (live && st == ST_VALID && idx != cur) {
-                gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
-                if constexpr (FROZEN) {
-#pragma unroll
-                    for (int i = 0; i < NP; ++i) B[i] = S[i];
-                } else {
-                    gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
-                }
-#pragma unroll
-                for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
-                cur = idx;
-            }
-            if (sg == 2) interp_pairs<DIM>(S, f, T2);                 // T2 = 2 k2
-            else interp_pairs<DIM>(S, f, T3);                         // T3 = 2 k3
-        }
-
-        // ---- stage 4 (alpha = 1: B) ----
-#pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], T3[ax], cs.f1[ax]);
-        {
-            const int idx = stage_cell<DIM, BTO>(a, cs.v1c, cs.idx1, e, live && st == ST_VALID, st, ghost_bad, f);
-            LAG_CHECK_GATHER(a, idx, live && st == ST_VALID);
-            if (live && st == ST_VALID && idx != cur) gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
-        }
-        float k4[3];
-        interp_pairs<DIM>(B, f, k4);
-
-        // ---- update and membership ----
-        float dn[3];
-#pragma unroll
-        for (int ax = 0; ax < DIM; ++ax)
-            dn[ax] = fmaf(a.sdth[ax], (k1[ax] + k4[ax]) + (T2[ax] + T3[ax]), d[ax]);
-        if constexpr (DIM == 2) dn[2] = 0.f;
-        bool finite = true;
-#pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) finite &= fabsf(dn[ax]) < 4194304.f;   // 2^22 cells
-        bool migrate = false;
-        int nb = 0;
-        {
-            int cn[3];
-            float fn[3];
-            int gbb[3];
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) gbb[ax] = BTO ? cs.gb[ax] : cs.g[ax] - a.bmin[ax] - kMagicBits;
-            const bool inblk = cells_b<DIM>(gbb, dn, a.bspan, cn, fn);
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) cn[ax] += a.bmin[ax];
-            if (!inblk && live && st == ST_VALID) {
-                bool gdummy = false;
-                if constexpr (BTO) {
-                    st = classify_slow<DIM, true>(a, cn, fn, gdummy);
-                } else {
-                    bool out_dom = false;
-                    int mul = 1;
-#pragma unroll
-                    for (int ax = 0; ax < DIM; ++ax) {
-                        out_dom |= (cn[ax] < 0) | (cn[ax] > a.N[ax] - 1) |
-                                   ((cn[ax] == a.N[ax] - 1) & (fn[ax] != 0.f));
-                        const int o = (cn[ax] < a.lo[ax]) ? -1
-                                      : ((cn[ax] >= a.hi[ax] && a.hi[ax] < a.N[ax]) ? 1 : 0);
-                        migrate |= (o != 0);
-                        nb += (o + 1) * mul;
-                        mul *= 3;
-                    }
-                    if constexpr (DIM == 2) nb += 9;
-                    if (out_dom) { st = ST_EXIT; migrate = false; }
-                }
-            }
-        }
-        if (live && !finite) { errbits |= ERR_NONFINITE; st = ST_EXIT; migrate = false; }
-        if (live && ghost_bad) { errbits |= ERR_GHOST; if (st == ST_VALID) st = ST_EXIT; migrate = false; }
-        const float4 r = cs.r;
-        const int rtile = cs.rtile, cnt = cs.cnt;
-
-        // ---- next tile: locate and issue its corner loads now ----
-        TileSetup<DIM> ns;
-        const bool nhave = pipe_setup<DIM, BTO, FROZEN>(a, ntile, ncnt, nr, n_tiles, tstride, lane, ns, S, B);
-
-        // ---- particle management of this tile (overlaps those loads) ----
-        float4* trec = a.state + (size_t)rtile * kTile;
-        const bool keep = live && st == ST_VALID && !migrate;
-        const unsigned kmask = __ballot_sync(0xffffffffu, keep);
-        const unsigned dmask = __ballot_sync(0xffffffffu, live && st != ST_VALID);
-        const unsigned tmask = __ballot_sync(0xffffffffu, live && st == ST_TERM);
-        __syncwarp();
-        if (keep) {
-            const int pos = __popc(kmask & ((1u << lane) - 1u));
-            trec[pos] = make_float4(dn[0], dn[1], dn[2], r.w);
-        }
-        if constexpr (!BTO) {
-            const unsigned mmask = __ballot_sync(0xffffffffu, migrate);
-            if (migrate) {
-                const unsigned peers = __match_any_sync(mmask, nb);
-                const int leader = __ffs(peers) - 1;
-                float4* sb = a.slot_ptr[nb];
-                uint32_t base0 = 0;
-                if (lane == leader) base0 = atomicAdd(reinterpret_cast<uint32_t*>(sb), (uint32_t)__popc(peers));
-                base0 = __shfl_sync(peers, base0, leader);
-                const uint32_t pos = base0 + __popc(peers & ((1u << lane) - 1u));
-                if (pos < (uint32_t)a.slot_capv[nb])
-                    sb[1 + pos] = make_float4(dn[0], dn[1], dn[2], r.w);
-                else
-                    errbits |= ERR_OVERFLOW;
-                did_remote = true;
-            }
-            if (lane == 0) nsent += __popc(mmask);
-        }
-        if (dmask) {
-            uint32_t slot0 = 0;
-            if (lane == 0) slot0 = atomicAdd(a.dead_count, (uint32_t)__popc(dmask));
-            slot0 = __shfl_sync(0xffffffffu, slot0, 0);
-            if (live && st != ST_VALID) {
-                const uint32_t si = slot0 + __popc(dmask & ((1u << lane) - 1u));
-                if (si < a.dead_cap) {
-                    a.dead_rec[si] = r;                   // pre-step position
-                    a.dead_info[si] = ((uint32_t)st << 24) | (uint32_t)(a.cycle & 0xffffff);
-                } else {
-                    errbits |= ERR_OVERFLOW;
-                }
-            }
-        }
-        if (lane == 0) {
-            a.tile_count[rtile] = (uint8_t)__popc(kmask);
-            steps += (unsigned long long)cnt;
-            nterm += __popc(tmask);
-            nexit += __popc(dmask) - __popc(tmask);
-        }
-        cs = ns;
-        have = nhave;
-    }
-
-    if (lane == 0 && steps) {
-        atomicAdd(&a.counters[CNT_STEPS], steps);
-        if (nterm) atomicAdd(&a.counters[CNT_TERM], nterm);
-        if (nexit) atomicAdd(&a.counters[CNT_EXIT], nexit);
-        if (nsent) atomicAdd(&a.counters[CNT_SENT], nsent);
-    }
-    errbits = __reduce_or_sync(0xffffffffu, errbits);
-    if (lane == 0 && errbits) atomicOr(a.err, errbits);
-    if constexpr (!BTO) {
-        if (a.n_sig) {
-            if (did_remote) __threadfence_system();          // my remote hand-offs are performed
-            __syncwarp();
-            if (lane == 0) {
-                const uint32_t total = (ncta * kThreads) >> 5;
-                if (atomicAdd(a.done_warps, 1u) == total - 1) {  // last warp of the grid
-                    *a.done_warps = 0u;
-                    __threadfence_system();
-                    for (int k = 0; k < a.n_sig; ++k)
-                        *reinterpret_cast<volatile unsigned long long*>(a.sig_flag[k]) = a.sig_value;
-                    __threadfence_system();
-                }
-            }
-        }
-    }
-}
-
 template <int DIM, bool BTO, bool FROZEN>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 advect_kernel(const AdvectArgs a) {
-#if LAG_EPI_PIPE && LAG_ADV_PERSIST
-    if (BTO || a.pass == 0) { advect_body_pipe<DIM, BTO, FROZEN>(a, blockIdx.x, gridDim.x); return; }
-#endif
     advect_body<DIM, BTO, FROZEN>(a, blockIdx.x, gridDim.x);
 }
 
