@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define LAG_ABI_VERSION 1
+#define LAG_ABI_VERSION 2   /* 2: LAG_ASYNC extract flag, LAG_XCHG_PEER_OVERLAP */
 
 #if defined(__GNUC__)
 #define LAG_API __attribute__((visibility("default")))

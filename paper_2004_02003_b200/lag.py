@@ -21,6 +21,7 @@ LAG_ECUDA, LAG_ENCCL, LAG_EOVERFLOW, LAG_EGHOST, LAG_ENONFINITE = -5, -6, -7, -8
 LAG_BTO, LAG_COMM = 0, 1
 LAG_XCHG_NCCL, LAG_XCHG_PEER, LAG_XCHG_PEER_OVERLAP = 0, 1, 2
 LAG_VALID, LAG_TERM_BOUNDARY, LAG_EXIT_DOMAIN = 0, 1, 2
+LAG_ABI_VERSION = 2          # include/lag.h
 LAG_NO_RESEED = 1
 LAG_ASYNC = 2
 STATUS_NAMES = {0: "LAG_OK", -1: "LAG_EINVAL", -2: "LAG_ESTATE", -3: "LAG_EEMPTY",
@@ -85,6 +86,9 @@ def load(path: str = LIB_PATH):
     lib.lag_kernel_launches.argtypes = [vp]
     lib.lag_kernel_launches.restype = ctypes.c_int64
     lib.lag_abi_version.restype = ctypes.c_int32
+    if lib.lag_abi_version() != LAG_ABI_VERSION:
+        raise ImportError(f"{path} implements ABI {lib.lag_abi_version()}, the binding expects "
+                          f"{LAG_ABI_VERSION}: rebuild with `python __graft_entry__.py build`")
     if hasattr(lib, "lag_stitch"):
         lib.lag_stitch.argtypes = [ctypes.c_int32, P(ctypes.c_int64), P(ctypes.c_double), P(ctypes.c_double),
                                    ctypes.c_int32, vp, vp, ctypes.c_int64, vp, vp, vp, vp]

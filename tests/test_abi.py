@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", P.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (lag_\w+)", out))
     assert set(declared_functions()) <= exported
-    assert P.lag_abi_version() == 1
+    assert P.lag_abi_version() == 2
 
 
 def test_library_is_sm100a():
