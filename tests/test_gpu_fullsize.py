@@ -17,7 +17,7 @@ from helpers import compare
 pytestmark = pytest.mark.gpu
 
 
-def _lockstep(cfg, block, stride, ncycles, nsample=4096, seed=5, near=0):
+def _lockstep(cfg, block, stride, ncycles, nsample=4096, seed=5, near=0, twin=0.0, raw=False):
     import torch
     import paper_2004_02003_b200 as P
     g = cfg["grid"]
@@ -52,6 +52,10 @@ def _lockstep(cfg, block, stride, ncycles, nsample=4096, seed=5, near=0):
         pick = np.unique(pick)
         gs = gall[pick]
         orc = oracle.Interval(g, block.lo, block.hi, stride, oracle.BTO, gs, faces=(block.lo, block.hi))
+        tw = None
+        if twin:                # the same seeds moved by `twin` cells in x (reading R15)
+            tw = oracle.Interval(g, block.lo, block.hi, stride, oracle.BTO, gs, faces=(block.lo, block.hi))
+            tw.pos[:, 0] += twin * g.spacing[0]
         Vp = gen(0)
         Hp = host_global(Vp)
         for k in range(ncycles):
@@ -59,6 +63,8 @@ def _lockstep(cfg, block, stride, ncycles, nsample=4096, seed=5, near=0):
             ctx.advect(Vp, Vn, cfg["dt"])
             Hn = host_global(Vn)
             orc.cycle(Hp, Hn, cfg["dt"])
+            if tw is not None:
+                tw.cycle(Hp, Hn, cfg["dt"])
             Vp, Hp = Vn, Hn
         start = torch.empty((n, g.dim), dtype=torch.float64, device="cuda")
         end = torch.empty_like(start)
@@ -67,6 +73,8 @@ def _lockstep(cfg, block, stride, ncycles, nsample=4096, seed=5, near=0):
         st = ctx.stats()
     finally:
         ctx.close()
+    if raw:
+        return (orc, tw, start.cpu().numpy()[pick], end.cpu().numpy()[pick], status.cpu().numpy()[pick], st, n)
     orc_view = type("O", (), {})()
     orc_view.start, orc_view.pos, orc_view.status, orc_view.min_face = orc.start, orc.pos, orc.status, orc.min_face
     res = compare(cfg, orc_view, start.cpu().numpy()[pick], end.cpu().numpy()[pick],
@@ -111,3 +119,30 @@ def test_c2_full_size_block_sampled(rank):
     res, st, n = _lockstep(cfg, b, 1, cfg["interval"], near=4)
     assert n == 64 ** 3
     assert res["term"] > 100
+
+
+def test_c4_full_size_interval_100_twin_criterion():
+    """C4 block 0 (512^3 as 2x2x2) at stride 4, interval 100 — the chaotic
+    stress case of the sweep.  SURVEY.md §8(c) reading 15 (R15):
+    every particle valid in both runs must be within 1e-4 cells of the oracle
+    unless a twin oracle run, seeded 1e-6 cells away, deviates from the oracle
+    at least as much (the trajectory amplifies rounding); flags must agree
+    outside the excuse band unless the twin's flag also differs."""
+    from helpers import POS_TOL_CELLS, EXCUSE_CELLS
+    cfg = L.make_config("C4", interval=100)
+    b = L.decompose(cfg["grid"], cfg["layout"])[0]
+    orc, tw, start, end, status, st, n = _lockstep(cfg, b, cfg["stride"], 100, near=12, twin=1e-6, raw=True)
+    h = np.array(cfg["grid"].spacing[:3])
+    assert n == 64 ** 3 and st["particle_steps"] > 0
+    np.testing.assert_allclose(start, orc.start, rtol=0, atol=1e-12 * np.abs(orc.start).max())
+    flag_bad = (status != orc.status) & (orc.min_face >= EXCUSE_CELLS) & (tw.status == orc.status)
+    assert not flag_bad.any(), ("flag mismatch the twin does not share", int(flag_bad.sum()))
+    both = (status == 0) & (orc.status == 0)
+    err = (np.abs(end[both] - orc.pos[both]) / h).max(axis=1)
+    twin_dev = (np.abs(tw.pos[both] - orc.pos[both]) / h).max(axis=1)
+    beyond = err > POS_TOL_CELLS
+    assert not (beyond & (twin_dev < err)).any(), (
+        "GPU deviation beyond 1e-4 cells larger than the twin's",
+        int((beyond & (twin_dev < err)).sum()), float(err.max()))
+    print({"n_sample": int(status.size), "valid_both": int(both.sum()), "max_err_cells": float(err.max()),
+           "beyond_1e-4": int(beyond.sum()), "twin_dev_median": float(np.median(twin_dev))})
