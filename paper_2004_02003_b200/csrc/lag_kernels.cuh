@@ -615,17 +615,34 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         const int idx1 = cur;                 // stage-1 cell: offsets, fractions
         const int v1c[3] = {c[0], c[1], c[2]};
         const float f1[3] = {f[0], f[1], f[2]};
-        gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
-        if constexpr (FROZEN) {
-#pragma unroll
-            for (int i = 0; i < NP; ++i) B[i] = S[i];
-        } else {
-            gather_pairs<DIM>(a.v1, cur, a.sx, a.sxy, B);
-        }
         float k1[3];
-        interp_pairs<DIM>(S, f, k1);
+        if (__all_sync(0xffffffffu, !live || ((d[0] == 0.f) & (d[1] == 0.f) & (d[2] == 0.f)))) {
+            // every particle sits on its seed node (first cycle of an interval):
+            // the trilinear value at a node is the node value (f = 0, or f = 1
+            // on a clamped top face) — 3 loads; the stage-2 sample gathers its
+            // own cell (cur = -1 forces it)
+            int node[3];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);   // S = v0 + v1 (stages 2, 3)
+            for (int ax = 0; ax < 3; ++ax) node[ax] = c[ax] + (f[ax] != 0.f ? 1 : 0);
+            const float* pv = a.v0 + DIM * (live ? vindex<DIM>(a, node) : 0);
+#pragma unroll
+            for (int ax = 0; ax < DIM; ++ax) k1[ax] = __ldg(pv + ax);
+            if constexpr (DIM == 2) k1[2] = 0.f;
+            cur = -1;
+#pragma unroll
+            for (int i = 0; i < NP; ++i) S[i] = B[i] = 0ull;   // lanes stopped at stage 2 stay finite
+        } else {
+            gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
+            if constexpr (FROZEN) {
+#pragma unroll
+                for (int i = 0; i < NP; ++i) B[i] = S[i];
+            } else {
+                gather_pairs<DIM>(a.v1, cur, a.sx, a.sxy, B);
+            }
+            interp_pairs<DIM>(S, f, k1);
+#pragma unroll
+            for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);   // S = v0 + v1 (stages 2, 3)
+        }
 
         // ---- stage 2: q2 = x + dt/2 k1, alpha = 1/2 ----
 #pragma unroll
