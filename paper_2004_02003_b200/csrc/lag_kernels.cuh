@@ -557,7 +557,7 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
     const int n_tiles = min(n_tiles_all, tile0 + a.tiles_per_warp);
 #endif
 
-    unsigned long long steps = 0, nterm = 0, nexit = 0, nsent = 0;
+    uint32_t steps = 0, nterm = 0, nexit = 0, nsent = 0;  // per warp and launch: < 2^32
     uint32_t errbits = 0;
     bool did_remote = false;
 #ifdef LAG_EXP_TIMELINE
@@ -833,7 +833,7 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         }
         if (lane == 0) {
             a.tile_count[rtile] = (uint8_t)__popc(kmask);
-            steps += (unsigned long long)cnt;
+            steps += (uint32_t)cnt;
             nterm += __popc(tmask);
             nexit += __popc(dmask) - __popc(tmask);
         }
@@ -842,10 +842,10 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
 
     // one atomic per warp per counter (no CTA barrier: finished warps retire)
     if (lane == 0 && steps) {
-        atomicAdd(&a.counters[CNT_STEPS], steps);
-        if (nterm) atomicAdd(&a.counters[CNT_TERM], nterm);
-        if (nexit) atomicAdd(&a.counters[CNT_EXIT], nexit);
-        if (nsent) atomicAdd(&a.counters[CNT_SENT], nsent);
+        atomicAdd(&a.counters[CNT_STEPS], (unsigned long long)steps);
+        if (nterm) atomicAdd(&a.counters[CNT_TERM], (unsigned long long)nterm);
+        if (nexit) atomicAdd(&a.counters[CNT_EXIT], (unsigned long long)nexit);
+        if (nsent) atomicAdd(&a.counters[CNT_SENT], (unsigned long long)nsent);
     }
     errbits = __reduce_or_sync(0xffffffffu, errbits);
     if (lane == 0 && errbits) atomicOr(a.err, errbits);
