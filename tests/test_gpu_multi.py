@@ -20,7 +20,9 @@ def _ngpu():
 
 
 @pytest.mark.parametrize("nproc,config,scale", [(2, "C2", 33), (2, "C5", 20), (2, "C1", 0),
-                                                (4, "C2", 41), (4, "C1", 0), (8, "C4", 65)])
+                                                (2, "C5", 0),     # full size: 256x128x128, every particle
+                                                (4, "C2", 41), (4, "C1", 0), (4, "C5", 0),
+                                                (8, "C4", 65)])
 def test_mgpu_comm_and_bto(nproc, config, scale):
     if _ngpu() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
