@@ -228,7 +228,7 @@ LAG_API int64_t lag_kernel_launches(lag_ctx ctx);
 
 /* lag_gridfill — post hoc reconstruction of BTO holes on a dense seed
  * lattice (paper P:229-233 §3.1 "interpolated ... post hoc"; Eq. 2,
- * P:289-303 §3.3; GridFill; reading R12 in DESIGN.md).
+ * P:289-303 §3.3; GridFill; reading R18 in DESIGN.md).
  *   dim      2 or 3.
  *   dims     [dim] host array: lattice extent per axis (x fastest), each >= 1.
  *   k        components per node (1..3), e.g. k = dim for end positions.

@@ -29,7 +29,12 @@
  *    the whole domain, i.e. block := domain.
  *
  * Parity pins: tests/test_oracle_pins.py (closed forms, brute force, paper
- * values).  No function here is "parity unpinned".
+ * values).  No function here is "parity unpinned": orc_tri (tent sums, affine
+ * exactness), rk4_step (uniform, rotation, affine series, 4th order, closed
+ * crossing schedules), face_distance (uniform-flow distances,
+ * test_face_distance_uniform_flow_closed_form), mark_touched (exact node set,
+ * test_touched_nodes_exact_set_uniform_flow).  scripts/mutation_check.sh
+ * plants one mistake per function and checks that a pin fails.
  */
 #include <math.h>
 #include <stdint.h>

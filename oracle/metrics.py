@@ -169,7 +169,7 @@ def grid_fill(lat: np.ndarray, values: np.ndarray, valid: np.ndarray, hole: np.n
     """GridFill reconstruction on the seed lattice (justified
     by Eq. 2): each hole is filled by linear interpolation (Eq. 1)
     between the nearest valid seeds on both sides along a lattice axis, using
-    the axis with the shortest such bracket (ties averaged; reading R12).  `lat` are integer
+    the axis with the shortest such bracket (ties averaged; reading R18).  `lat` are integer
     lattice coordinates [n, dim] (seed node // stride); returns
     (filled values [n, k] with NaN where no axis has both bounds, filled mask)."""
     lat = np.asarray(lat)

@@ -5,7 +5,7 @@
 // reconstruction P:262-274 §3.2).  Eq. 2 (§3.3) shows linear
 // interpolation through a hole equals interpolation between its valid
 // neighbours; GridFill applies Eq. 1 along lattice axes.
-// Reading R12: each hole takes the axis with the shortest valid
+// Reading R18: each hole takes the axis with the shortest valid
 // bracket; ties are averaged.
 //
 // Two passes: (1) a coalesced copy of the valid nodes that compacts the holes

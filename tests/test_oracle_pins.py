@@ -648,3 +648,145 @@ def test_stitch_interpolant_is_continuous_across_simplices_and_cubes():
         a = stitch(ends, None, dims, o, sp, base + dv)[0][:, 1]
         b = stitch(ends, None, dims, o, sp, base - dv)[0][:, 1]
         assert np.abs(a - b).max() < 50 * eps
+
+
+# ------------------------------------------------ excuse band, sector counter,
+# GridFill axis choice, Delaunay tiling (the functions behind the flag-parity
+# excuse band, the roofline's algorithmic bytes and the agreement metric)
+
+def _uniform_x(grid, U=1.0):
+    V = np.zeros((grid.nodes[2], grid.nodes[1], grid.nodes[0], 3), dtype=np.float32)
+    V[..., 0] = U
+    return V
+
+
+def test_face_distance_uniform_flow_closed_form():
+    """Reading R14: min over post-seed stage samples and
+    committed positions of the distance, in cells, to any block or global
+    face.  Uniform flow u = (1,0,0), h = 1, dt = 1/4 (all samples dyadic, exact
+    in fp64): a seed at x = g visits g + n/4 + 1/8 (stages 2, 3) and
+    g + (n+1)/4 (stage 4 and the committed position), n = 0..I-1.  Block
+    x in [0, 8) of N_x = 17 (faces 0, 8, 16); y = z = 4 of N = 9 (distance 4).
+    Hand values: g = 2 -> 2.125 (the first stage sample; the seed itself,
+    2.0, does not count), g = 3 -> 3.0 (x = 5 at the end, 3 from face 8),
+    g = 5 -> 1.0 (x = 7), g = 7 -> 0.0 (stage 4 of cycle 3 lands on face 8 and
+    terminates there)."""
+    g = grid3((17, 9, 9))
+    V = _uniform_x(g)
+    seeds = np.array([[2, 4, 4], [3, 4, 4], [5, 4, 4], [7, 4, 4], [0, 4, 4]], dtype=np.int64)
+    it = oracle.Interval(g, (0, 0, 0), (8, 9, 9), 1, oracle.BTO, g_seeds=seeds)
+    for _ in range(8):
+        it.cycle(V, V, 0.25)
+    assert it.min_face[:4].tolist() == [2.125, 3.0, 1.0, 0.0]
+    assert it.status.tolist() == [0, 0, 0, 1, 0]
+    assert it.term_cycle[3] == 3
+    # seed 0 sits on the block's lower face and on the global face: its first
+    # stage sample is 1/8 away
+    assert it.min_face[4] == 0.125
+    # far from every x-face the y/z faces decide (4 cells)
+    g2 = grid3((41, 9, 9))
+    it2 = oracle.Interval(g2, (0, 0, 0), (41, 9, 9), 1, oracle.BTO,
+                          g_seeds=np.array([[10, 4, 4]], dtype=np.int64))
+    for _ in range(4):
+        it2.cycle(_uniform_x(g2), _uniform_x(g2), 0.25)
+    assert it2.min_face[0] == 4.0
+
+
+def test_touched_nodes_exact_set_uniform_flow():
+    """The sector counter's node map (scripts/algbytes.py, the roofline's
+    algorithmic bytes): bit 0 = nodes of V_t the stage gathers read (stages
+    1-3), bit 1 = nodes of V_t1 (stages 2-4).  Uniform flow (1,0,0), dt = 1/4,
+    one cycle from node (2,1,1): every stage sample (x = 2, 2.125, 2.125, 2.25)
+    lies in cell (2,1,1), so exactly its 8 corners x in {2,3}, y in {1,2},
+    z in {1,2} carry both bits.  From the closed top face x = 5 = N-1 moving
+    in -x the cell is clamped to 4 (corners {4,5}); stage samples 4.875 stay
+    in cell 4."""
+    g = grid3((6, 5, 4))
+    expected = np.zeros((4, 5, 6), dtype=np.uint8)
+    for z in (1, 2):
+        for y in (1, 2):
+            for x in (2, 3):
+                expected[z, y, x] = 3
+    V = _uniform_x(g)
+    touched = np.zeros((4, 5, 6), dtype=np.uint8)
+    it = oracle.Interval(g, (0, 0, 0), (6, 5, 4), 1, oracle.BTO,
+                         g_seeds=np.array([[2, 1, 1]], dtype=np.int64))
+    it.cycle(V, V, 0.25, touched=touched)
+    np.testing.assert_array_equal(touched, expected)
+    # the brute-force tent support of every stage sample lies inside the set
+    for xs in (2.0, 2.125, 2.25):
+        for idx in np.ndindex(4, 5, 6):
+            n = idx[::-1]
+            w = max(0.0, 1 - abs(xs - n[0])) * max(0.0, 1 - abs(1 - n[1])) * max(0.0, 1 - abs(1 - n[2]))
+            if w > 0:
+                assert touched[idx] == 3
+    # clamped top face
+    touched[:] = 0
+    Vm = _uniform_x(g, U=-1.0)
+    it = oracle.Interval(g, (0, 0, 0), (6, 5, 4), 1, oracle.BTO,
+                         g_seeds=np.array([[5, 1, 1]], dtype=np.int64))
+    it.cycle(Vm, Vm, 0.25, touched=touched)
+    expected[:] = 0
+    for z in (1, 2):
+        for y in (1, 2):
+            for x in (4, 5):
+                expected[z, y, x] = 3
+    np.testing.assert_array_equal(touched, expected)
+    assert it.status[0] == 0 and it.pos[0, 0] == 4.75
+
+
+def test_grid_fill_takes_the_shortest_bracket():
+    """Reading R18: a hole is filled along the lattice axis with
+    the shortest valid bracket (ties averaged).  5x5 lattice, holes at
+    (2,1), (2,2), (2,3); valid values v = 10 i + j^2 (not affine in j, so the
+    axes disagree).  Hole (2,2): x-bracket (1,2)-(3,2), span 2 -> (14 + 34)/2
+    = 24; y-bracket (2,0)-(2,4), span 4 -> (20 + 36)/2 = 28.  Hole (2,1):
+    x -> (11 + 31)/2 = 21; y (span 4) -> 20 + 16/4 = 24.  The shortest-bracket
+    rule gives 24 and 21; averaging both axes would give 26 and
+    22.5; the longest bracket 28 and 24."""
+    lat = np.array([[i, j] for j in range(5) for i in range(5)], dtype=np.int64)
+    vals = (10.0 * lat[:, 0] + lat[:, 1] ** 2)[:, None].astype(np.float64)
+    hole = np.zeros(25, dtype=bool)
+    for (i, j) in ((2, 1), (2, 2), (2, 3)):
+        hole[j * 5 + i] = True
+    valid = ~hole
+    out, filled = metrics.grid_fill(lat, np.where(valid[:, None], vals, np.nan), valid, hole)
+    assert filled.sum() == 3
+    assert out[2 * 5 + 2, 0] == 24.0
+    assert out[1 * 5 + 2, 0] == 21.0
+    assert out[3 * 5 + 2, 0] == (19 + 39) / 2     # x-bracket (1,3)-(3,3)
+    # a tie (isolated hole: spans 2 on both axes) averages the two fills
+    hole2 = np.zeros(25, dtype=bool)
+    hole2[2 * 5 + 2] = True
+    out2, _ = metrics.grid_fill(lat, vals, ~hole2, hole2)
+    assert out2[12, 0] == ((14 + 34) / 2 + (21 + 29) / 2) / 2
+
+
+def test_reconstruct_holes_one_interior_hole_and_one_corner():
+    """Reading R12 (Delaunay over the valid seeds around each hole tile,
+    barycentric end interpolation): on a 7x7 lattice with an affine
+    end map, the interior hole (3,3) is reconstructed exactly (barycentric
+    interpolation is exact on affine maps) and the corner hole (0,0) lies
+    outside the hull of the valid seeds, so it is excluded: exactly 1 of 2.
+    The tile triangulates the valid seeds within `margin` lattice steps of its
+    holes; with none (margin 0) nothing would be reconstructed."""
+    n = 7
+    g = np.array([[i, j, 0] for j in range(n) for i in range(n)], dtype=np.int64)
+    start = g[:, :2].astype(np.float64)
+    M = np.array([[1.1, 0.3], [-0.2, 0.9]])
+    end = start @ M.T + np.array([0.25, -0.5])
+    hole = np.zeros(n * n, dtype=bool)
+    hole[0] = True
+    hole[3 * n + 3] = True
+    valid = ~hole
+    rec, inside = metrics.reconstruct_holes(g, start, np.where(valid[:, None], end, np.nan), valid,
+                                            hole, 1, workers=1)
+    assert inside.tolist().count(True) == 1 and bool(inside[3 * n + 3]) and not inside[0]
+    np.testing.assert_allclose(rec[3 * n + 3], end[3 * n + 3], rtol=0, atol=1e-12)
+    # the agreement fold counts it: one hole compared, one excluded
+    st = np.where(valid, 0, 1).astype(np.uint8)
+    grid = L.Grid(2, (n, n, 1), (0.0, 0.0, 0.0), (1.0, 1.0, 1.0))
+    r = metrics.agreement(grid, g, start, np.where(valid[:, None], end, np.nan), st, end,
+                          np.zeros(n * n, dtype=np.uint8), 1)
+    assert r["holes"] == 2 and r["excluded"] == 1 and r["compared"] == n * n - 1
+    assert r["L"] < 1e-12
