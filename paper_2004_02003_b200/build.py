@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblag.so")
 SOURCES = ["lag_api.cu", "lag_comm.cu", "lag_peer.cu", "lag_recon.cu", "lag_ftle.cu", "lag_pathline.cu"]
-HEADERS = ["lag_kernels.cuh", "lag_brick.cuh", "lag_advect2.cuh", "lag_internal.h", "lag_append.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 
 def nccl_paths():

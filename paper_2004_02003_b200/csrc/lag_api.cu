@@ -198,7 +198,6 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     if ((st = dmalloc(ctx, &ctx->dead_rec, (size_t)ctx->cap)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->dead_info, (size_t)ctx->cap)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->words, (size_t)kWords)) != LAG_OK) return fail(st);
-    if ((st = dmalloc(ctx, &ctx->bbox, (size_t)(ctx->cap_tiles / kBrickTiles + 1) * kBBoxInts)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->counters, (size_t)CNT_N)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->out_start, (size_t)owned * D)) != LAG_OK) return fail(st);
     if ((st = dmalloc(ctx, &ctx->out_end, (size_t)owned * D)) != LAG_OK) return fail(st);
@@ -223,19 +222,6 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<2, true, false> : advect_kernel<2, false, false>, kThreads, 0);
     ctx->advect_blocks_per_sm = occ > 0 ? occ : 1;
-    if (D == 3) {
-        int occ2 = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, cfg->mode == LAG_BTO ? advect2_kernel<true> : advect2_kernel<false>, kThreads, 0);
-        ctx->advect2_blocks_per_sm = occ2 > 0 ? occ2 : 1;
-        const char* e2 = getenv("LAG_ADV2");
-        ctx->use_adv2 = e2 && e2[0] == '1';
-        cudaFuncSetAttribute(advect_brick_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBoxBytes);
-        cudaFuncSetAttribute(advect_brick_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBoxBytes);
-    }
-    if (const char* o = getenv("LAG_ADV_OCC")) {       // experiment hook: fewer resident CTAs per SM
-        const int v = atoi(o);
-        if (v > 0 && v < ctx->advect_blocks_per_sm) ctx->advect_blocks_per_sm = v;
-    }
     {
         const char* pt = getenv("LAG_PHASE_TIMING");
         ctx->phase_timing = pt && pt[0] == '1';
@@ -254,7 +240,7 @@ extern "C" lag_status lag_destroy(lag_ctx ctx) {
     lag_comm_destroy(ctx);
     dfree(ctx->defer_list);
     dfree(ctx->state); dfree(ctx->tile_count); dfree(ctx->dead_rec); dfree(ctx->dead_info);
-    dfree(ctx->words); dfree(ctx->counters); dfree(ctx->bbox); dfree(ctx->out_start); dfree(ctx->out_end);
+    dfree(ctx->words); dfree(ctx->counters); dfree(ctx->out_start); dfree(ctx->out_end);
     if (ctx->phase_timing)
         for (int i = 0; i < 64; ++i)
             for (int j = 0; j < 4; ++j) cudaEventDestroy(ctx->ph_ev[i][j]);
@@ -327,21 +313,6 @@ extern "C" lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out
     seed_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(sa);
     ++ctx->launches;
     CK(cudaGetLastError());
-    // experiment (LAG_BRICK=1): stride-1 3-D intervals advect brick by brick
-    // with the velocity box staged in shared memory (lag_brick.cuh; slower
-    // than advect_kernel on B200); the seeds' cell boxes start it
-    {
-        const char* eb = getenv("LAG_BRICK");
-        ctx->use_brick = D == 3 && stride == 1 && eb && eb[0] == '1';
-    }
-    if (ctx->use_brick) {
-        BBoxInitArgs ba{};
-        ba.bbox = ctx->bbox; ba.n_bricks = ctx->n_tiles / kBrickTiles; ba.stride = stride;
-        for (int a = 0; a < 3; ++a) { ba.first[a] = ctx->first[a]; ba.ns[a] = ctx->ns[a]; }
-        brick_bbox_kernel<<<(unsigned)((ba.n_bricks + 127) / 128), 128, 0, ctx->stream>>>(ba);
-        ++ctx->launches;
-        CK(cudaGetLastError());
-    }
     ctx->seeded = true;
     ctx->cycles_in_interval = 0;
     ctx->active_host = n;
@@ -505,15 +476,10 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
 
     const int tiles = ctx->cfg.mode == LAG_COMM ? ctx->cap_tiles : ctx->n_tiles;
     const int warps_per_block = kThreads / 32;
-    a.tiles_per_warp = kTilesPerWarp;
-#if LAG_ADV_PERSIST
+    // persistent grid: at most the resident CTAs (one wave)
     int blocks = (tiles + warps_per_block - 1) / warps_per_block;
     const int max_blocks = ctx->num_sms * ctx->advect_blocks_per_sm;
     if (blocks > max_blocks) blocks = max_blocks;
-#else
-    const int warps = (tiles + kTilesPerWarp - 1) / kTilesPerWarp;
-    int blocks = (warps + warps_per_block - 1) / warps_per_block;
-#endif
     if (blocks < 1) blocks = 1;
     const bool bto = ctx->cfg.mode == LAG_BTO;
     auto launch = [&](const AdvectArgs& aa, int nb) {
@@ -555,23 +521,6 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
         AdvectArgs a2 = a;
         a2.pass = 2;
         launch(a2, blocks);
-    } else if (ctx->use_brick && !a.frozen) {
-        BrickArgs b{};
-        b.a = a;
-        b.bbox = ctx->bbox;
-        b.n_seed_bricks = ctx->n_tiles / kBrickTiles;
-        b.slice_bytes = ctx->slice_floats * (int64_t)sizeof(float);
-        // persistent: one CTA per SM (two box buffers fill its shared memory)
-        const int bricks = (tiles + kBrickTiles - 1) / kBrickTiles;
-        const unsigned grid = (unsigned)std::max(1, std::min(bricks, ctx->num_sms));
-        if (bto) advect_brick_kernel<true><<<grid, kBrickThreads, 4 * kBoxBytes, ctx->stream>>>(b);
-        else advect_brick_kernel<false><<<grid, kBrickThreads, 4 * kBoxBytes, ctx->stream>>>(b);
-    } else if (D == 3 && ctx->use_adv2 && !a.frozen) {
-        const int groups = (tiles + kNpt - 1) / kNpt;
-        int nb = (groups + warps_per_block - 1) / warps_per_block;
-        nb = std::max(1, std::min(nb, ctx->num_sms * ctx->advect2_blocks_per_sm));
-        if (bto) advect2_kernel<true><<<nb, kThreads, 0, ctx->stream>>>(a);
-        else advect2_kernel<false><<<nb, kThreads, 0, ctx->stream>>>(a);
     } else {
         launch(a, blocks);
     }

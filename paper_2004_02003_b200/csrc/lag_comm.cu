@@ -40,13 +40,7 @@ float4* lag_peer_remote_slot(PeerState* ps, int i, int prank, int pback, int q);
 float4* lag_peer_inbox_slot(PeerState* ps, int q, int poff);
 float* lag_peer_outbox(PeerState* ps, int q);
 unsigned long long& lag_peer_seq(PeerState* ps);
-lag_status lag_peer_signal(lag_ctx_s* ctx, PeerState* ps, const std::vector<int>& prank,
-                           const std::vector<int>& pback, int kind, unsigned long long value);
-lag_status lag_peer_wait(lag_ctx_s* ctx, PeerState* ps, const std::vector<int>& poff,
-                         unsigned long long need_halo, unsigned long long need_part);
-lag_status lag_peer_unpack(lag_ctx_s* ctx, PeerState* ps, float* v0, float* v1, bool with_v0, int parity);
 uint32_t* lag_peer_done_counter(PeerState* ps);
-unsigned long long* lag_peer_timeline(PeerState* ps);
 unsigned long long* lag_peer_remote_flag(PeerState* ps, int i, int kind, int pback);
 lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_boxes, int nsend,
                              int64_t sfl, float* v0, float* v1, bool with_v0, bool halo,
@@ -570,9 +564,6 @@ void lag_comm_fill_args(lag_ctx_s* ctx, AdvectArgs* a) {
         a->n_sig = (int)cm->peers.size();
         a->sig_value = seq;
         a->done_warps = lag_peer_done_counter(cm->peer);
-#ifdef LAG_EXP_TIMELINE
-        a->tl = lag_peer_timeline(cm->peer);
-#endif
     }
 }
 

@@ -2,8 +2,6 @@
 #pragma once
 #include "lag.h"
 #include "lag_kernels.cuh"
-#include "lag_brick.cuh"
-#include "lag_advect2.cuh"
 
 #include <cuda_runtime.h>
 #include <string>
@@ -24,15 +22,11 @@ struct lag_ctx_s {
     int64_t slice_floats = 0;
     int num_sms = 148;
     int advect_blocks_per_sm = 1;
-    int advect2_blocks_per_sm = 1;
-    bool use_adv2 = false;           // 3-D two-slice cycles advect with advect2_kernel
     // particles
     int64_t max_seeds = 0, cap = 0;
     int cap_tiles = 0;
     int n_tiles = 0;                 // tiles holding seeds
     int brick[2] = {1, 1};           // seed brick rows (y, z) of 32-seed tiles
-    int32_t* bbox = nullptr;         // stride-1 3-D: cell box per seed brick (advect_brick_kernel)
-    bool use_brick = false;          // this interval advects with advect_brick_kernel
     int64_t n_seeds = 0, active_host = 0;
     int first[3] = {0, 0, 0}, ns[3] = {1, 1, 1};
     int stride = 1;
@@ -69,7 +63,6 @@ struct lag_ctx_s {
     lag::Comm* comm = nullptr;
     // LAG_XCHG_PEER_OVERLAP: the exchange runs in the first CTAs of the advect
     // pass 1 while the ghost-free tiles advect; deferred tile ids in defer_list
-    cudaStream_t xstream = nullptr;            // exchange launches on this stream when set (default: stream)
     void* xchg_fused = nullptr;                // non-null: lag_peer_exchange fills this XchgFused, no launch
     uint32_t* defer_list = nullptr;
     // phase timing (LAG_PHASE_TIMING=1): events around pre-exchange / advect / post

@@ -19,27 +19,9 @@
 namespace lag {
 
 constexpr int kTile = 32;
-#ifndef LAG_ADV_THREADS
-#define LAG_ADV_THREADS 128
-#endif
-#ifndef LAG_ADV_MINB
-#define LAG_ADV_MINB 4
-#endif
-#ifndef LAG_ADV_TPW
-#define LAG_ADV_TPW 4
-#endif
-constexpr int kThreads = LAG_ADV_THREADS;     // advect CTA size
-constexpr int kMinBlocks = LAG_ADV_MINB;      // __launch_bounds__ min CTAs per SM
-constexpr int kTilesPerWarp = LAG_ADV_TPW;    // contiguous 32-particle tiles per warp
-#ifndef LAG_ADV_PERSIST
-#define LAG_ADV_PERSIST 1
-#endif
-#ifndef LAG_PREFETCH
-#define LAG_PREFETCH 0   // 1: L2, 2: L1 prefetch of the next tile's stage-1 corner rows
-#endif
-#ifndef LAG_POLY
-#define LAG_POLY 0       // 1: polynomial-form trilinear (coefficients per corner set)
-#endif
+constexpr int kThreads = 128;          // advect CTA size (4 warps; DESIGN.md §9 CTA-size sweep)
+constexpr int kMinBlocks = 4;          // __launch_bounds__ min CTAs per SM
+constexpr int kBrickRows = 4;          // seed tiles are ordered in 32 x 4 x 4 bricks (3-D)
 
 enum : uint32_t { ERR_OVERFLOW = 1u, ERR_GHOST = 2u, ERR_NONFINITE = 4u, ERR_XCHG = 8u };
 enum : int { CNT_STEPS = 0, CNT_TERM = 1, CNT_EXIT = 2, CNT_SENT = 3, CNT_RECV = 4, CNT_N = 8 };
@@ -75,13 +57,12 @@ struct AdvectArgs {
     unsigned long long* counters;   // CNT_*
     uint32_t* err;
     int32_t cycle;
-    int32_t tiles_per_warp;         // contiguous tiles per warp (non-persistent grid)
     // COMM: outgoing slots, one per neighbour offset (3^dim):
     // slot k = slot_rec[slot_base[k]] = header (u32 count) then slot_capv[k] records
     float4* slot_rec;
     int32_t slot_base[27];
     int32_t slot_capv[27];
-    float4* slot_ptr[27];           // slot of offset k: local (NCCL) or the owner's inbox (peer)
+    float4* slot_ptr[27];           // slot of offset k: local (NCCL) or the owner's inbox (peer/local)
     // peer transport: the last warp to retire signals "particles of cycle
     // sig_value ready" into each neighbour's flag word
     unsigned long long* sig_flag[26];
@@ -97,177 +78,16 @@ struct AdvectArgs {
     uint32_t* defer_list;
     uint32_t* defer_count;
     int32_t smin[3], sspan[3];      // ghost-free cells (gather offsets): samples stay off ghost nodes
-#ifdef LAG_EXP_TIMELINE
-    unsigned long long* tl;         // experiment: per-cycle globaltimer stamps [64][8]
-#endif
 };
 
-#ifdef LAG_EXP_TIMELINE
-__device__ __forceinline__ unsigned long long lag_gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-#endif
-
-__device__ __forceinline__ void unpack_g(uint32_t w, const AdvectArgs& a, int g[3]) {
-    g[0] = (int)(w & a.mx);
-    g[1] = (int)((w >> a.bx) & a.my);
-    g[2] = (int)(w >> (a.bx + a.by));
-}
-
-// Corner gather: the 2^DIM corners of local cell li, DIM components each, AoS.
-// C layout: [(dz*2 + dy)*2 + dx][comp].
-template <int DIM>
-__device__ __forceinline__ void gather(const float* __restrict__ v, const int li[3],
-                                       int sx, int sxy, float* C) {
-    if constexpr (DIM == 3) {
-        const float* p = v + 3 * (li[0] + sx * li[1] + sxy * li[2]);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int dy = r & 1, dz = r >> 1;
-            const float* q = p + 3 * (dy * sx + dz * sxy);
-#pragma unroll
-            for (int e = 0; e < 6; ++e) C[r * 6 + e] = __ldg(q + e);
-        }
-    } else {
-        const float* p = v + 2 * (li[0] + sx * li[1]);
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const float* q = p + 2 * (r * sx);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) C[r * 4 + e] = __ldg(q + e);
-        }
-    }
-}
-
-// Multilinear interpolation inside one cell with fractional offsets f
-// (two partial sums per component for ILP).
-template <int DIM>
-__device__ __forceinline__ void interp(const float* C, const float f[3], float out[3]) {
-    if constexpr (DIM == 3) {
-        const float ux = 1.f - f[0], uy = 1.f - f[1], uz = 1.f - f[2];
-        float w[8];
-        const float w00 = uy * uz, w10 = f[1] * uz, w01 = uy * f[2], w11 = f[1] * f[2];
-        w[0] = ux * w00; w[1] = f[0] * w00;
-        w[2] = ux * w10; w[3] = f[0] * w10;
-        w[4] = ux * w01; w[5] = f[0] * w01;
-        w[6] = ux * w11; w[7] = f[0] * w11;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            float s0 = w[0] * C[c], s1 = w[1] * C[3 + c];
-#pragma unroll
-            for (int k = 2; k < 8; k += 2) {
-                s0 = fmaf(w[k], C[k * 3 + c], s0);
-                s1 = fmaf(w[k + 1], C[(k + 1) * 3 + c], s1);
-            }
-            out[c] = s0 + s1;
-        }
-    } else {
-        const float ux = 1.f - f[0], uy = 1.f - f[1];
-        float w[4] = {ux * uy, f[0] * uy, ux * f[1], f[0] * f[1]};
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            float s = w[0] * C[c];
-#pragma unroll
-            for (int k = 1; k < 4; ++k) s = fmaf(w[k], C[k * 2 + c], s);
-            out[c] = s;
-        }
-        out[2] = 0.f;
-    }
-}
-
-// Trilinear polynomial form of one cell's corners (in place, per component):
-//   Tri(f) = p0 + fx (px + fy (pxy + fz pxyz) + fz pxz) + fy (py + fz pyz) + fz pz
-// Built once per gathered corner set (off the stage-to-stage critical path);
-// each evaluation is then 7 FFMA per component with a 4-deep chain.  Linear
-// in the corner values, so coefficients of v_t + v_t1 are the sums.
-template <int DIM>
-__device__ __forceinline__ void to_poly(float* C) {
-    if constexpr (!LAG_POLY) return;
-    if constexpr (DIM == 3) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const float v000 = C[0 * 3 + c], v100 = C[1 * 3 + c], v010 = C[2 * 3 + c], v110 = C[3 * 3 + c];
-            const float v001 = C[4 * 3 + c], v101 = C[5 * 3 + c], v011 = C[6 * 3 + c], v111 = C[7 * 3 + c];
-            const float px = v100 - v000, py = v010 - v000, pz = v001 - v000;
-            const float d1 = v110 - v010, d2 = v101 - v001, d3 = v011 - v001, d4 = v111 - v011;
-            const float pxy = d1 - px;
-            C[0 * 3 + c] = v000;
-            C[1 * 3 + c] = px;
-            C[2 * 3 + c] = py;
-            C[3 * 3 + c] = pxy;
-            C[4 * 3 + c] = pz;
-            C[5 * 3 + c] = d2 - px;              // pxz
-            C[6 * 3 + c] = d3 - py;              // pyz
-            C[7 * 3 + c] = (d4 - d2) - pxy;      // pxyz
-        }
-    } else {
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const float v00 = C[0 * 2 + c], v10 = C[1 * 2 + c], v01 = C[2 * 2 + c], v11 = C[3 * 2 + c];
-            const float px = v10 - v00, py = v01 - v00;
-            C[1 * 2 + c] = px;
-            C[2 * 2 + c] = py;
-            C[3 * 2 + c] = (v11 - v01) - px;     // pxy
-        }
-    }
-}
-
-template <int DIM>
-__device__ __forceinline__ void interp(const float* C, const float f[3], float out[3]);
-
-template <int DIM>
-__device__ __forceinline__ void poly_eval(const float* P, const float f[3], float out[3]) {
-    if constexpr (!LAG_POLY) { interp<DIM>(P, f, out); return; }
-    if constexpr (DIM == 3) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const float a = fmaf(f[2], P[7 * 3 + c], P[3 * 3 + c]);   // pxy + fz pxyz
-            float b = fmaf(f[1], a, P[1 * 3 + c]);                    // px + fy (...)
-            b = fmaf(f[2], P[5 * 3 + c], b);                          //    + fz pxz
-            const float t = fmaf(f[2], P[6 * 3 + c], P[2 * 3 + c]);   // py + fz pyz
-            float r = fmaf(f[2], P[4 * 3 + c], P[0 * 3 + c]);         // p0 + fz pz
-            r = fmaf(f[1], t, r);
-            out[c] = fmaf(f[0], b, r);
-        }
-    } else {
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const float b = fmaf(f[1], P[3 * 2 + c], P[1 * 2 + c]);   // px + fy pxy
-            const float r = fmaf(f[1], P[2 * 2 + c], P[0 * 2 + c]);   // p0 + fy py
-            out[c] = fmaf(f[0], b, r);
-        }
-        out[2] = 0.f;
-    }
-}
-
-// Cell of a stage sample e (displacement from g, cell units):
-// c = g + floor(e), f = e - floor(e) (exact).  Fast path: every axis inside
-// the range [lo_, lo_ + span_] (one unsigned compare per axis).
 // floor(e) on the FMA pipe (no FRND): for |e| < 2^22, e + 1.5*2^23 rounded
 // toward -inf is 1.5*2^23 + floor(e) exactly, so its bits hold floor(e) in
 // the low mantissa (bits - 0x4B400000 = floor(e)) and t - 1.5*2^23 is floor(e).
+constexpr int kMagicBits = 0x4B400000;    // bits of 12582912.0f = 1.5 * 2^23
 __device__ __forceinline__ float floor_fma(float e, int& bits) {
     const float t = __fadd_rd(e, 12582912.0f);
     bits = __float_as_int(t);
     return t - 12582912.0f;
-}
-
-template <int DIM>
-__device__ __forceinline__ bool cells(const int g[3], const float e[3], const int32_t* rmin,
-                                      const int32_t* rspan, int c[3], float f[3]) {
-    bool ok = true;
-#pragma unroll
-    for (int ax = 0; ax < DIM; ++ax) {
-        int tb;
-        const float fl = floor_fma(e[ax], tb);
-        f[ax] = e[ax] - fl;                              // exact
-        c[ax] = g[ax] + (tb - 0x4B400000);
-        ok &= (unsigned)(c[ax] - rmin[ax]) <= (unsigned)rspan[ax];
-    }
-    if constexpr (DIM == 2) { c[2] = 0; f[2] = 0.f; }
-    return ok;
 }
 
 // Slow path (a sample near a block or global face): full classification with
@@ -279,7 +99,7 @@ __device__ __forceinline__ bool cells(const int g[3], const float e[3], const in
 //          COMM flags a gather outside the ghost layers.
 template <int DIM, bool BTO>
 __device__ __forceinline__ uint8_t classify_slow(const AdvectArgs& a, int c[3], float f[3],
-                                              bool& ghost_bad) {
+                                                 bool& ghost_bad) {
     bool out_dom = false, out_blk = false;
 #pragma unroll
     for (int ax = 0; ax < DIM; ++ax) {
@@ -303,41 +123,10 @@ __device__ __forceinline__ uint8_t classify_slow(const AdvectArgs& a, int c[3], 
     return ST_VALID;
 }
 
-// Biased form used on the hot path: gb = g - rmin - bits(1.5*2^23) per
-// axis (per particle, once), so v = c - rmin is one add of the floor's float
-// bits and the range test one unsigned compare.
-constexpr int kMagicBits = 0x4B400000;    // bits of 12582912.0f = 1.5 * 2^23
-template <int DIM>
-__device__ __forceinline__ bool cells_b(const int gb[3], const float e[3], const int32_t* rspan,
-                                        int v[3], float f[3]) {
-    bool ok = true;
-#pragma unroll
-    for (int ax = 0; ax < DIM; ++ax) {
-        int tb;
-        const float fl = floor_fma(e[ax], tb);
-        f[ax] = e[ax] - fl;                              // exact
-        v[ax] = gb[ax] + tb;                             // = c - rmin (|e| < 2^22)
-        ok &= (unsigned)v[ax] <= (unsigned)rspan[ax];
-    }
-    if constexpr (DIM == 2) { v[2] = 0; f[2] = 0.f; }
-    return ok;
-}
-
-// Node index (local slice coordinates) of the cell with gather offsets v.
-template <int DIM>
-__device__ __forceinline__ int vindex(const AdvectArgs& a, const int v[3]) {
-    if constexpr (DIM == 3) return v[0] + a.sx * v[1] + a.sxy * v[2] + a.gidx0;
-    else return v[0] + a.sx * v[1] + a.gidx0;
-}
-
-// Slow path on gather offsets: convert to cells, classify, convert back.
+// Slow path on gather offsets v = c - gmin: convert to cells, classify, convert back.
 template <int DIM, bool BTO>
 __device__ __forceinline__ uint8_t classify_slow_v(const AdvectArgs& a, int v[3], float f[3],
-                                                   bool& ghost_bad);
-
-template <int DIM, bool BTO>
-__device__ __forceinline__ uint8_t classify_slow_v(const AdvectArgs& a, int v[3], float f[3],
-                                                   bool& ghost_bad) {
+                                                bool& ghost_bad) {
     int c[3];
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) c[ax] = v[ax] + a.gmin[ax];
@@ -347,48 +136,11 @@ __device__ __forceinline__ uint8_t classify_slow_v(const AdvectArgs& a, int v[3]
     return st;
 }
 
-// Stage sample s >= 2 relative to the stage-1 cell: fs = f1 + beta dt k (cell
-// units from the stage-1 cell origin).  fs in [0, 1) on every axis (one
-// unsigned compare of the float bits per axis: negatives have the sign bit)
-// means the stage-1 cell, which the committed position already validated, so
-// nothing else is tested.  Otherwise the sample's cell v1 + floor(fs) takes
-// the fast-range test and, outside it, the full classification.  Returns the
-// node index of the cell to interpolate in (f = fractions inside it).
-template <int DIM, bool BTO>
-__device__ __forceinline__ int stage_cell(const AdvectArgs& a, const int v1[3], int idx1,
-                                          const float fs[3], bool test, uint8_t& st,
-                                          bool& ghost_bad, float f[3]) {
-    bool same = true;
-#pragma unroll
-    for (int ax = 0; ax < DIM; ++ax) {
-        f[ax] = fs[ax];
-        same &= __float_as_uint(fs[ax]) < 0x3F800000u;
-    }
-    if constexpr (DIM == 2) f[2] = 0.f;
-    int idx = idx1;
-    if (!same && test) {
-        int v[3];
-        bool ok = true;
-#pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) {
-            int tb;
-            const float fl = floor_fma(fs[ax], tb);
-            f[ax] = fs[ax] - fl;                                   // exact
-            v[ax] = v1[ax] + (tb - 0x4B400000);
-            ok &= (unsigned)v[ax] <= (unsigned)a.gspan[ax];
-        }
-        if constexpr (DIM == 2) v[2] = 0;
-        if (!ok) st = classify_slow_v<DIM, BTO>(a, v, f, ghost_bad);
-        idx = vindex<DIM>(a, v);
-    }
-    return idx;
-}
-
+// Node index (local slice coordinates) of the cell with gather offsets v.
 template <int DIM>
-__device__ __forceinline__ int node_index(const AdvectArgs& a, const int c[3]) {
-    const int lx = c[0] - a.base[0], ly = c[1] - a.base[1];
-    if constexpr (DIM == 3) return lx + a.sx * ly + a.sxy * (c[2] - a.base[2]);
-    else return lx + a.sx * ly;
+__device__ __forceinline__ int vindex(const AdvectArgs& a, const int v[3]) {
+    if constexpr (DIM == 3) return v[0] + a.sx * v[1] + a.sxy * v[2] + a.gidx0;
+    else return v[0] + a.sx * v[1] + a.gidx0;
 }
 
 // ---------------------------------------------------------------------------
@@ -441,12 +193,6 @@ template <int DIM> struct Pairs { static constexpr int n = (1 << (DIM - 1)) * DI
 template <int DIM>
 __device__ __forceinline__ void gather_pairs(const float* __restrict__ v, int idx, int sx, int sxy,
                                              f2_t* P) {
-#ifdef LAG_EXP_NOLOAD   // timing experiment: synthetic corners, no velocity traffic
-#pragma unroll
-    for (int i = 0; i < Pairs<DIM>::n; ++i)
-        P[i] = f2_pack(__int_as_float(idx + i) * 1e-30f, __int_as_float(idx - i) * 1e-30f);
-    return;
-#endif
     const float* p = v + DIM * idx;
 #pragma unroll
     for (int r = 0; r < (1 << (DIM - 1)); ++r) {
@@ -487,53 +233,218 @@ __device__ __forceinline__ void interp_pairs(const f2_t* P, const float f[3], fl
     if constexpr (DIM == 2) out[2] = 0.f;
 }
 
-// Corner gather by linear node index (see gather()).
+// "in the stage-1 cell": fs in [0, 1) on every axis.  Non-negative floats
+// order like their bits and negatives have the sign bit, so one unsigned
+// compare of the largest bit pattern decides (NaN and inf fail it too).
 template <int DIM>
-__device__ __forceinline__ void gather_idx(const float* __restrict__ v, int idx, int sx, int sxy,
-                                           float* C) {
-#ifdef LAG_EXP_NOLOAD   // timing experiment: synthetic corners, no velocity traffic
+__device__ __forceinline__ bool in_unit_cell(const float fs[3]) {
+    uint32_t m = max(__float_as_uint(fs[0]), __float_as_uint(fs[1]));
+    if constexpr (DIM == 3) m = max(m, __float_as_uint(fs[2]));
+    return m < 0x3F800000u;
+}
+
+// A stage sample that left the stage-1 cell (rare): its cell v1 + floor(fs),
+// fractions, the fast-range test and, outside it, the full classification.
+// Latches non-finite samples (non-finite velocity reached the particle).
+template <int DIM, bool BTO>
+__device__ __forceinline__ int stage_moved(const AdvectArgs& a, const int v1[3], const float fs[3],
+                                        uint8_t& st, bool& ghost_bad, uint32_t& errbits, float f[3]) {
+    int v[3] = {0, 0, 0};
+    bool ok = true, finite = true;
 #pragma unroll
-    for (int i = 0; i < (1 << DIM) * DIM; ++i) C[i] = __int_as_float(idx + i) * 1e-30f;
-    return;
-#endif
-    if constexpr (DIM == 3) {
-        const float* p = v + 3 * idx;
+    for (int ax = 0; ax < DIM; ++ax) {
+        int tb;
+        const float fl = floor_fma(fs[ax], tb);
+        f[ax] = fs[ax] - fl;                                   // exact
+        v[ax] = v1[ax] + (tb - kMagicBits);
+        ok &= (unsigned)v[ax] <= (unsigned)a.gspan[ax];
+        finite &= fabsf(fs[ax]) < 4194304.f;                   // 2^22 cells
+    }
+    if constexpr (DIM == 2) f[2] = 0.f;
+    if (!finite) {
+        errbits |= ERR_NONFINITE;
+        st = ST_EXIT;
+        return 0;
+    }
+    if (!ok) st = classify_slow_v<DIM, BTO>(a, v, f, ghost_bad);
+    if constexpr (!BTO) {
+        // overlap pass 1 (LAG_XCHG_PEER_OVERLAP): the tile was judged
+        // ghost-free from its stage-1 cells, which holds while samples stay
+        // within one cell of them (CFL < 1); a farther sample may read ghost
+        // nodes the exchange CTAs are writing: latched as a ghost error
+        if (a.pass == 1) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int dy = r & 1, dz = r >> 1;
-            const float* q = p + 3 * (dy * sx + dz * sxy);
-#pragma unroll
-            for (int e = 0; e < 6; ++e) C[r * 6 + e] = __ldg(q + e);
-        }
-    } else {
-        const float* p = v + 2 * idx;
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const float* q = p + 2 * (r * sx);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) C[r * 4 + e] = __ldg(q + e);
+            for (int ax = 0; ax < DIM; ++ax) ghost_bad |= (unsigned)(v[ax] - v1[ax] + 1) > 2u;
         }
     }
+    return vindex<DIM>(a, v);
+}
+
+// One stage s >= 2 of the RK4 step for the lane's particle: the sample
+// fs = f1 + beta dt k (cell units from the stage-1 cell origin).  In the
+// common case every lane's sample lies in its stage-1 cell and the corner
+// cache holds that cell: nothing to do (one vote).  Otherwise the lanes that
+// left the cell, or whose cache holds another cell, locate their sample and
+// reload the cache (both slices for stages 2-3, v_t1 only for stage 4).
+template <int DIM, bool BTO, bool FROZEN, int SLICES>
+__device__ __forceinline__ void stage_locate(const AdvectArgs& a, bool active, const int v1[3], int idx1,
+                                             const float fs[3], int& cur, uint8_t& st, bool& ghost_bad,
+                                             uint32_t& errbits, float f[3], f2_t* S, f2_t* B) {
+    constexpr int NP = Pairs<DIM>::n;
+    const bool same = in_unit_cell<DIM>(fs);
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) f[ax] = fs[ax];
+    const bool need = active && st == ST_VALID && (!same || cur != idx1);
+    if (__any_sync(0xffffffffu, need)) {
+        if (need) {
+            int idx = idx1;
+            if (!same) idx = stage_moved<DIM, BTO>(a, v1, fs, st, ghost_bad, errbits, f);
+            LAG_CHECK_GATHER(a, idx, st == ST_VALID);
+            if (st == ST_VALID && idx != cur) {
+                if constexpr (SLICES == 2) {
+                    gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
+                    if constexpr (FROZEN) {
+#pragma unroll
+                        for (int i = 0; i < NP; ++i) B[i] = S[i];
+                    } else {
+                        gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
+                    }
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
+                } else {
+                    gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
+                }
+                cur = idx;
+            }
+        }
+    }
+}
+
+// Rare per-tile work after the update (warp-uniform branch): membership of
+// the updated position for lanes outside the fast block range (BTO: TERM or
+// EXIT; COMM: hand-off or EXIT), non-finite updates, compaction with holes,
+// termination records and COMM hand-offs.  Returns the new live count.
+template <int DIM, bool BTO>
+__device__ __forceinline__ int tile_slow(const AdvectArgs& a, float4* trec, int lane, bool live, bool inblk,
+                                      const int g[3], const float4 r, const float dn[3], uint8_t st,
+                                      bool ghost_bad, uint32_t& errbits, uint32_t& nterm,
+                                      uint32_t& nexit, uint32_t& nsent, bool& did_remote) {
+    bool migrate = false;
+    int nb = 0;
+    if (live && st == ST_VALID) {
+        bool finite = true;
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax) finite &= fabsf(dn[ax]) < 4194304.f;   // 2^22 cells
+        if (!finite) {
+            errbits |= ERR_NONFINITE;
+            st = ST_EXIT;
+        } else if (!inblk) {
+            int cn[3] = {0, 0, 0};
+            float fn[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+            for (int ax = 0; ax < DIM; ++ax) {
+                int tb;
+                const float fl = floor_fma(dn[ax], tb);
+                fn[ax] = dn[ax] - fl;
+                cn[ax] = g[ax] + (tb - kMagicBits);
+            }
+            bool gdummy = false;
+            if constexpr (BTO) {
+                st = classify_slow<DIM, true>(a, cn, fn, gdummy);
+            } else {
+                // COMM: in the domain but outside the block -> hand off
+                bool out_dom = false;
+                int mul = 1;
+#pragma unroll
+                for (int ax = 0; ax < DIM; ++ax) {
+                    out_dom |= (cn[ax] < 0) | (cn[ax] > a.N[ax] - 1) |
+                               ((cn[ax] == a.N[ax] - 1) & (fn[ax] != 0.f));
+                    const int o = (cn[ax] < a.lo[ax]) ? -1
+                                  : ((cn[ax] >= a.hi[ax] && a.hi[ax] < a.N[ax]) ? 1 : 0);
+                    migrate |= (o != 0);
+                    nb += (o + 1) * mul;
+                    mul *= 3;
+                }
+                if constexpr (DIM == 2) nb += 9;     // offset index (ox+1) + 3(oy+1) + 9(oz+1), oz = 0
+                if (out_dom) { st = ST_EXIT; migrate = false; }
+            }
+        }
+    }
+    if (live && ghost_bad) { errbits |= ERR_GHOST; if (st == ST_VALID) st = ST_EXIT; migrate = false; }
+
+    const bool keep = live && st == ST_VALID && !migrate;
+    const unsigned kmask = __ballot_sync(0xffffffffu, keep);
+    const unsigned dmask = __ballot_sync(0xffffffffu, live && st != ST_VALID);
+    const unsigned tmask = __ballot_sync(0xffffffffu, live && st == ST_TERM);
+    __syncwarp();
+    if (keep) {
+        const int pos = __popc(kmask & ((1u << lane) - 1u));
+        trec[pos] = make_float4(dn[0], dn[1], dn[2], r.w);
+    }
+    if constexpr (!BTO) {
+        const unsigned mmask = __ballot_sync(0xffffffffu, migrate);
+        if (migrate) {
+            const unsigned peers = __match_any_sync(mmask, nb);
+            const int leader = __ffs(peers) - 1;
+            float4* sb = a.slot_ptr[nb];
+            uint32_t base0 = 0;
+            if (lane == leader) base0 = atomicAdd(reinterpret_cast<uint32_t*>(sb), (uint32_t)__popc(peers));
+            base0 = __shfl_sync(peers, base0, leader);
+            const uint32_t pos = base0 + __popc(peers & ((1u << lane) - 1u));
+            if (pos < (uint32_t)a.slot_capv[nb])
+                sb[1 + pos] = make_float4(dn[0], dn[1], dn[2], r.w);
+            else
+                errbits |= ERR_OVERFLOW;
+            did_remote = true;
+        }
+        if (lane == 0) nsent += __popc(mmask);
+    }
+    if (dmask) {
+        uint32_t slot0 = 0;
+        if (lane == 0) slot0 = atomicAdd(a.dead_count, (uint32_t)__popc(dmask));
+        slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+        if (live && st != ST_VALID) {
+            const uint32_t s = slot0 + __popc(dmask & ((1u << lane) - 1u));
+            if (s < a.dead_cap) {
+                a.dead_rec[s] = r;                   // pre-step position
+                a.dead_info[s] = ((uint32_t)st << 24) | (uint32_t)(a.cycle & 0xffffff);
+            } else {
+                errbits |= ERR_OVERFLOW;
+            }
+        }
+    }
+    if (lane == 0) {
+        nterm += __popc(tmask);
+        nexit += __popc(dmask) - __popc(tmask);
+    }
+    return __popc(kmask);
 }
 
 // The advect loop over a virtual grid of `ncta` CTAs (this CTA = `cta`):
 // advect_kernel runs it on the whole grid; the COMM overlap pass 1
 // (advect_xchg_kernel, lag_api.cu) on the CTAs after its exchange CTAs.
+// Persistent: warp w owns tiles w, w + W, w + 2W, ... (W = all warps), so the
+// GPU sweeps the particle list as one compact window (L2-friendly).
+//
+// The common path is straight-line: every sample in its stage-1 cell, the
+// updated position inside the block, every live particle kept.  Anything
+// else (a cell change, a face, a termination, a hand-off) is detected by one
+// warp vote and handled out of line (stage_locate, tile_slow).
 template <int DIM, bool BTO, bool FROZEN>
 __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, const int ncta) {
-    constexpr int NC = (1 << DIM) * DIM;             // corner floats per slice
+    constexpr int NP = Pairs<DIM>::n;
     const int lane = threadIdx.x & 31;
     const int warp = (cta * kThreads + threadIdx.x) >> 5;
-    int n_tiles_all = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
+    int n_tiles = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
     // overlap passes (COMM): loop over virtual tile indices, map to real tiles
     int n_def = 0, n_b = 0;
     if constexpr (!BTO) {
         if (a.pass == 1) {
-            n_tiles_all = (int)*a.n_tiles_b;
+            n_tiles = (int)*a.n_tiles_b;
         } else if (a.pass == 2) {
             n_def = (int)*a.defer_count;
             n_b = (int)*a.n_tiles_b;
-            n_tiles_all = n_def + (n_tiles_all - n_b);
+            n_tiles = n_def + (n_tiles - n_b);
         }
     }
     auto real_tile = [&](int v) -> int {
@@ -542,31 +453,15 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         }
         return v;
     };
-    // non-persistent grid: warp w owns tiles [w*tpw, (w+1)*tpw) (contiguous, so
-    // a CTA's particles are spatial neighbours); the block scheduler balances
-    // the load across SMs
-#if LAG_ADV_PERSIST
-    // persistent grid: warp w owns tiles w, w + W, w + 2W, ... (W = all warps),
-    // so the GPU sweeps the particle list as one compact window
-    const int tile0 = warp;
     const int tstride = (ncta * kThreads) >> 5;
-    const int n_tiles = n_tiles_all;
-#else
-    const int tile0 = warp * a.tiles_per_warp;
-    const int tstride = 1;
-    const int n_tiles = min(n_tiles_all, tile0 + a.tiles_per_warp);
-#endif
 
     uint32_t steps = 0, nterm = 0, nexit = 0, nsent = 0;  // per warp and launch: < 2^32
     uint32_t errbits = 0;
     bool did_remote = false;
-#ifdef LAG_EXP_TIMELINE
-    if (a.tl && cta == 0 && threadIdx.x == 0) a.tl[(a.sig_value & 63) * 8 + 6] = lag_gtimer();
-#endif
 
-    // software pipeline: the next tile's count and records are in flight while
+    // software pipeline: the next tile's count and record are in flight while
     // the current tile computes
-    int tile = tile0;                         // virtual index (== real outside overlap pass 2)
+    int tile = warp;                          // virtual index (== real outside overlap pass 2)
     int rtile = tile < n_tiles ? real_tile(tile) : 0;
     int cnt = tile < n_tiles ? a.tile_count[rtile] : 0;
     float4 r = tile < n_tiles ? a.state[(size_t)rtile * kTile + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -580,28 +475,35 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         if (cnt == 0) { tile = ntile; rtile = nrtile; cnt = ncnt; r = nr; continue; }
         const bool live = lane < cnt;
         float4* trec = a.state + (size_t)rtile * kTile;
-        int g[3];
-        unpack_g(__float_as_uint(r.w), a, g);
+        const uint32_t w = __float_as_uint(r.w);
+        const int g[3] = {(int)(w & a.mx), (int)((w >> a.bx) & a.my), DIM == 3 ? (int)(w >> (a.bx + a.by)) : 0};
         const float d[3] = {r.x, r.y, DIM == 3 ? r.z : 0.f};
 
-        constexpr int NP = Pairs<DIM>::n;
         f2_t S[NP], B[NP];
-        int c[3];
-        float f[3], e[3];
         bool ghost_bad = false;
         uint8_t st = ST_VALID;
 
         // ---- stage 1: q1 = x (validated when committed) ----
-        int gb[3];                            // g - gmin - magic (see cells_b)
+        // gather offsets v = g + floor(d) - gmin; one unsigned compare per axis
+        int v1c[3] = {0, 0, 0};
+        float f1[3] = {0.f, 0.f, 0.f};
+        bool ok1 = true;
 #pragma unroll
-        for (int ax = 0; ax < 3; ++ax) gb[ax] = g[ax] - a.gmin[ax] - kMagicBits;
-        if (!cells_b<DIM>(gb, d, a.gspan, c, f) && live)
-            classify_slow_v<DIM, BTO>(a, c, f, ghost_bad);   // top-face clamp only
+        for (int ax = 0; ax < DIM; ++ax) {
+            int tb;
+            const float fl = floor_fma(d[ax], tb);
+            f1[ax] = d[ax] - fl;                             // exact
+            v1c[ax] = g[ax] + tb - (a.gmin[ax] + kMagicBits);
+            ok1 &= (unsigned)v1c[ax] <= (unsigned)a.gspan[ax];
+        }
+        if (__any_sync(0xffffffffu, live && !ok1)) {         // closed top face: clamp (rare)
+            if (live && !ok1) classify_slow_v<DIM, BTO>(a, v1c, f1, ghost_bad);
+        }
         if constexpr (!BTO) {
             if (a.pass == 1) {                // a sample could reach a ghost node: after the exchange
                 bool safe = true;
 #pragma unroll
-                for (int ax = 0; ax < DIM; ++ax) safe &= (unsigned)(c[ax] - a.smin[ax]) <= (unsigned)a.sspan[ax];
+                for (int ax = 0; ax < DIM; ++ax) safe &= (unsigned)(v1c[ax] - a.smin[ax]) <= (unsigned)a.sspan[ax];
                 if (__any_sync(0xffffffffu, live && !safe)) {
                     if (lane == 0) a.defer_list[atomicAdd(a.defer_count, 1u)] = (uint32_t)rtile;
                     tile = ntile; rtile = nrtile; cnt = ncnt; r = nr;
@@ -609,136 +511,55 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
                 }
             }
         }
-        int cur = vindex<DIM>(a, c);
-        LAG_CHECK_GATHER(a, cur, live);
-        if (!live) cur = 0;
-        const int idx1 = cur;                 // stage-1 cell: offsets, fractions
-        const int v1c[3] = {c[0], c[1], c[2]};
-        const float f1[3] = {f[0], f[1], f[2]};
+        const int idx1 = live ? vindex<DIM>(a, v1c) : 0;     // stage-1 cell origin (node index)
+        LAG_CHECK_GATHER(a, idx1, live);
+        int cur = idx1;                                      // cell held by the corner cache
         float k1[3];
         if (__all_sync(0xffffffffu, !live || ((d[0] == 0.f) & (d[1] == 0.f) & (d[2] == 0.f)))) {
             // every particle sits on its seed node (first cycle of an interval):
             // the trilinear value at a node is the node value (f = 0, or f = 1
-            // on a clamped top face) — 3 loads; the stage-2 sample gathers its
-            // own cell (cur = -1 forces it)
+            // on a clamped top face) — 3 loads; stage 2 gathers its own cell
+            // (cur = -1 forces it)
             int node[3];
 #pragma unroll
-            for (int ax = 0; ax < 3; ++ax) node[ax] = c[ax] + (f[ax] != 0.f ? 1 : 0);
+            for (int ax = 0; ax < 3; ++ax) node[ax] = v1c[ax] + (f1[ax] != 0.f ? 1 : 0);
             const float* pv = a.v0 + DIM * (live ? vindex<DIM>(a, node) : 0);
 #pragma unroll
             for (int ax = 0; ax < DIM; ++ax) k1[ax] = __ldg(pv + ax);
             if constexpr (DIM == 2) k1[2] = 0.f;
             cur = -1;
-#pragma unroll
-            for (int i = 0; i < NP; ++i) S[i] = B[i] = 0ull;   // lanes stopped at stage 2 stay finite
         } else {
-            gather_pairs<DIM>(a.v0, cur, a.sx, a.sxy, S);
+            gather_pairs<DIM>(a.v0, idx1, a.sx, a.sxy, S);
             if constexpr (FROZEN) {
 #pragma unroll
                 for (int i = 0; i < NP; ++i) B[i] = S[i];
             } else {
-                gather_pairs<DIM>(a.v1, cur, a.sx, a.sxy, B);
+                gather_pairs<DIM>(a.v1, idx1, a.sx, a.sxy, B);
             }
-            interp_pairs<DIM>(S, f, k1);
+            interp_pairs<DIM>(S, f1, k1);
 #pragma unroll
             for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);   // S = v0 + v1 (stages 2, 3)
         }
 
+        float e[3], f[3];
         // ---- stage 2: q2 = x + dt/2 k1, alpha = 1/2 ----
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], k1[ax], f1[ax]);
-        {
-            const int idx = stage_cell<DIM, BTO>(a, v1c, idx1, e, live, st, ghost_bad, f);
-            LAG_CHECK_GATHER(a, idx, live && st == ST_VALID);
-#ifdef LAG_EXP_NORELOAD
-            if (false) {
-#else
-            if (live && st == ST_VALID && idx != cur) {
-#endif
-                gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
-                if constexpr (FROZEN) {
-#pragma unroll
-                    for (int i = 0; i < NP; ++i) B[i] = S[i];
-                } else {
-                    gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
-                }
-#pragma unroll
-                for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
-                cur = idx;
-            }
-        }
+        for (int ax = 0; ax < 3; ++ax) e[ax] = ax < DIM ? fmaf(a.hdth[ax], k1[ax], f1[ax]) : 0.f;
+        stage_locate<DIM, BTO, FROZEN, 2>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
         float T2[3];
         interp_pairs<DIM>(S, f, T2);                          // T2 = 2 k2
-#if LAG_PREFETCH
-        // the next tile's stage-1 corner rows (its record arrived by now): one
-        // prefetch per row and slice, so its gathers hit the cache
-        if (ntile < n_tiles && lane < ncnt) {
-            int gn[3];
-            unpack_g(__float_as_uint(nr.w), a, gn);
-            const float dn0[3] = {nr.x, nr.y, DIM == 3 ? nr.z : 0.f};
-            int vn[3];
-            bool okn = true;
-#pragma unroll
-            for (int ax = 0; ax < DIM; ++ax) {
-                vn[ax] = gn[ax] - a.gmin[ax] + (__float_as_int(floorf(dn0[ax]) + 12582912.0f) - kMagicBits);
-                okn &= (unsigned)vn[ax] <= (unsigned)a.gspan[ax];
-            }
-            if constexpr (DIM == 2) vn[2] = 0;
-            if (okn) {
-                const int in = vindex<DIM>(a, vn);
-#pragma unroll
-                for (int r = 0; r < (1 << (DIM - 1)); ++r) {
-                    const int o = DIM * (in + (r & 1) * a.sx + (r >> 1) * a.sxy);
-#if LAG_PREFETCH == 1
-                    asm volatile("prefetch.global.L2 [%0];" :: "l"(a.v0 + o));
-                    if constexpr (!FROZEN) asm volatile("prefetch.global.L2 [%0];" :: "l"(a.v1 + o));
-#else
-                    asm volatile("prefetch.global.L1 [%0];" :: "l"(a.v0 + o));
-                    if constexpr (!FROZEN) asm volatile("prefetch.global.L1 [%0];" :: "l"(a.v1 + o));
-#endif
-                }
-            }
-        }
-#endif
 
         // ---- stage 3: q3 = x + dt/2 k2 = x + dt/4 T2, alpha = 1/2 ----
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.qdth[ax], T2[ax], f1[ax]);
-        {
-            const int idx = stage_cell<DIM, BTO>(a, v1c, idx1, e, live && st == ST_VALID, st, ghost_bad, f);
-            LAG_CHECK_GATHER(a, idx, live && st == ST_VALID);
-#ifdef LAG_EXP_NORELOAD
-            if (false) {
-#else
-            if (live && st == ST_VALID && idx != cur) {
-#endif
-                gather_pairs<DIM>(a.v0, idx, a.sx, a.sxy, S);
-                if constexpr (FROZEN) {
-#pragma unroll
-                    for (int i = 0; i < NP; ++i) B[i] = S[i];
-                } else {
-                    gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
-                }
-#pragma unroll
-                for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);
-                cur = idx;
-            }
-        }
+        for (int ax = 0; ax < 3; ++ax) e[ax] = ax < DIM ? fmaf(a.qdth[ax], T2[ax], f1[ax]) : 0.f;
+        stage_locate<DIM, BTO, FROZEN, 2>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
         float T3[3];
         interp_pairs<DIM>(S, f, T3);                          // T3 = 2 k3
 
         // ---- stage 4: q4 = x + dt k3 = x + dt/2 T3, alpha = 1 ----
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) e[ax] = fmaf(a.hdth[ax], T3[ax], f1[ax]);
-        {
-            const int idx = stage_cell<DIM, BTO>(a, v1c, idx1, e, live && st == ST_VALID, st, ghost_bad, f);
-            LAG_CHECK_GATHER(a, idx, live && st == ST_VALID);
-#ifndef LAG_EXP_NORELOAD
-            if (live && st == ST_VALID && idx != cur) {
-                gather_pairs<DIM>(a.v1, idx, a.sx, a.sxy, B);
-            }
-#endif
-        }
+        for (int ax = 0; ax < 3; ++ax) e[ax] = ax < DIM ? fmaf(a.hdth[ax], T3[ax], f1[ax]) : 0.f;
+        stage_locate<DIM, BTO, FROZEN, 1>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
         float k4[3];
         interp_pairs<DIM>(B, f, k4);
 
@@ -748,95 +569,27 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         for (int ax = 0; ax < DIM; ++ax)
             dn[ax] = fmaf(a.sdth[ax], (k1[ax] + k4[ax]) + (T2[ax] + T3[ax]), d[ax]);
         if constexpr (DIM == 2) dn[2] = 0.f;
-        bool finite = true;
+        // membership of the updated position: g + floor(dn) in the fast block
+        // range (non-finite or huge dn fails the compare too)
+        bool inblk = true;
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) finite &= fabsf(dn[ax]) < 4194304.f;   // 2^22 cells
-        // membership of the updated position: fast = inside the block
-        bool migrate = false;
-        int nb = 0;
-        {
-            int cn[3];
-            float fn[3];
-            int gbb[3];                       // g - bmin - magic
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) gbb[ax] = BTO ? gb[ax] : g[ax] - a.bmin[ax] - kMagicBits;
-            const bool inblk = cells_b<DIM>(gbb, dn, a.bspan, cn, fn);
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) cn[ax] += a.bmin[ax];         // back to cells (slow path)
-            if (!inblk && live && st == ST_VALID) {
-                bool gdummy = false;
-                if constexpr (BTO) {
-                    st = classify_slow<DIM, true>(a, cn, fn, gdummy);
-                } else {
-                    // COMM: in the domain but outside the block -> hand off
-                    bool out_dom = false;
-                    int mul = 1;
-#pragma unroll
-                    for (int ax = 0; ax < DIM; ++ax) {
-                        out_dom |= (cn[ax] < 0) | (cn[ax] > a.N[ax] - 1) |
-                                   ((cn[ax] == a.N[ax] - 1) & (fn[ax] != 0.f));
-                        const int o = (cn[ax] < a.lo[ax]) ? -1
-                                      : ((cn[ax] >= a.hi[ax] && a.hi[ax] < a.N[ax]) ? 1 : 0);
-                        migrate |= (o != 0);
-                        nb += (o + 1) * mul;
-                        mul *= 3;
-                    }
-                    if constexpr (DIM == 2) nb += 9;     // offset index (ox+1) + 3(oy+1) + 9(oz+1), oz = 0
-                    if (out_dom) { st = ST_EXIT; migrate = false; }
-                }
-            }
+        for (int ax = 0; ax < DIM; ++ax) {
+            int tb;
+            floor_fma(dn[ax], tb);
+            inblk &= (unsigned)(g[ax] + tb - (a.bmin[ax] + kMagicBits)) <= (unsigned)a.bspan[ax];
         }
-        if (live && !finite) { errbits |= ERR_NONFINITE; st = ST_EXIT; migrate = false; }
-        if (live && ghost_bad) { errbits |= ERR_GHOST; if (st == ST_VALID) st = ST_EXIT; migrate = false; }
 
         // ---- particle management: compact survivors, record terminations ----
-        const bool keep = live && st == ST_VALID && !migrate;
-        const unsigned kmask = __ballot_sync(0xffffffffu, keep);
-        const unsigned dmask = __ballot_sync(0xffffffffu, live && st != ST_VALID);
-        const unsigned tmask = __ballot_sync(0xffffffffu, live && st == ST_TERM);
-        __syncwarp();
-        if (keep) {
-            const int pos = __popc(kmask & ((1u << lane) - 1u));
-            trec[pos] = make_float4(dn[0], dn[1], dn[2], r.w);
+        const bool fast = live && st == ST_VALID && inblk && !ghost_bad;
+        if (__all_sync(0xffffffffu, fast || !live)) {
+            // every live particle kept: in place, the tile count is unchanged
+            if (live) trec[lane] = make_float4(dn[0], dn[1], dn[2], r.w);
+        } else {
+            const int kept = tile_slow<DIM, BTO>(a, trec, lane, live, inblk, g, r, dn, st, ghost_bad, errbits,
+                                                 nterm, nexit, nsent, did_remote);
+            if (lane == 0) a.tile_count[rtile] = (uint8_t)kept;
         }
-        if constexpr (!BTO) {
-            const unsigned mmask = __ballot_sync(0xffffffffu, migrate);
-            if (migrate) {
-                const unsigned peers = __match_any_sync(mmask, nb);
-                const int leader = __ffs(peers) - 1;
-                float4* sb = a.slot_ptr[nb];
-                uint32_t base0 = 0;
-                if (lane == leader) base0 = atomicAdd(reinterpret_cast<uint32_t*>(sb), (uint32_t)__popc(peers));
-                base0 = __shfl_sync(peers, base0, leader);
-                const uint32_t pos = base0 + __popc(peers & ((1u << lane) - 1u));
-                if (pos < (uint32_t)a.slot_capv[nb])
-                    sb[1 + pos] = make_float4(dn[0], dn[1], dn[2], r.w);
-                else
-                    errbits |= ERR_OVERFLOW;
-                did_remote = true;
-            }
-            if (lane == 0) nsent += __popc(mmask);
-        }
-        if (dmask) {
-            uint32_t slot0 = 0;
-            if (lane == 0) slot0 = atomicAdd(a.dead_count, (uint32_t)__popc(dmask));
-            slot0 = __shfl_sync(0xffffffffu, slot0, 0);
-            if (live && st != ST_VALID) {
-                const uint32_t s = slot0 + __popc(dmask & ((1u << lane) - 1u));
-                if (s < a.dead_cap) {
-                    a.dead_rec[s] = r;                   // pre-step position
-                    a.dead_info[s] = ((uint32_t)st << 24) | (uint32_t)(a.cycle & 0xffffff);
-                } else {
-                    errbits |= ERR_OVERFLOW;
-                }
-            }
-        }
-        if (lane == 0) {
-            a.tile_count[rtile] = (uint8_t)__popc(kmask);
-            steps += (uint32_t)cnt;
-            nterm += __popc(tmask);
-            nexit += __popc(dmask) - __popc(tmask);
-        }
+        steps += (uint32_t)cnt;
         tile = ntile; rtile = nrtile; cnt = ncnt; r = nr;
     }
 
@@ -851,15 +604,12 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
     if (lane == 0 && errbits) atomicOr(a.err, errbits);
     if constexpr (!BTO) {
         if (a.n_sig) {
-            if (did_remote) __threadfence_system();          // my remote hand-offs are performed
+            if (__any_sync(0xffffffffu, did_remote)) __threadfence_system();   // my remote hand-offs are performed
             __syncwarp();
             if (lane == 0) {
                 const uint32_t total = (ncta * kThreads) >> 5;
                 if (atomicAdd(a.done_warps, 1u) == total - 1) {  // last warp of the grid
                     *a.done_warps = 0u;
-#ifdef LAG_EXP_TIMELINE
-                    if (a.tl) a.tl[(a.sig_value & 63) * 8 + 7] = lag_gtimer();
-#endif
                     __threadfence_system();
                     for (int k = 0; k < a.n_sig; ++k)
                         *reinterpret_cast<volatile unsigned long long*>(a.sig_flag[k]) = a.sig_value;
@@ -879,17 +629,11 @@ advect_kernel(const AdvectArgs a) {
 // ---------------------------------------------------------------------------
 // seeding: lattice nodes g = first + stride * (ix, iy, iz).
 // Tile order: bricks of (32 x by x bz) seeds, x fastest inside a tile, tiles
-// of a brick consecutive (rows ry fastest, then rz), bricks x-fastest.  A CTA
-// of by*bz warps then advects one brick at a time, so the node rows its
-// corner gathers share stay in that SM's L1 (a row of nodes serves the
-// particle rows on both sides of it).  Tiles past a ragged edge are partial
-// or empty (count 0).  by = bz = 1 is plain x-fastest row order.
-#ifndef LAG_BRICK_Y
-#define LAG_BRICK_Y 1
-#endif
-#ifndef LAG_BRICK_Z
-#define LAG_BRICK_Z 1
-#endif
+// of a brick consecutive (rows ry fastest, then rz), bricks x-fastest, so
+// the warps sweeping consecutive tiles share node rows in L1/L2 (a row of
+// nodes serves the particle rows on both sides of it).  Tiles past a ragged
+// edge are partial or empty (count 0).  by = bz = 1 is plain x-fastest row
+// order (2-D).
 struct SeedArgs {
     float4* state;
     uint8_t* tile_count;

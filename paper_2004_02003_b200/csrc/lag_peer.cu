@@ -58,70 +58,6 @@ namespace lag {
 enum : int { T_INBOX = 0, T_INBOX_PAR = 1, T_OUTBOX = 2, T_HALO = 3, T_RECV = 4, T_SEND = 4 + kOff,
              T_WORDS = 4 + 2 * kOff };
 
-struct PeerArgs {
-    // wait
-    const unsigned long long* my_flags;   // [2][27]
-    int npeers;
-    int back[kMaxPeers];                  // offset index of each peer as seen from me
-    unsigned long long need_halo, need_part;
-    uint32_t* err;
-    long long timeout_cycles;
-    // signal
-    unsigned long long* remote_flags[kMaxPeers];  // neighbour's flags base
-    int my_index_at_peer[kMaxPeers];              // my offset index as seen from the peer
-    int kind;                                     // 0 = halo, 1 = particles
-    unsigned long long value;
-};
-
-__global__ void peer_signal_kernel(PeerArgs a) {
-    const int p = threadIdx.x;
-    if (p >= a.npeers) return;
-    __threadfence_system();                       // prior packs / remote stores visible first
-    volatile unsigned long long* f = a.remote_flags[p] + a.kind * kOff + a.my_index_at_peer[p];
-    *f = a.value;
-    __threadfence_system();
-}
-
-__global__ void peer_wait_kernel(PeerArgs a) {
-    const int p = threadIdx.x;
-    if (p < a.npeers) {
-        const volatile unsigned long long* fh = a.my_flags + 0 * kOff + a.back[p];
-        const volatile unsigned long long* fp = a.my_flags + 1 * kOff + a.back[p];
-        const long long t0 = clock64();
-        while (*fh < a.need_halo || *fp < a.need_part) {
-            if (clock64() - t0 > a.timeout_cycles) { atomicOr(a.err, ERR_XCHG); break; }
-            __nanosleep(200);
-        }
-        __threadfence_system();
-    }
-}
-
-struct PeerUnpackArgs {
-    float* v0;
-    float* v1;
-    const PeerBox* boxes;
-    int nbox;
-    int parity;
-    int sx, sxy, dim;
-    int64_t total;
-};
-
-__global__ void peer_unpack_kernel(PeerUnpackArgs a) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int k = 0;
-        while (k + 1 < a.nbox && a.boxes[k + 1].off <= i) ++k;
-        const PeerBox& b = a.boxes[k];
-        const int64_t j = i - b.off;
-        const int comp = (int)(j % a.dim);
-        const int64_t node = j / a.dim;
-        const int x = (int)(node % b.nx), y = (int)((node / b.nx) % b.ny), z = (int)(node / ((int64_t)b.nx * b.ny));
-        float* dst = b.slice ? a.v1 : a.v0;
-        dst[(int64_t)a.dim * ((b.x0 + x) + (int64_t)a.sx * (b.y0 + y) + (int64_t)a.sxy * (b.z0 + z)) + comp] =
-            b.src[a.parity][b.slice][j];
-    }
-}
-
 __global__ void __launch_bounds__(256) peer_pack_signal_kernel(XchgArgs x) {
     xchg_pack_signal(x, blockIdx.x, gridDim.x);
 }
@@ -150,7 +86,6 @@ struct PeerState {
     unsigned long long seq = 0;
     uint32_t* done_warps = nullptr;           // advect completion counter
     uint32_t* done_ctas = nullptr;            // pack-kernel completion counter
-    unsigned long long* tl = nullptr;         // experiment timeline [64][8]
 };
 
 lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>& prank,
@@ -238,10 +173,6 @@ lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>
     CKC(cudaMalloc(&ps->done_warps, 2 * sizeof(uint32_t)));
     CKC(cudaMemset(ps->done_warps, 0, 2 * sizeof(uint32_t)));
     ps->done_ctas = ps->done_warps + 1;
-#ifdef LAG_EXP_TIMELINE
-    CKC(cudaMalloc(&ps->tl, 64 * 8 * sizeof(unsigned long long)));
-    CKC(cudaMemset(ps->tl, 0, 64 * 8 * sizeof(unsigned long long)));
-#endif
     CKC(cudaMalloc(&ps->d_boxes, sizeof(PeerBox) * std::max<size_t>(1, ps->boxes.size())));
     if (!ps->boxes.empty())
         CKC(cudaMemcpy(ps->d_boxes, ps->boxes.data(), sizeof(PeerBox) * ps->boxes.size(), cudaMemcpyHostToDevice));
@@ -252,27 +183,6 @@ lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>
 
 void lag_peer_destroy(PeerState* ps) {
     if (!ps) return;
-#ifdef LAG_EXP_TIMELINE
-    if (ps->tl) {
-        unsigned long long h[64 * 8];
-        cudaDeviceSynchronize();
-        cudaMemcpy(h, ps->tl, sizeof(h), cudaMemcpyDeviceToHost);
-        // per cycle, µs relative to the pack start: pack_end wp_start wait_done pull_done append_done adv_start adv_end
-        char fn[256];
-        const char* dir = getenv("LAG_TL_DIR");
-        snprintf(fn, sizeof(fn), "%s/tl_%d.txt", dir ? dir : ".", (int)getpid());
-        FILE* f = fopen(fn, "a");
-        for (int c = 0; f && c < 64; ++c) {
-            const unsigned long long* r = h + c * 8;
-            if (!r[0] || !r[7]) continue;
-            fprintf(f, "TL %d %llu", c, r[0]);
-            for (int k = 1; k < 8; ++k) fprintf(f, " %.1f", r[k] ? (double)(long long)(r[k] - r[0]) * 1e-3 : -1.0);
-            fprintf(f, "\n");
-        }
-        if (f) fclose(f);
-        cudaFree(ps->tl);
-    }
-#endif
     for (char* p : ps->remote) if (p) cudaIpcCloseMemHandle(p);
     cudaFree(ps->d_boxes);
     cudaFree(ps->done_warps);
@@ -286,59 +196,6 @@ float4* lag_peer_remote_slot(PeerState* ps, int i, int prank, int pback, int q) 
     return reinterpret_cast<float4*>(ps->remote[i] + t[T_INBOX] + (size_t)q * t[T_INBOX_PAR]) + t[T_RECV + pback];
 }
 
-lag_status lag_peer_signal(lag_ctx_s* ctx, PeerState* ps, const std::vector<int>& prank,
-                           const std::vector<int>& pback, int kind, unsigned long long value) {
-    const int np = (int)prank.size();
-    if (np == 0) return LAG_OK;
-    PeerArgs a{};
-    a.npeers = np;
-    a.kind = kind;
-    a.value = value;
-    for (int i = 0; i < np; ++i) {
-        a.remote_flags[i] = reinterpret_cast<unsigned long long*>(ps->remote[i]);
-        a.my_index_at_peer[i] = pback[i];
-    }
-    peer_signal_kernel<<<1, 32, 0, ctx->stream>>>(a);
-    ++ctx->launches;
-    CKC(cudaGetLastError());
-    return LAG_OK;
-}
-
-lag_status lag_peer_wait(lag_ctx_s* ctx, PeerState* ps, const std::vector<int>& poff,
-                         unsigned long long need_halo, unsigned long long need_part) {
-    const int np = (int)poff.size();
-    if (np == 0) return LAG_OK;
-    PeerArgs a{};
-    a.my_flags = ps->flags;
-    a.npeers = np;
-    for (int i = 0; i < np; ++i) a.back[i] = poff[i];     // the peer writes at its offset index from me
-    a.need_halo = need_halo;
-    a.need_part = need_part;
-    a.err = ctx->words + W_ERR;
-    a.timeout_cycles = 8000000000LL;                      // ~4 s at 2 GHz
-    peer_wait_kernel<<<1, 32, 0, ctx->stream>>>(a);
-    ++ctx->launches;
-    CKC(cudaGetLastError());
-    return LAG_OK;
-}
-
-lag_status lag_peer_unpack(lag_ctx_s* ctx, PeerState* ps, float* v0, float* v1, bool with_v0, int parity) {
-    const int nb = (int)ps->boxes.size() / 2;
-    if (nb == 0) return LAG_OK;
-    PeerUnpackArgs u{};
-    u.v0 = v0; u.v1 = v1;
-    u.boxes = ps->d_boxes;                                // v1 boxes first, then v0 boxes
-    u.nbox = with_v0 ? 2 * nb : nb;
-    u.parity = parity;
-    u.sx = ctx->ext[0]; u.sxy = ctx->ext[0] * ctx->ext[1]; u.dim = ctx->cfg.dim;
-    u.total = (with_v0 ? 2 : 1) * ps->halo_recv_floats;
-    const int blocks = (int)std::min<int64_t>((u.total + 255) / 256, (int64_t)ctx->num_sms * 8);
-    peer_unpack_kernel<<<std::max(1, blocks), 256, 0, ctx->stream>>>(u);
-    ++ctx->launches;
-    CKC(cudaGetLastError());
-    return LAG_OK;
-}
-
 float4* lag_peer_inbox_slot(PeerState* ps, int q, int poff) {
     // my inbox slot (parity q) filled by the neighbour at offset index poff
     const int64_t* t = ps->my_table.data();
@@ -350,7 +207,6 @@ float* lag_peer_outbox(PeerState* ps, int q) { return ps->outbox + (size_t)q * 2
 unsigned long long& lag_peer_seq(PeerState* ps) { return ps->seq; }
 
 uint32_t* lag_peer_done_counter(PeerState* ps) { return ps->done_warps; }
-unsigned long long* lag_peer_timeline(PeerState* ps) { return ps->tl; }
 
 unsigned long long* lag_peer_remote_flag(PeerState* ps, int i, int kind, int pback) {
     return reinterpret_cast<unsigned long long*>(ps->remote[i]) + kind * kOff + pback;
@@ -364,7 +220,7 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
                              const std::vector<int>& poff, const std::vector<int>& pback,
                              unsigned long long need_part, const void* append_args) {
     const int np = (int)poff.size();
-    cudaStream_t st = ctx->xstream ? ctx->xstream : ctx->stream;   // overlap: the side stream
+    cudaStream_t st = ctx->stream;
     XchgArgs x{};
     const unsigned long long seq = ps->seq;
     const int q = (int)(seq & 1);
@@ -393,10 +249,6 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
     x.seq = seq;
     x.do_append = append_args ? 1 : 0;
     x.done_ctas = ps->done_ctas;
-#ifdef LAG_EXP_TIMELINE
-    x.tl = ps->tl;
-    if (ps->tl) cudaMemsetAsync(ps->tl + (seq & 63) * 8, 0, 8 * sizeof(unsigned long long), st);
-#endif
     AppendArgs ap{};
     if (append_args) ap = *reinterpret_cast<const AppendArgs*>(append_args);
     if (ctx->xchg_fused && halo) {           // overlap: the advect kernel's first CTAs run it

@@ -48,18 +48,9 @@ struct XchgArgs {
     int sx, sxy, dim;
     unsigned long long seq;
     int do_append;
-#ifdef LAG_EXP_TIMELINE
-    unsigned long long* tl;
-#endif
 };
 
 __device__ __forceinline__ void xchg_pack_signal(const XchgArgs& x, int cta, int ncta) {
-#ifdef LAG_EXP_TIMELINE
-    if (x.tl && cta == 0 && threadIdx.x == 0) x.tl[(x.seq & 63) * 8 + 0] = lag_gtimer();
-#endif
-#ifdef LAG_EXP_NOPACK
-    if (false)
-#endif
     for (int64_t i = (int64_t)cta * blockDim.x + threadIdx.x; i < x.sfl;
          i += (int64_t)ncta * blockDim.x) {
         int k = 0;
@@ -77,9 +68,6 @@ __device__ __forceinline__ void xchg_pack_signal(const XchgArgs& x, int cta, int
         __threadfence_system();                       // cumulative: orders the CTA's packs
         if (atomicAdd(x.done_ctas, 1u) == (uint32_t)ncta - 1) {   // last CTA: halo(seq) ready
             *x.done_ctas = 0u;
-#ifdef LAG_EXP_TIMELINE
-            if (x.tl) x.tl[(x.seq & 63) * 8 + 1] = lag_gtimer();
-#endif
             __threadfence_system();
             for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(x.halo_flag[p]) = x.seq;
             __threadfence_system();
@@ -88,10 +76,6 @@ __device__ __forceinline__ void xchg_pack_signal(const XchgArgs& x, int cta, int
 }
 
 __device__ __forceinline__ void xchg_wait_pull(const XchgArgs& x, const AppendArgs& ap, int cta, int ncta) {
-#ifdef LAG_EXP_TIMELINE
-    if (x.tl && cta == 0 && threadIdx.x == 0) x.tl[(x.seq & 63) * 8 + 2] = lag_gtimer();
-#endif
-#ifndef LAG_EXP_NOWAIT
     if (threadIdx.x < x.npeers) {
         const volatile unsigned long long* fh = x.my_flags + 0 * kOff + x.back[threadIdx.x];
         const volatile unsigned long long* fp = x.my_flags + 1 * kOff + x.back[threadIdx.x];
@@ -102,14 +86,7 @@ __device__ __forceinline__ void xchg_wait_pull(const XchgArgs& x, const AppendAr
         }
         __threadfence_system();
     }
-#endif
     __syncthreads();
-#ifdef LAG_EXP_TIMELINE
-    if (x.tl && threadIdx.x == 0) atomicMax(x.tl + (x.seq & 63) * 8 + 3, lag_gtimer());
-#endif
-#ifdef LAG_EXP_NOPULL
-    if (false)
-#endif
     // remote loads: 8 in flight per thread (a few CTAs cover the ghost layers
     // when they run inside the advect kernel's pass 1)
     const int64_t step = (int64_t)ncta * blockDim.x;
@@ -140,22 +117,11 @@ __device__ __forceinline__ void xchg_wait_pull(const XchgArgs& x, const AppendAr
         for (int u = 0; u < 8; ++u)
             if (dst[u]) *dst[u] = val[u];
     }
-#ifdef LAG_EXP_TIMELINE
-    __syncthreads();
-    if (x.tl && threadIdx.x == 0) atomicMax(x.tl + (x.seq & 63) * 8 + 4, lag_gtimer());
-#endif
     if (x.do_append) append_body(ap, cta, ncta);                         // hand-offs of cycle seq-1 (all CTAs)
-#ifdef LAG_EXP_TIMELINE
-    __syncthreads();
-    if (x.tl && threadIdx.x == 0) atomicMax(x.tl + (x.seq & 63) * 8 + 5, lag_gtimer());
-#endif
 }
 
 // exchange role of the advect kernel's pass 1 (LAG_XCHG_PEER_OVERLAP)
-#ifndef LAG_XCHG_CTAS
-#define LAG_XCHG_CTAS 48
-#endif
-constexpr int kXchgCtas = LAG_XCHG_CTAS;   // CTAs of kThreads running the exchange
+constexpr int kXchgCtas = 48;   // CTAs of kThreads running the exchange
 struct XchgFused {
     int32_t ncta;                   // CTAs 0..ncta-1 run the exchange; 0 = none
     XchgArgs x;
