@@ -34,7 +34,9 @@
  *     whose block_hi == N owns the closed upper face.  Rank = x-fastest block
  *     index in `layout`.
  *   - Velocity slice arrays (borrowed, read-only in BTO mode): fp32, AoS
- *     (vx, vy[, vz]) per node, x fastest, dense rows.  Extent per axis =
+ *     (vx, vy[, vz]) per node, x fastest; rows dense or padded to
+ *     lag_config.row_pitch_bytes (a padded pitch that is a multiple of 16 B
+ *     makes the rows legal TMA strides).  Extent per axis =
  *     (min(block_hi + 1, N) - block_lo) + 2 * ghost nodes: the owned nodes,
  *     the neighbour's first (shared) node plane when block_hi < N, and `ghost`
  *     layers on every side (allocated even at global faces, never read there).
@@ -57,7 +59,8 @@
 extern "C" {
 #endif
 
-#define LAG_ABI_VERSION 2   /* 2: LAG_ASYNC extract flag, LAG_XCHG_PEER_OVERLAP */
+#define LAG_ABI_VERSION 3   /* 3: lag_extract interval_index, row_pitch_bytes,
+                               LAG_XCHG_LOCAL + lag_local_group */
 
 #if defined(__GNUC__)
 #define LAG_API __attribute__((visibility("default")))
@@ -84,11 +87,17 @@ typedef enum { LAG_BTO = 0, LAG_COMM = 1 } lag_mode;
 typedef enum {
     LAG_XCHG_NCCL = 0,          /* grouped NCCL send/recv before the advect kernel            */
     LAG_XCHG_PEER = 1,          /* the kernels read/write the neighbours' memory (CUDA IPC)   */
-    LAG_XCHG_PEER_OVERLAP = 2   /* LAG_XCHG_PEER fused with the advection: the first CTAs of
+    LAG_XCHG_PEER_OVERLAP = 2,  /* LAG_XCHG_PEER fused with the advection: the first CTAs of
                                    the advect kernel run the exchange while the others
                                    advect the tiles whose stage samples cannot reach a ghost
                                    node; the rest (and the particles received this cycle)
                                    advect in a second pass.  Bitwise equal to the others.  */
+    LAG_XCHG_LOCAL = 3          /* several blocks on ONE device, driven by one host thread
+                                   (lag_local_group): ghost layers are copied straight from
+                                   the neighbours' slice arrays and hand-offs are appended
+                                   from the neighbours' slots, ordered by the group's single
+                                   stream (no NCCL, no flags, no spinning).  Bitwise equal
+                                   to the other transports.                                  */
 } lag_exchange;
 
 /* Per-basis-flow status returned by lag_extract. */
@@ -120,6 +129,10 @@ typedef struct {
     int32_t nranks;              /* COMM: number of ranks = prod(layout)                  */
     int32_t layout[3];           /* COMM: blocks per axis                                 */
     int32_t exchange;            /* COMM transport: lag_exchange                          */
+    int64_t row_pitch_bytes;     /* bytes between consecutive x-rows of the slice arrays;
+                                    0 = dense (dim * 4 * extent_x); else a multiple of
+                                    dim * 4 and >= dim * 4 * extent_x (padding nodes are
+                                    never read).  Plane pitch = row pitch * extent_y.    */
     const void* nccl_id;         /* COMM: 128-byte ncclUniqueId shared by all ranks (from
                                     lag_nccl_unique_id on one rank); NULL for BTO         */
     void*   stream;              /* cudaStream_t the library enqueues on (borrowed);
@@ -142,9 +155,13 @@ typedef struct {
 } lag_stats_t;
 
 /*
- * lag_init — validate the configuration, allocate every device buffer the
- * context needs (particle list, exchange slots, staging) and, in COMM mode,
- * join the NCCL communicator.  Collective in COMM mode (all ranks must call).
+ * lag_init — one context per rank block.  The decomposition is the
+ * simulation's (§2.2: the Lagrangian analysis runs on the data each
+ * rank already holds), so the caller states the block; the library validates
+ * the configuration, allocates every device buffer the context needs
+ * (particle list, exchange slots, staging) and, in COMM mode over NCCL or
+ * peer memory, joins the communicator.  Collective in COMM mode (all ranks
+ * must call; LAG_XCHG_LOCAL contexts are connected by lag_local_group).
  * Errors: LAG_EINVAL (dims, spacing, bounds, layout, ghost, packed seed-node
  * width > 32 bits), LAG_ECUDA, LAG_ENCCL, LAG_ENOMEM.  *out is NULL on error.
  */
@@ -173,14 +190,27 @@ LAG_API lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out);
  * v_t, v_t1: slice arrays (see Conventions), device or host memory.  Passing
  * the same array twice is the frozen-snapshot regime (one accessible time
  * step per cycle): identical results, corners gathered once.
- * Errors: LAG_ESTATE (no lag_seed), LAG_EINVAL (dt <= 0 or non-finite, NULL
- * slice), LAG_ECUDA, LAG_ENCCL.  Async conditions are latched (see lag_stats).
+ * LAG_XCHG_LOCAL: collective over the group in the same sense: each block's
+ * call records its (device) slices; the call that completes the group's cycle
+ * enqueues the whole cycle of every block (ghost copy, appends, advection) on
+ * the group's stream.  The slices must stay unmodified until then.
+ * Errors: LAG_ESTATE (no lag_seed; LOCAL: a block called twice in one group
+ * cycle, or before every block extracted), LAG_EINVAL (dt <= 0 or
+ * non-finite, NULL slice; LOCAL: host slice), LAG_ECUDA, LAG_ENCCL (an NCCL
+ * call failed or the communicator reports an asynchronous error).  Async
+ * conditions are latched (see lag_stats).
  */
 LAG_API lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, double dt);
 
 /*
- * lag_extract — end of interval (write cycle).  COMM: first returns every
- * particle to its origin rank (collective).  Writes, for each of the n seeds
+ * lag_extract — end of interval (write cycle, "at the end of an
+ * interval ... the particle end locations are saved").  interval_index
+ * is the 0-based index of the interval being extracted, counted per context
+ * from lag_init: each call must pass the next one (the write cycles of one
+ * block follow one another); out of order -> LAG_ESTATE.  COMM:
+ * first returns every particle to its origin rank (collective; LAG_XCHG_LOCAL:
+ * each block gathers its basis flows from every block of the group, and the
+ * reseed of the group waits for the last block's extract).  Writes, for each of the n seeds
  * of the last lag_seed in seed order: start[i][dim] = x(g_i), end[i][dim] =
  * o + (g_i + d_i) h in fp64, status[i] = lag_flow_status.  Any of start, end,
  * status may be NULL (skipped); each may be a host or device pointer with
@@ -191,11 +221,12 @@ LAG_API lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, double d
  * only enqueues (no host synchronisation, for a simulation that must not
  * stall on the write cycle): BTO only needs device outputs; errors stay
  * latched across the reseed until a synchronous lag_extract reports them.
- * Errors: LAG_ESTATE (no lag_seed), LAG_EINVAL (capacity < n; LAG_ASYNC with
- * a host output pointer).
+ * Errors: LAG_ESTATE (no lag_seed; interval_index out of order),
+ * LAG_EINVAL (capacity < n; LAG_ASYNC with a host output pointer), LAG_ENCCL
+ * (NCCL failure or asynchronous communicator error).
  */
-LAG_API lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8_t* status,
-                       int64_t capacity, int64_t* n_out, uint32_t flags);
+LAG_API lag_status lag_extract(lag_ctx ctx, int64_t interval_index, double* start, double* end,
+                               uint8_t* status, int64_t capacity, int64_t* n_out, uint32_t flags);
 
 /*
  * lag_extract_ex — lag_extract plus, when term_cycle is not NULL, the cycle
@@ -204,11 +235,29 @@ LAG_API lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8_t*
  * on the block boundary the paper names as future work.  Same
  * conventions and errors as lag_extract.
  */
-LAG_API lag_status lag_extract_ex(lag_ctx ctx, double* start, double* end, uint8_t* status,
-                                  int32_t* term_cycle, int64_t capacity, int64_t* n_out,
-                                  uint32_t flags);
+LAG_API lag_status lag_extract_ex(lag_ctx ctx, int64_t interval_index, double* start, double* end,
+                                  uint8_t* status, int32_t* term_cycle, int64_t capacity,
+                                  int64_t* n_out, uint32_t flags);
 
-/* lag_stats — synchronise the stream and report counters (see lag_stats_t). */
+/*
+ * lag_local_group — connect n COMM contexts created with exchange =
+ * LAG_XCHG_LOCAL into one group: ctxs[r] must hold rank r of the same layout
+ * (nranks = n <= 64), the same device and the same stream.  Call once, after
+ * every lag_init and before the first lag_seed.  The group lives until its
+ * last context is destroyed.  Not collective across processes: the whole
+ * group is in this process (the single-GPU form of the COMM baseline, used
+ * to run several blocks of a decomposition on one B200).
+ * Errors: LAG_EINVAL (mismatched contexts, wrong transport, n out of range),
+ * LAG_ESTATE (already grouped or already seeded), LAG_ENOMEM, LAG_ECUDA.
+ */
+LAG_API lag_status lag_local_group(lag_ctx* ctxs, int32_t n);
+
+/* lag_stats — synchronise the stream and report counters (see lag_stats_t):
+ * particle-steps are the unit of the paper's per-cycle timing (P:363-367
+ * §4.2), terminations/exits and hand-offs are the particle-management and
+ * communication counts of P:205-207 §3.1;
+ * COMM over NCCL also polls the communicator's asynchronous error
+ * (ncclCommGetAsyncError): a failure returns LAG_ENCCL. */
 LAG_API lag_status lag_stats(lag_ctx ctx, lag_stats_t* out);
 
 /* lag_destroy — free every resource of the context (NULL is a no-op). */

@@ -122,15 +122,28 @@ static lag_status validate(const lag_config* c) {
             prod *= c->layout[a];
         }
         if (prod != c->nranks || c->rank < 0 || c->rank >= c->nranks) { lag_set_error(ctx, "rank/nranks/layout mismatch"); return LAG_EINVAL; }
-        if (c->nranks > 1 && !c->nccl_id) { lag_set_error(ctx, "COMM mode with nranks > 1 needs nccl_id"); return LAG_EINVAL; }
-        if (c->exchange != LAG_XCHG_NCCL && c->exchange != LAG_XCHG_PEER && c->exchange != LAG_XCHG_PEER_OVERLAP) {
-            lag_set_error(ctx, "exchange must be LAG_XCHG_NCCL, LAG_XCHG_PEER or LAG_XCHG_PEER_OVERLAP");
+        if (c->exchange != LAG_XCHG_NCCL && c->exchange != LAG_XCHG_PEER && c->exchange != LAG_XCHG_PEER_OVERLAP &&
+            c->exchange != LAG_XCHG_LOCAL) {
+            lag_set_error(ctx, "exchange must be LAG_XCHG_NCCL, LAG_XCHG_PEER, LAG_XCHG_PEER_OVERLAP or LAG_XCHG_LOCAL");
+            return LAG_EINVAL;
+        }
+        if (c->exchange == LAG_XCHG_LOCAL) {
+            if (c->nranks > 64) { lag_set_error(ctx, "LAG_XCHG_LOCAL groups hold at most 64 blocks"); return LAG_EINVAL; }
+        } else if (c->nranks > 1 && !c->nccl_id) {
+            lag_set_error(ctx, "COMM mode with nranks > 1 needs nccl_id");
             return LAG_EINVAL;
         }
     }
+    const int64_t ext_x = std::min(c->block_hi[0] + 1, c->global_nodes[0]) - c->block_lo[0] + 2 * c->ghost;
+    if (c->row_pitch_bytes != 0 &&
+        (c->row_pitch_bytes < 0 || c->row_pitch_bytes % (4 * c->dim) != 0 || c->row_pitch_bytes < 4 * c->dim * ext_x)) {
+        lag_set_error(ctx, "row_pitch_bytes = %lld must be 0 or a multiple of %d that is >= %lld",
+                      (long long)c->row_pitch_bytes, 4 * c->dim, (long long)(4 * c->dim * ext_x));
+        return LAG_EINVAL;
+    }
     // slice extent must fit 32-bit element offsets
-    int64_t nodes = 1;
-    for (int a = 0; a < c->dim; ++a)
+    int64_t nodes = c->row_pitch_bytes ? c->row_pitch_bytes / (4 * c->dim) : ext_x;
+    for (int a = 1; a < c->dim; ++a)
         nodes *= (std::min(c->block_hi[a] + 1, c->global_nodes[a]) - c->block_lo[a] + 2 * c->ghost);
     if (nodes * c->dim >= (int64_t(1) << 31)) { lag_set_error(ctx, "block slice too large for 32-bit offsets"); return LAG_EINVAL; }
     return LAG_OK;
@@ -164,7 +177,9 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     ctx->bits[0] = bits_for(cfg->global_nodes[0]);
     ctx->bits[1] = bits_for(cfg->global_nodes[1]);
     ctx->bits[2] = D == 3 ? bits_for(cfg->global_nodes[2]) : 0;
-    ctx->slice_floats = (int64_t)ctx->ext[0] * ctx->ext[1] * ctx->ext[2] * D;
+    ctx->sx = cfg->row_pitch_bytes ? (int)(cfg->row_pitch_bytes / (4 * D)) : ctx->ext[0];
+    ctx->sxy = ctx->sx * ctx->ext[1];
+    ctx->slice_floats = (int64_t)ctx->sxy * ctx->ext[2] * D;
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
     ctx->num_sms = dev_sms;
@@ -237,6 +252,7 @@ extern "C" lag_status lag_destroy(lag_ctx ctx) {
     if (!ctx) return LAG_OK;
     cudaSetDevice(ctx->cfg.device);
     if (ctx->stream_synced_needed) cudaStreamSynchronize(ctx->stream);
+    lag_local_leave(ctx);
     lag_comm_destroy(ctx);
     dfree(ctx->defer_list);
     dfree(ctx->state); dfree(ctx->tile_count); dfree(ctx->dead_rec); dfree(ctx->dead_info);
@@ -271,6 +287,10 @@ extern "C" lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out
     if (n_seeds_out) *n_seeds_out = 0;
     if (!ctx) { lag_set_error(nullptr, "ctx is NULL"); return LAG_EINVAL; }
     if (stride < 1) { lag_set_error(ctx, "stride must be >= 1 (got %d)", stride); return LAG_EINVAL; }
+    if (ctx->cfg.mode == LAG_COMM && ctx->cfg.exchange == LAG_XCHG_LOCAL && !ctx->group) {
+        lag_set_error(ctx, "LAG_XCHG_LOCAL context without lag_local_group");
+        return LAG_ESTATE;
+    }
     CK(cudaSetDevice(ctx->cfg.device));
     const int D = ctx->cfg.dim;
     int64_t n = 1;
@@ -385,18 +405,12 @@ static void fold_phases(lag_ctx_s* ctx) {
     ctx->ph_n = 0;
 }
 
-extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, double dt) {
-    if (!ctx) { lag_set_error(nullptr, "ctx is NULL"); return LAG_EINVAL; }
-    if (!ctx->seeded) { lag_set_error(ctx, "lag_advect_cycle before lag_seed"); return LAG_ESTATE; }
-    if (!v_t || !v_t1) { lag_set_error(ctx, "velocity slice pointer is NULL"); return LAG_EINVAL; }
-    if (!(dt > 0.0) || !std::isfinite(dt)) { lag_set_error(ctx, "dt must be finite and > 0"); return LAG_EINVAL; }
-    CK(cudaSetDevice(ctx->cfg.device));
-    float* d0 = nullptr;
-    float* d1 = nullptr;
+// One cycle of one block, slices already device-resident: (COMM) the
+// pre-advect exchange unless the LOCAL group ran it, the advect kernel, the
+// post-advect bookkeeping.  s0/s1: staging buffers read (host slices) or -1.
+static lag_status advect_enqueue(lag_ctx_s* ctx, float* d0, float* d1, double dt, bool v0_prev,
+                                 int s0, int s1) {
     lag_status st;
-    int s0 = -1, s1 = -1;
-    if ((st = resolve_slice(ctx, v_t, -1, &d0, &s0)) != LAG_OK) return st;
-    if ((st = resolve_slice(ctx, v_t1, s0, &d1, &s1)) != LAG_OK) return st;
     const int D = ctx->cfg.dim;
     if (ctx->phase_timing && ctx->ph_n == 64) fold_phases(ctx);
     cudaEvent_t* ev = ctx->phase_timing ? ctx->ph_ev[ctx->ph_n++] : nullptr;
@@ -410,12 +424,12 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
                            cudaMemcpyDeviceToDevice, ctx->stream));
         CK(cudaMemsetAsync(ctx->words + W_DEFER, 0, sizeof(uint32_t), ctx->stream));
         ctx->xchg_fused = &xf;
-        st = lag_comm_pre_advect(ctx, d0, d1, v_t == ctx->last_v1);
+        st = lag_comm_pre_advect(ctx, d0, d1, v0_prev);
         ctx->xchg_fused = nullptr;
         if (st != LAG_OK) return st;
         xf.ncta = kXchgCtas;
-    } else if (ctx->cfg.mode == LAG_COMM) {
-        st = lag_comm_pre_advect(ctx, d0, d1, v_t == ctx->last_v1);
+    } else if (ctx->cfg.mode == LAG_COMM && !ctx->group) {      // LOCAL: the group ran it
+        st = lag_comm_pre_advect(ctx, d0, d1, v0_prev);
         if (st != LAG_OK) return st;
     }
     if (ev && !overlap) cudaEventRecord(ev[1], ctx->stream);
@@ -448,8 +462,8 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
         a.qdth[ax] = (float)(0.25 * dth);
         a.sdth[ax] = (float)(dth / 6.0);
     }
-    a.sx = ctx->ext[0];
-    a.sxy = ctx->ext[0] * ctx->ext[1];
+    a.sx = ctx->sx;
+    a.sxy = ctx->sxy;
     a.gidx0 = (a.gmin[0] - a.base[0]) + a.sx * (a.gmin[1] - a.base[1]) + a.sxy * (a.gmin[2] - a.base[2]);
     a.bx = ctx->bits[0]; a.by = ctx->bits[1];
     a.mx = (1u << ctx->bits[0]) - 1u; a.my = (1u << ctx->bits[1]) - 1u;
@@ -537,10 +551,59 @@ extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, doubl
             CK(cudaEventRecord(ctx->stage_free[k], ctx->stream));
             ctx->stage_use[k] = ctx->cycles_total;
         }
-    ctx->last_v1 = v_t1;
     ctx->last_v1_slot = s1;
     ++ctx->cycles_in_interval;
     ++ctx->cycles_total;
+    return LAG_OK;
+}
+
+
+extern "C" lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, double dt) {
+    if (!ctx) { lag_set_error(nullptr, "ctx is NULL"); return LAG_EINVAL; }
+    if (!ctx->seeded) { lag_set_error(ctx, "lag_advect_cycle before lag_seed"); return LAG_ESTATE; }
+    if (!v_t || !v_t1) { lag_set_error(ctx, "velocity slice pointer is NULL"); return LAG_EINVAL; }
+    if (!(dt > 0.0) || !std::isfinite(dt)) { lag_set_error(ctx, "dt must be finite and > 0"); return LAG_EINVAL; }
+    CK(cudaSetDevice(ctx->cfg.device));
+    lag_status st;
+    if (ctx->cfg.mode == LAG_COMM && ctx->cfg.exchange == LAG_XCHG_LOCAL) {
+        if (!ctx->group) { lag_set_error(ctx, "LAG_XCHG_LOCAL context without lag_local_group"); return LAG_ESTATE; }
+        if (lag_local_extracting(ctx)) {
+            lag_set_error(ctx, "LAG_XCHG_LOCAL: lag_advect_cycle while the group's write cycle is incomplete");
+            return LAG_ESTATE;
+        }
+        for (void* p : {v_t, v_t1}) {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, p) != cudaSuccess || at.type != cudaMemoryTypeDevice ||
+                at.device != ctx->cfg.device) {
+                cudaGetLastError();
+                lag_set_error(ctx, "LAG_XCHG_LOCAL needs device slices on device %d", ctx->cfg.device);
+                return LAG_EINVAL;
+            }
+        }
+        lag_local_rec rec{(float*)v_t, (float*)v_t1, dt, v_t == ctx->last_v1};
+        bool complete = false;
+        if ((st = lag_local_record(ctx, rec, &complete)) != LAG_OK) return st;
+        ctx->last_v1 = v_t1;
+        if (!complete) return LAG_OK;            // the group's last block enqueues the cycle
+        if ((st = lag_local_run_cycle(ctx)) != LAG_OK) return st;
+        for (int r = 0; r < lag_local_size(ctx); ++r) {
+            lag_ctx_s* m = lag_local_member(ctx, r);
+            const lag_local_rec& q = lag_local_recorded(ctx, r);
+            if ((st = advect_enqueue(m, q.v0, q.v1, q.dt, q.v0_prev, -1, -1)) != LAG_OK) {
+                if (m != ctx) lag_set_error(ctx, "block %d: %s", r, m->msg.c_str());
+                return st;
+            }
+        }
+        return LAG_OK;
+    }
+    float* d0 = nullptr;
+    float* d1 = nullptr;
+    int s0 = -1, s1 = -1;
+    if ((st = resolve_slice(ctx, v_t, -1, &d0, &s0)) != LAG_OK) return st;
+    if ((st = resolve_slice(ctx, v_t1, s0, &d1, &s1)) != LAG_OK) return st;
+    st = advect_enqueue(ctx, d0, d1, dt, v_t == ctx->last_v1, s0, s1);
+    if (st != LAG_OK) return st;
+    ctx->last_v1 = v_t1;
     return LAG_OK;
 }
 
@@ -569,24 +632,34 @@ static T* out_target(lag_ctx_s* ctx, T* user, T* staging) {
     return staging;
 }
 
-extern "C" lag_status lag_extract(lag_ctx ctx, double* start, double* end, uint8_t* status,
-                                  int64_t capacity, int64_t* n_out, uint32_t flags) {
-    return lag_extract_ex(ctx, start, end, status, nullptr, capacity, n_out, flags);
+extern "C" lag_status lag_extract(lag_ctx ctx, int64_t interval_index, double* start, double* end,
+                                  uint8_t* status, int64_t capacity, int64_t* n_out, uint32_t flags) {
+    return lag_extract_ex(ctx, interval_index, start, end, status, nullptr, capacity, n_out, flags);
 }
 
-extern "C" lag_status lag_extract_ex(lag_ctx ctx, double* start, double* end, uint8_t* status,
-                                     int32_t* term_cycle, int64_t capacity, int64_t* n_out,
-                                     uint32_t flags) {
+extern "C" lag_status lag_extract_ex(lag_ctx ctx, int64_t interval_index, double* start, double* end,
+                                     uint8_t* status, int32_t* term_cycle, int64_t capacity,
+                                     int64_t* n_out, uint32_t flags) {
     if (n_out) *n_out = 0;
     if (!ctx) { lag_set_error(nullptr, "ctx is NULL"); return LAG_EINVAL; }
     if (!ctx->seeded) { lag_set_error(ctx, "lag_extract before lag_seed"); return LAG_ESTATE; }
+    if (interval_index != ctx->intervals_done) {
+        lag_set_error(ctx, "lag_extract of interval %lld out of order (next is %lld)",
+                      (long long)interval_index, (long long)ctx->intervals_done);
+        return LAG_ESTATE;
+    }
+    const bool local = ctx->cfg.mode == LAG_COMM && ctx->cfg.exchange == LAG_XCHG_LOCAL;
+    if (local && !ctx->group) { lag_set_error(ctx, "LAG_XCHG_LOCAL context without lag_local_group"); return LAG_ESTATE; }
     if (capacity < ctx->n_seeds && (start || end || status || term_cycle)) {
         lag_set_error(ctx, "capacity %lld < %lld seeds", (long long)capacity, (long long)ctx->n_seeds);
         return LAG_EINVAL;
     }
     CK(cudaSetDevice(ctx->cfg.device));
     lag_status st;
-    if (ctx->cfg.mode == LAG_COMM) {
+    if (local) {
+        st = lag_local_flush(ctx);                // the group's pending hand-offs, once
+        if (st != LAG_OK) return st;
+    } else if (ctx->cfg.mode == LAG_COMM) {
         st = lag_comm_return_to_origin(ctx);      // collective; leaves only own-origin records
         if (st != LAG_OK) return st;
     }
@@ -623,20 +696,40 @@ extern "C" lag_status lag_extract_ex(lag_ctx ctx, double* start, double* end, ui
     }
     e.write_start = ctx->cfg.mode == LAG_BTO ? 1 : 0;
     const unsigned nb_seed = (unsigned)((ctx->n_seeds + 255) / 256);
-    const unsigned nb_live = (unsigned)(((int64_t)e.n_tiles * kTile + 255) / 256);
     const unsigned nb_dead = (unsigned)std::max(1, ctx->num_sms * 2);
-    if (D == 3) {
-        if (!e.write_start) { extract_start_kernel<3><<<nb_seed, 256, 0, ctx->stream>>>(e); ++ctx->launches; }
-        extract_live_kernel<3><<<nb_live, 256, 0, ctx->stream>>>(e);
-        extract_dead_kernel<3><<<nb_dead, 256, 0, ctx->stream>>>(e);
-        if (e.n_ret > 0) { extract_returned_kernel<3><<<(e.n_ret + 255) / 256, 256, 0, ctx->stream>>>(e); ++ctx->launches; }
-    } else {
-        if (!e.write_start) { extract_start_kernel<2><<<nb_seed, 256, 0, ctx->stream>>>(e); ++ctx->launches; }
-        extract_live_kernel<2><<<nb_live, 256, 0, ctx->stream>>>(e);
-        extract_dead_kernel<2><<<nb_dead, 256, 0, ctx->stream>>>(e);
-        if (e.n_ret > 0) { extract_returned_kernel<2><<<(e.n_ret + 255) / 256, 256, 0, ctx->stream>>>(e); ++ctx->launches; }
+    if (!e.write_start) {
+        if (D == 3) extract_start_kernel<3><<<nb_seed, 256, 0, ctx->stream>>>(e);
+        else extract_start_kernel<2><<<nb_seed, 256, 0, ctx->stream>>>(e);
+        ++ctx->launches;
     }
-    ctx->launches += 2;
+    // LOCAL: every block of the group may hold particles seeded here (the
+    // group's last hand-offs were appended by lag_local_flush); the own-seed
+    // filter of the scatter kernels picks this block's
+    const int nsrc = local ? lag_local_size(ctx) : 1;
+    for (int q = 0; q < nsrc; ++q) {
+        ExtractArgs eq = e;
+        if (local) {
+            const lag_ctx_s* m = lag_local_member(ctx, q);
+            eq.state = m->state; eq.tile_count = m->tile_count; eq.n_tiles = m->cap_tiles;
+            eq.n_tiles_dev = (const int32_t*)(m->words + W_NTILES);
+            eq.dead_rec = m->dead_rec; eq.dead_info = m->dead_info;
+            eq.n_dead_dev = m->words + W_DEAD; eq.dead_cap = (uint32_t)m->cap;
+        }
+        const unsigned nbl = (unsigned)(((int64_t)eq.n_tiles * kTile + 255) / 256);
+        if (D == 3) {
+            extract_live_kernel<3><<<nbl, 256, 0, ctx->stream>>>(eq);
+            extract_dead_kernel<3><<<nb_dead, 256, 0, ctx->stream>>>(eq);
+        } else {
+            extract_live_kernel<2><<<nbl, 256, 0, ctx->stream>>>(eq);
+            extract_dead_kernel<2><<<nb_dead, 256, 0, ctx->stream>>>(eq);
+        }
+        ctx->launches += 2;
+    }
+    if (e.n_ret > 0) {
+        if (D == 3) extract_returned_kernel<3><<<(e.n_ret + 255) / 256, 256, 0, ctx->stream>>>(e);
+        else extract_returned_kernel<2><<<(e.n_ret + 255) / 256, 256, 0, ctx->stream>>>(e);
+        ++ctx->launches;
+    }
     CK(cudaGetLastError());
     const size_t n = (size_t)ctx->n_seeds;
     if ((st = copy_out(ctx, start, e.start, n * D * sizeof(double))) != LAG_OK) return st;
@@ -647,11 +740,36 @@ extern "C" lag_status lag_extract_ex(lag_ctx ctx, double* start, double* end, ui
     if (!async) {
         CK(cudaMemcpyAsync(&ctx->host_words[0], ctx->words, kWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));  // the only host sync of the write cycle
+        if (ctx->cfg.mode == LAG_COMM) {
+            lag_status ne = lag_comm_async_error(ctx);
+            if (ne != LAG_OK) return ne;
+        }
         err = latched(ctx, ctx->host_words[W_ERR]);
         if (ctx->host_words[W_ERR])              // reported: clear the latch
             CK(cudaMemsetAsync(ctx->words + W_ERR, 0, sizeof(uint32_t), ctx->stream));
     }
     if (n_out) *n_out = ctx->n_seeds;
+    ++ctx->intervals_done;
+    if (local) {
+        // every block must gather its flows before any block is reseeded:
+        // the last extract of the group reseeds the blocks that asked for it
+        ctx->reseed_pending = !(flags & LAG_NO_RESEED);
+        bool all = false;
+        lag_local_extracted(ctx, &all);
+        if (all) {
+            for (int q = 0; q < lag_local_size(ctx); ++q) {
+                lag_ctx_s* m = lag_local_member(ctx, q);
+                if (!m->reseed_pending) continue;
+                m->reseed_pending = false;
+                st = lag_seed(m, m->stride, nullptr);
+                if (st != LAG_OK) {
+                    if (m != ctx) lag_set_error(ctx, "block %d: %s", q, m->msg.c_str());
+                    return st;
+                }
+            }
+        }
+        return err;
+    }
     if (!(flags & LAG_NO_RESEED)) {
         st = lag_seed(ctx, ctx->stride, nullptr);
         if (st != LAG_OK) return st;
@@ -668,6 +786,10 @@ extern "C" lag_status lag_stats(lag_ctx ctx, lag_stats_t* out) {
     CK(cudaMemcpyAsync(c, ctx->counters, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(&ctx->host_words[0], ctx->words, kWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->cfg.mode == LAG_COMM) {
+        lag_status ne = lag_comm_async_error(ctx);
+        if (ne != LAG_OK) return ne;
+    }
     std::memset(out, 0, sizeof(*out));
     out->seeded = ctx->seeded ? ctx->n_seeds : 0;
     out->term_boundary = (int64_t)c[CNT_TERM];

@@ -26,7 +26,8 @@ struct AppendArgs {
     float4* slots;                  // outgoing slots: headers reset here (NCCL)
     int32_t slot_base[kMaxOff];
     int noff;
-    int zero_recv;                  // peer transport: reset the consumed inbox headers instead
+    int zero_recv;                  // peer/local transport: reset the consumed inbox headers instead
+    int discard;                    // drop the records (a reseed in the middle of an interval)
 };
 
 // Received particles become new tiles at the end of the list.  Every CTA of
@@ -45,6 +46,7 @@ __device__ __forceinline__ void append_body(const AppendArgs& a, int cta, int nc
             if (c > a.cap[p]) { c = a.cap[p]; atomicOr(a.words + W_ERR, ERR_OVERFLOW); }
             s += c;
         }
+        if (a.discard) s = 0;
         pre[a.npeers] = s;
         old_tiles = *reinterpret_cast<const volatile uint32_t*>(a.words + W_NTILES);
         const uint32_t room = (uint32_t)(a.cap_tiles - (int)old_tiles) * kTile;

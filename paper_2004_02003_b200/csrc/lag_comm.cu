@@ -113,6 +113,8 @@ struct Comm {
     RouteRec* route = nullptr;          // [cap]
     RouteRec* route_recv = nullptr;     // [cap]
     uint32_t* d_route_pos = nullptr;
+    uint32_t* d_seg = nullptr;          // [nranks + 1] segment starts
+    uint32_t* d_all = nullptr;          // [nranks * (nranks + 1)] count exchange
     int64_t route_cap = 0;
     uint32_t n_returned = 0;
     // LAG_XCHG_PEER transport
@@ -235,18 +237,22 @@ __global__ void route_kernel(RouteArgs a) {
 // host side
 
 static int off_index(const int o[3]) { return (o[0] + 1) + 3 * ((o[1] + 1) + 3 * (o[2] + 1)); }
+static lag_status comm_setup(lag_ctx_s* ctx);
 
 lag_status lag_comm_init(lag_ctx_s* ctx) {
     const lag_config& c = ctx->cfg;
     Comm* cm = new Comm();
     ctx->comm = cm;
-    const int D = c.dim;
-    const int G = c.ghost;
     cm->me[0] = c.rank % c.layout[0];
     cm->me[1] = (c.rank / c.layout[0]) % c.layout[1];
     cm->me[2] = c.rank / (c.layout[0] * c.layout[1]);
     cm->blocks.assign((size_t)c.nranks * 6, 0);
     int64_t mine[6] = {c.block_lo[0], c.block_lo[1], c.block_lo[2], c.block_hi[0], c.block_hi[1], c.block_hi[2]};
+    if (c.exchange == LAG_XCHG_LOCAL) {
+        // the other blocks are contexts of this process: lag_local_group
+        // fills the block table and finishes the setup
+        return LAG_OK;
+    }
     if (c.nranks > 1) {
         ncclUniqueId id;
         std::memcpy(&id, c.nccl_id, sizeof(id));
@@ -261,6 +267,17 @@ lag_status lag_comm_init(lag_ctx_s* ctx) {
     } else {
         std::copy(mine, mine + 6, cm->blocks.begin());
     }
+    return comm_setup(ctx);
+}
+
+// Neighbours, ghost boxes, particle slots and routing tables from the block
+// table cm->blocks (every rank's [lo, hi)).
+static lag_status comm_setup(lag_ctx_s* ctx) {
+    const lag_config& c = ctx->cfg;
+    Comm* cm = ctx->comm;
+    const int D = c.dim;
+    const int G = c.ghost;
+    const int64_t* mine = &cm->blocks[(size_t)c.rank * 6];
     // per-axis cut points (block lo values along each axis, plus N)
     for (int ax = 0; ax < 3; ++ax) {
         std::vector<int32_t> v;
@@ -401,6 +418,8 @@ lag_status lag_comm_init(lag_ctx_s* ctx) {
     CKC(cudaMemcpy(cm->d_cuts, cm->cuts, sizeof(int32_t) * 3 * kMaxCuts, cudaMemcpyHostToDevice));
     CKC(cudaMalloc(&cm->d_route_count, sizeof(uint32_t) * 2 * std::max(1, c.nranks)));
     cm->d_route_pos = cm->d_route_count + c.nranks;
+    CKC(cudaMalloc(&cm->d_seg, sizeof(uint32_t) * (c.nranks + 1)));
+    CKC(cudaMalloc(&cm->d_all, sizeof(uint32_t) * c.nranks * (c.nranks + 1)));
     cm->route_cap = ctx->cap;
     CKC(cudaMalloc(&cm->route, sizeof(RouteRec) * std::max<int64_t>(1, cm->route_cap)));
     CKC(cudaMalloc(&cm->route_recv, sizeof(RouteRec) * std::max<int64_t>(1, cm->route_cap)));
@@ -434,20 +453,35 @@ void lag_comm_destroy(lag_ctx_s* ctx) {
     cudaFree(cm->halo_send); cudaFree(cm->halo_recv);
     cudaFree(cm->slots); cudaFree(cm->recv_slots); cudaFree(cm->d_cuts);
     cudaFree(cm->d_route_count); cudaFree(cm->route); cudaFree(cm->route_recv);
+    cudaFree(cm->d_seg); cudaFree(cm->d_all);
     delete cm;
     ctx->comm = nullptr;
 }
 
+static void local_unrecord(lag_ctx_s* ctx);
+static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity);
+
 lag_status lag_comm_reset(lag_ctx_s* ctx) {
     Comm* cm = ctx->comm;
+    local_unrecord(ctx);
+    if (cm->peer && cm->pending) {
+        // peer transports, reseed in the middle of an interval: the last
+        // cycle's hand-offs are being stored into my inbox by the neighbours'
+        // advect kernels; wait for their "particles(seq)" signal and drop them
+        // (zero the inbox headers) so the next interval does not append them
+        const unsigned long long seq = lag_peer_seq(cm->peer);
+        AppendArgs ap = append_args(ctx, (int)(seq & 1));
+        ap.discard = 1;
+        lag_status st = lag_peer_exchange(ctx, cm->peer, cm->d_send_boxes, (int)cm->peers.size(), 0,
+                                          nullptr, nullptr, false, false, cm->poff, cm->pback, seq, &ap);
+        if (st != LAG_OK) return st;
+    }
     // empty outgoing slots; nothing pending (seed_kernel sets W_NTILES)
     CKC(cudaMemsetAsync(cm->slots, 0, sizeof(float4) * std::max<int64_t>(1, cm->slot_total), ctx->stream));
     cm->pending = false;
     cm->n_returned = 0;
     return LAG_OK;
 }
-
-static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity);
 
 static lag_status launch_append(lag_ctx_s* ctx, int peer_parity = -1) {
     AppendArgs a = append_args(ctx, peer_parity);
@@ -487,7 +521,7 @@ static lag_status exchange(lag_ctx_s* ctx, float* v0, float* v1, bool halo, bool
     if (halo && sfl > 0) {
         BoxArgs b{};
         b.v0 = v0; b.v1 = v1; b.v0w = v0; b.boxes = cm->d_send_boxes; b.nbox = nbox;
-        b.buf = cm->halo_send; b.sx = ctx->ext[0]; b.sxy = ctx->ext[0] * ctx->ext[1]; b.dim = D; b.total = sfl;
+        b.buf = cm->halo_send; b.sx = ctx->sx; b.sxy = ctx->sxy; b.dim = D; b.total = sfl;
         const int blocks = (int)std::min<int64_t>((sfl + 255) / 256, (int64_t)ctx->num_sms * 8);
         halo_pack_kernel<<<blocks, 256, 0, ctx->stream>>>(b);
         ++ctx->launches;
@@ -513,7 +547,7 @@ static lag_status exchange(lag_ctx_s* ctx, float* v0, float* v1, bool halo, bool
     if (halo && rfl > 0) {
         BoxArgs b{};
         b.v0 = v0; b.v1 = v1; b.v0w = v0; b.boxes = cm->d_recv_boxes; b.nbox = nbox;
-        b.buf = cm->halo_recv; b.sx = ctx->ext[0]; b.sxy = ctx->ext[0] * ctx->ext[1]; b.dim = D; b.total = rfl;
+        b.buf = cm->halo_recv; b.sx = ctx->sx; b.sxy = ctx->sxy; b.dim = D; b.total = rfl;
         const int blocks = (int)std::min<int64_t>((rfl + 255) / 256, (int64_t)ctx->num_sms * 8);
         halo_unpack_kernel<<<blocks, 256, 0, ctx->stream>>>(b);
         ++ctx->launches;
@@ -604,8 +638,7 @@ lag_status lag_comm_return_to_origin(lag_ctx_s* ctx) {
     ra.me = c.rank;
     ra.count = cm->d_route_count; ra.pos = cm->d_route_pos;
     std::vector<uint32_t> seg(R + 1, 0), cnt(R, 0);
-    uint32_t* d_seg = nullptr;
-    CKC(cudaMalloc(&d_seg, sizeof(uint32_t) * (R + 1)));
+    uint32_t* d_seg = cm->d_seg;
     CKC(cudaMemsetAsync(cm->d_route_count, 0, sizeof(uint32_t) * 2 * R, ctx->stream));
     const int blocks = ctx->num_sms * 4;
     ra.pass = 0;
@@ -614,23 +647,21 @@ lag_status lag_comm_return_to_origin(lag_ctx_s* ctx) {
     CKC(cudaMemcpyAsync(cnt.data(), cm->d_route_count, sizeof(uint32_t) * R, cudaMemcpyDeviceToHost, ctx->stream));
     CKC(cudaStreamSynchronize(ctx->stream));
     for (int r = 0; r < R; ++r) seg[r + 1] = seg[r] + cnt[r];
-    if (seg[R] > (uint32_t)cm->route_cap) { cudaFree(d_seg); lag_set_error(ctx, "route buffer overflow"); return LAG_EOVERFLOW; }
+    if (seg[R] > (uint32_t)cm->route_cap) { lag_set_error(ctx, "route buffer overflow"); return LAG_EOVERFLOW; }
     CKC(cudaMemcpyAsync(d_seg, seg.data(), sizeof(uint32_t) * (R + 1), cudaMemcpyHostToDevice, ctx->stream));
     ra.pass = 1; ra.seg = d_seg; ra.out = cm->route;
     route_kernel<<<blocks, 256, 0, ctx->stream>>>(ra);
     ++ctx->launches;
     // exchange the counts: everyone learns how much it receives from whom
-    uint32_t* d_all = nullptr;
-    CKC(cudaMalloc(&d_all, sizeof(uint32_t) * R * (R + 1)));
+    uint32_t* d_all = cm->d_all;
     CKC(cudaMemcpyAsync(d_all, cnt.data(), sizeof(uint32_t) * R, cudaMemcpyHostToDevice, ctx->stream));
     CKN(ncclAllGather(d_all, d_all + R, R, ncclUint32, cm->nccl, ctx->stream));
     std::vector<uint32_t> all((size_t)R * R);
     CKC(cudaMemcpyAsync(all.data(), d_all + R, sizeof(uint32_t) * R * R, cudaMemcpyDeviceToHost, ctx->stream));
     CKC(cudaStreamSynchronize(ctx->stream));
-    cudaFree(d_all);
     std::vector<uint32_t> rseg(R + 1, 0);
     for (int r = 0; r < R; ++r) rseg[r + 1] = rseg[r] + (r == c.rank ? 0 : all[(size_t)r * R + c.rank]);
-    if (rseg[R] > (uint32_t)cm->route_cap) { cudaFree(d_seg); lag_set_error(ctx, "route receive overflow"); return LAG_EOVERFLOW; }
+    if (rseg[R] > (uint32_t)cm->route_cap) { lag_set_error(ctx, "route receive overflow"); return LAG_EOVERFLOW; }
     CKN(ncclGroupStart());
     for (int r = 0; r < R; ++r) {
         if (r == c.rank) continue;
@@ -640,7 +671,6 @@ lag_status lag_comm_return_to_origin(lag_ctx_s* ctx) {
     }
     CKN(ncclGroupEnd());
     CKC(cudaStreamSynchronize(ctx->stream));
-    cudaFree(d_seg);
     cm->n_returned = rseg[R];
     return LAG_OK;
 }
@@ -663,4 +693,289 @@ extern "C" lag_status lag_nccl_unique_id(void* out, int64_t out_bytes) {
     CKN(ncclGetUniqueId(&id));
     std::memcpy(out, &id, sizeof(id));
     return LAG_OK;
+}
+
+lag_status lag_comm_async_error(lag_ctx_s* ctx) {
+    Comm* cm = ctx->comm;
+    if (!cm || !cm->nccl) return LAG_OK;
+    ncclResult_t res = ncclSuccess;
+    CKN(ncclCommGetAsyncError(cm->nccl, &res));
+    if (res != ncclSuccess && res != ncclInProgress) {
+        lag_set_error(ctx, "NCCL communicator asynchronous error: %s", ncclGetErrorString(res));
+        return LAG_ENCCL;
+    }
+    return LAG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// LAG_XCHG_LOCAL: the blocks of a decomposition as contexts of one process on
+// one device.  Per group cycle (enqueued by the call that completes it, on
+// the group's single stream, so stream order replaces every flag and wait):
+//   1. one kernel copies every block's ghost layers of v_t1 (and of v_t when
+//      it is not the previous call's v_t1) from the neighbours' slice arrays;
+//   2. per block, append_body adds the hand-offs the neighbours' advect
+//      kernels left in their slots toward it (the previous cycle's, as in the
+//      NCCL transport) and zeroes those slot headers;
+//   3. per block, the advect kernel (lag_api.cu) writes leaving particles to
+//      its own slots.
+// The write cycle appends the last cycle's hand-offs once; each block then
+// gathers its basis flows from every block's lists (lag_api.cu).
+
+namespace lag {
+constexpr int kLocalMax = 64;
+struct LocalBox {               // ghost box of block dst filled from block src's interior
+    int dst, src;
+    int dx0, dy0, dz0;          // dst slice coordinates
+    int sx0, sy0, sz0;          // src slice coordinates
+    int nx, ny, nz;
+    int64_t off;                // float offset in the flattened copy (one slice)
+};
+struct LocalCopyArgs {
+    const LocalBox* boxes;
+    int nbox;
+    int dim;
+    int64_t total;              // floats over all boxes (one slice)
+    unsigned long long fill_v0; // bit r: block r's v_t needs its ghosts too
+    float* v0[kLocalMax];
+    float* v1[kLocalMax];
+    int sx[kLocalMax], sxy[kLocalMax];
+};
+
+__global__ void __launch_bounds__(256) local_ghost_kernel(const LocalCopyArgs a) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * a.total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int slice = i >= a.total ? 0 : 1;         // first v_t1, then v_t
+        const int64_t j = slice ? i : i - a.total;
+        int lo = 0, hi = a.nbox - 1;                    // box with off <= j (offsets ascending)
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (a.boxes[mid].off <= j) lo = mid; else hi = mid - 1;
+        }
+        const LocalBox& b = a.boxes[lo];
+        if (!slice && !((a.fill_v0 >> b.dst) & 1ull)) continue;
+        const int64_t k = j - b.off;
+        const int comp = (int)(k % a.dim);
+        const int64_t node = k / a.dim;
+        const int x = (int)(node % b.nx), y = (int)((node / b.nx) % b.ny), z = (int)(node / ((int64_t)b.nx * b.ny));
+        const float* src = slice ? a.v1[b.src] : a.v0[b.src];
+        float* dst = slice ? a.v1[b.dst] : a.v0[b.dst];
+        dst[(int64_t)a.dim * ((b.dx0 + x) + (int64_t)a.sx[b.dst] * (b.dy0 + y) + (int64_t)a.sxy[b.dst] * (b.dz0 + z)) + comp] =
+            src[(int64_t)a.dim * ((b.sx0 + x) + (int64_t)a.sx[b.src] * (b.sy0 + y) + (int64_t)a.sxy[b.src] * (b.sz0 + z)) + comp];
+    }
+}
+
+struct LocalGroup {
+    std::vector<lag_ctx_s*> m;          // rank -> context (nullptr once destroyed)
+    std::vector<lag_local_rec> rec;
+    std::vector<char> has;              // recorded in the current group cycle
+    int nrec = 0;
+    std::vector<char> extracted;
+    int nextracted = 0;
+    std::vector<LocalBox> boxes;
+    LocalBox* d_boxes = nullptr;
+    int64_t total = 0;
+    int alive = 0;
+};
+}  // namespace lag
+
+static AppendArgs local_append_args(lag_ctx_s* ctx) {
+    Comm* cm = ctx->comm;
+    LocalGroup* g = ctx->group;
+    AppendArgs a{};
+    a.state = ctx->state; a.tile_count = ctx->tile_count; a.words = ctx->words;
+    a.counters = ctx->counters; a.cap_tiles = ctx->cap_tiles;
+    a.npeers = (int)cm->peers.size();
+    for (size_t i = 0; i < cm->peers.size(); ++i) {
+        const Peer& p = cm->peers[i];
+        const Comm* pc = g->m[p.rank]->comm;            // the neighbour's slot toward me
+        a.recv[i] = pc->slots + pc->slot_base[p.back];
+        a.cap[i] = (uint32_t)pc->slot_capv[p.back];
+    }
+    a.zero_recv = 1;                                    // each slot has exactly one reader: me
+    a.noff = 0;
+    return a;
+}
+
+static lag_status local_appends(lag_ctx_s* any) {
+    LocalGroup* g = any->group;
+    for (lag_ctx_s* ctx : g->m) {
+        if (!ctx || ctx->comm->peers.empty()) continue;
+        AppendArgs a = local_append_args(ctx);
+        append_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(a);
+        ++ctx->launches;
+        CKC(cudaGetLastError());
+        ctx->comm->pending = false;
+    }
+    return LAG_OK;
+}
+
+extern "C" lag_status lag_local_group(lag_ctx* ctxs, int32_t n) {
+    lag_ctx_s* ctx = nullptr;
+    if (!ctxs || n < 1 || n > kLocalMax) { lag_set_error(nullptr, "lag_local_group: need 1..%d contexts", kLocalMax); return LAG_EINVAL; }
+    for (int r = 0; r < n; ++r) {
+        lag_ctx_s* c = ctxs[r];
+        if (!c || c->cfg.mode != LAG_COMM || c->cfg.exchange != LAG_XCHG_LOCAL || c->cfg.rank != r ||
+            c->cfg.nranks != n || c->cfg.device != ctxs[0]->cfg.device || c->stream != ctxs[0]->stream ||
+            c->cfg.dim != ctxs[0]->cfg.dim || c->cfg.ghost < 1) {
+            lag_set_error(nullptr, "lag_local_group: context %d is not rank %d of an n = %d LAG_XCHG_LOCAL "
+                          "COMM group on the same device and stream", r, r, n);
+            return LAG_EINVAL;
+        }
+        for (int a = 0; a < 3; ++a)
+            if (c->cfg.global_nodes[a] != ctxs[0]->cfg.global_nodes[a] || c->cfg.layout[a] != ctxs[0]->cfg.layout[a]) {
+                lag_set_error(nullptr, "lag_local_group: context %d has another grid or layout", r);
+                return LAG_EINVAL;
+            }
+        if (c->group || c->seeded) {
+            lag_set_error(nullptr, "lag_local_group: context %d is already grouped or seeded", r);
+            return LAG_ESTATE;
+        }
+    }
+    for (int r = 0; r < n; ++r) {
+        ctx = ctxs[r];
+        Comm* cm = ctx->comm;
+        for (int q = 0; q < n; ++q)
+            for (int a = 0; a < 3; ++a) {
+                cm->blocks[(size_t)q * 6 + a] = ctxs[q]->cfg.block_lo[a];
+                cm->blocks[(size_t)q * 6 + 3 + a] = ctxs[q]->cfg.block_hi[a];
+            }
+        lag_status st = comm_setup(ctx);
+        if (st != LAG_OK) { lag_set_error(nullptr, "lag_local_group: block %d: %s", r, ctx->msg.c_str()); return st; }
+    }
+    LocalGroup* g = new LocalGroup();
+    g->m.assign(ctxs, ctxs + n);
+    g->rec.assign(n, lag_local_rec{});
+    g->has.assign(n, 0);
+    g->extracted.assign(n, 0);
+    g->alive = n;
+    // ghost boxes: block r's receive box from peer p <- p's send box toward r
+    for (int r = 0; r < n; ++r) {
+        const Comm* cr = ctxs[r]->comm;
+        for (const Peer& p : cr->peers) {
+            const Comm* cp = ctxs[p.rank]->comm;
+            const Box* sb = nullptr;
+            for (const Peer& pp : cp->peers)
+                if (pp.rank == r && pp.off == p.back) sb = &cp->send_boxes[(size_t)pp.send_box];
+            const Box& rb = cr->recv_boxes[(size_t)p.recv_box];
+            if (!sb || sb->nx != rb.nx || sb->ny != rb.ny || sb->nz != rb.nz) {
+                delete g;
+                lag_set_error(nullptr, "lag_local_group: ghost boxes of blocks %d and %d do not match", r, p.rank);
+                return LAG_EINVAL;
+            }
+            LocalBox b{};
+            b.dst = r; b.src = p.rank;
+            b.dx0 = rb.x0; b.dy0 = rb.y0; b.dz0 = rb.z0;
+            b.sx0 = sb->x0; b.sy0 = sb->y0; b.sz0 = sb->z0;
+            b.nx = rb.nx; b.ny = rb.ny; b.nz = rb.nz;
+            b.off = g->total;
+            g->total += (int64_t)b.nx * b.ny * b.nz * ctxs[0]->cfg.dim;
+            g->boxes.push_back(b);
+        }
+    }
+    ctx = ctxs[0];
+    if (!g->boxes.empty()) {
+        cudaError_t e = cudaMalloc(&g->d_boxes, sizeof(LocalBox) * g->boxes.size());
+        if (e == cudaSuccess)
+            e = cudaMemcpy(g->d_boxes, g->boxes.data(), sizeof(LocalBox) * g->boxes.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(g->d_boxes);
+            delete g;
+            lag_set_error(nullptr, "lag_local_group: %s", cudaGetErrorString(e));
+            return LAG_ECUDA;
+        }
+    }
+    for (int r = 0; r < n; ++r) ctxs[r]->group = g;
+    return LAG_OK;
+}
+
+static void local_unrecord(lag_ctx_s* ctx) {
+    LocalGroup* g = ctx->group;
+    if (!g) return;
+    const int r = ctx->cfg.rank;
+    if (g->has[r]) { g->has[r] = 0; --g->nrec; }
+}
+
+lag_status lag_local_record(lag_ctx_s* ctx, const lag_local_rec& rec, bool* complete) {
+    LocalGroup* g = ctx->group;
+    const int r = ctx->cfg.rank;
+    *complete = false;
+    if (g->has[r]) {
+        lag_set_error(ctx, "LAG_XCHG_LOCAL: block %d already recorded this group cycle", r);
+        return LAG_ESTATE;
+    }
+    for (int q = 0; q < (int)g->m.size(); ++q)
+        if (!g->m[q]) { lag_set_error(ctx, "LAG_XCHG_LOCAL: block %d was destroyed", q); return LAG_ESTATE; }
+    g->rec[r] = rec;
+    g->has[r] = 1;
+    if (++g->nrec == (int)g->m.size()) {
+        for (lag_ctx_s* c : g->m)
+            if (!c->seeded) { lag_set_error(ctx, "LAG_XCHG_LOCAL: block %d is not seeded", c->cfg.rank); g->has[r] = 0; --g->nrec; return LAG_ESTATE; }
+        std::fill(g->has.begin(), g->has.end(), 0);
+        g->nrec = 0;
+        *complete = true;
+    }
+    return LAG_OK;
+}
+
+lag_status lag_local_run_cycle(lag_ctx_s* ctx) {
+    LocalGroup* g = ctx->group;
+    const int n = (int)g->m.size();
+    if (g->total > 0) {
+        LocalCopyArgs a{};
+        a.boxes = g->d_boxes;
+        a.nbox = (int)g->boxes.size();
+        a.dim = ctx->cfg.dim;
+        a.total = g->total;
+        for (int r = 0; r < n; ++r) {
+            a.v0[r] = g->rec[r].v0;
+            a.v1[r] = g->rec[r].v1;
+            a.sx[r] = g->m[r]->sx;
+            a.sxy[r] = g->m[r]->sxy;
+            if (!g->rec[r].v0_prev) a.fill_v0 |= 1ull << r;
+        }
+        const int blocks = (int)std::min<int64_t>((2 * g->total + 255) / 256, (int64_t)ctx->num_sms * 8);
+        local_ghost_kernel<<<std::max(1, blocks), 256, 0, ctx->stream>>>(a);
+        ++ctx->launches;
+        CKC(cudaGetLastError());
+    }
+    return local_appends(ctx);
+}
+
+lag_ctx_s* lag_local_member(lag_ctx_s* ctx, int r) { return ctx->group->m[r]; }
+const lag_local_rec& lag_local_recorded(lag_ctx_s* ctx, int r) { return ctx->group->rec[r]; }
+int lag_local_size(lag_ctx_s* ctx) { return (int)ctx->group->m.size(); }
+
+lag_status lag_local_flush(lag_ctx_s* ctx) {
+    LocalGroup* g = ctx->group;
+    if (g->nextracted > 0) return LAG_OK;               // an earlier block of this write cycle did it
+    for (lag_ctx_s* c : g->m)
+        if (!c) { lag_set_error(ctx, "LAG_XCHG_LOCAL: a block of the group was destroyed"); return LAG_ESTATE; }
+    bool pending = false;
+    for (lag_ctx_s* c : g->m) pending |= c->comm->pending;
+    return pending ? local_appends(ctx) : LAG_OK;
+}
+
+bool lag_local_extracted(lag_ctx_s* ctx, bool* all) {
+    LocalGroup* g = ctx->group;
+    const int r = ctx->cfg.rank;
+    if (!g->extracted[r]) { g->extracted[r] = 1; ++g->nextracted; }
+    *all = g->nextracted == (int)g->m.size();
+    if (*all) {
+        std::fill(g->extracted.begin(), g->extracted.end(), 0);
+        g->nextracted = 0;
+    }
+    return true;
+}
+
+bool lag_local_extracting(lag_ctx_s* ctx) { return ctx->group && ctx->group->nextracted > 0; }
+
+void lag_local_leave(lag_ctx_s* ctx) {
+    LocalGroup* g = ctx->group;
+    if (!g) return;
+    g->m[ctx->cfg.rank] = nullptr;
+    ctx->group = nullptr;
+    if (--g->alive == 0) {
+        cudaFree(g->d_boxes);
+        delete g;
+    }
 }

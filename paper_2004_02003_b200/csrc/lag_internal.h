@@ -8,7 +8,8 @@
 
 namespace lag {
 enum : int { W_DEAD = 0, W_ERR = 1, W_NTILES = 2, W_APPEND_DONE = 3, W_NTILES_B = 4, W_DEFER = 5, kWords = 8 };
-struct Comm;   // lag_comm.cu
+struct Comm;         // lag_comm.cu
+struct LocalGroup;   // lag_comm.cu (LAG_XCHG_LOCAL)
 }
 
 struct lag_ctx_s {
@@ -19,7 +20,8 @@ struct lag_ctx_s {
     int ext[3] = {1, 1, 1};          // slice extent (nodes) incl. ghosts
     int base[3] = {0, 0, 0};         // global node of slice element 0
     int bits[3] = {0, 0, 0};         // packed seed-node widths
-    int64_t slice_floats = 0;
+    int sx = 1, sxy = 1;             // slice row / plane pitch in nodes (row_pitch_bytes)
+    int64_t slice_floats = 0;        // floats of one slice array (pitched)
     int num_sms = 148;
     int advect_blocks_per_sm = 1;
     // particles
@@ -34,6 +36,8 @@ struct lag_ctx_s {
     bool stream_synced_needed = true;
     int cycles_in_interval = 0;
     int64_t cycles_total = 0;
+    int64_t intervals_done = 0;      // write cycles extracted (lag_extract interval_index)
+    bool reseed_pending = false;     // LOCAL: reseed when the group's last block extracted
     int64_t launches = 0;
     float4* state = nullptr;
     uint8_t* tile_count = nullptr;
@@ -61,6 +65,7 @@ struct lag_ctx_s {
     const void* last_v1 = nullptr;
     // COMM
     lag::Comm* comm = nullptr;
+    lag::LocalGroup* group = nullptr;          // LAG_XCHG_LOCAL
     // LAG_XCHG_PEER_OVERLAP: the exchange runs in the first CTAs of the advect
     // pass 1 while the ghost-free tiles advect; deferred tile ids in defer_list
     void* xchg_fused = nullptr;                // non-null: lag_peer_exchange fills this XchgFused, no launch
@@ -84,4 +89,16 @@ void lag_comm_fill_args(lag_ctx_s* ctx, lag::AdvectArgs* a);
 lag_status lag_comm_post_advect(lag_ctx_s* ctx);
 bool lag_comm_overlap(lag_ctx_s* ctx);        // LAG_XCHG_PEER_OVERLAP with neighbours
 lag_status lag_comm_return_to_origin(lag_ctx_s* ctx);
+lag_status lag_comm_async_error(lag_ctx_s* ctx);   // ncclCommGetAsyncError poll
+// LAG_XCHG_LOCAL (lag_comm.cu): group cycle and write cycle
+struct lag_local_rec { float* v0; float* v1; double dt; bool v0_prev; };
+lag_status lag_local_record(lag_ctx_s* ctx, const lag_local_rec& r, bool* complete);
+lag_status lag_local_run_cycle(lag_ctx_s* ctx);   // ghost copy + appends (group-wide)
+lag_ctx_s* lag_local_member(lag_ctx_s* ctx, int r);
+const lag_local_rec& lag_local_recorded(lag_ctx_s* ctx, int r);
+int lag_local_size(lag_ctx_s* ctx);
+lag_status lag_local_flush(lag_ctx_s* ctx);       // first extract of the group: pending hand-offs
+bool lag_local_extracted(lag_ctx_s* ctx, bool* all);   // mark this block extracted
+bool lag_local_extracting(lag_ctx_s* ctx);        // some block extracted, not all
+void lag_local_leave(lag_ctx_s* ctx);
 void lag_comm_returned(lag_ctx_s* ctx, const float4** rec, int64_t* stride_f4, uint32_t* n);

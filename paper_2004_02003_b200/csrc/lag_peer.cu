@@ -245,7 +245,7 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
     x.nrecv = halo ? (with_v0 ? 2 * nb : nb) : 0;
     x.parity = q;
     x.rtotal = halo ? (with_v0 ? 2 : 1) * ps->halo_recv_floats : 0;
-    x.sx = ctx->ext[0]; x.sxy = ctx->ext[0] * ctx->ext[1]; x.dim = ctx->cfg.dim;
+    x.sx = ctx->sx; x.sxy = ctx->sxy; x.dim = ctx->cfg.dim;
     x.seq = seq;
     x.do_append = append_args ? 1 : 0;
     x.done_ctas = ps->done_ctas;

@@ -19,9 +19,10 @@ LIB_PATH = os.environ.get("LAG_LIB") or os.path.join(HERE, "liblag.so")
 LAG_OK, LAG_EINVAL, LAG_ESTATE, LAG_EEMPTY, LAG_ENOMEM = 0, -1, -2, -3, -4
 LAG_ECUDA, LAG_ENCCL, LAG_EOVERFLOW, LAG_EGHOST, LAG_ENONFINITE = -5, -6, -7, -8, -9
 LAG_BTO, LAG_COMM = 0, 1
-LAG_XCHG_NCCL, LAG_XCHG_PEER, LAG_XCHG_PEER_OVERLAP = 0, 1, 2
+LATCHED = (-7, -8, -9)       # async conditions lag_extract reports after writing its outputs
+LAG_XCHG_NCCL, LAG_XCHG_PEER, LAG_XCHG_PEER_OVERLAP, LAG_XCHG_LOCAL = 0, 1, 2, 3
 LAG_VALID, LAG_TERM_BOUNDARY, LAG_EXIT_DOMAIN = 0, 1, 2
-LAG_ABI_VERSION = 2          # include/lag.h
+LAG_ABI_VERSION = 3          # include/lag.h
 LAG_NO_RESEED = 1
 LAG_ASYNC = 2
 STATUS_NAMES = {0: "LAG_OK", -1: "LAG_EINVAL", -2: "LAG_ESTATE", -3: "LAG_EEMPTY",
@@ -31,7 +32,7 @@ STATUS_NAMES = {0: "LAG_OK", -1: "LAG_EINVAL", -2: "LAG_ESTATE", -3: "LAG_EEMPTY
 # every symbol include/lag.h declares
 EXPORTS = ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_extract_ex", "lag_stats",
            "lag_destroy", "lag_last_error", "lag_nccl_unique_id", "lag_kernel_launches",
-           "lag_abi_version", "lag_gridfill", "lag_ftle", "lag_stitch")
+           "lag_abi_version", "lag_gridfill", "lag_ftle", "lag_stitch", "lag_local_group")
 
 
 class LagError(RuntimeError):
@@ -47,6 +48,7 @@ class lag_config(ctypes.Structure):
                 ("block_hi", ctypes.c_int64 * 3), ("ghost", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("layout", ctypes.c_int32 * 3), ("exchange", ctypes.c_int32),
+                ("row_pitch_bytes", ctypes.c_int64),
                 ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
 
 
@@ -75,9 +77,11 @@ def load(path: str = LIB_PATH):
     lib.lag_init.argtypes = [P(lag_config), P(vp)]
     lib.lag_seed.argtypes = [vp, ctypes.c_int32, P(ctypes.c_int64)]
     lib.lag_advect_cycle.argtypes = [vp, vp, vp, ctypes.c_double]
-    lib.lag_extract.argtypes = [vp, vp, vp, vp, ctypes.c_int64, P(ctypes.c_int64), ctypes.c_uint32]
-    if hasattr(lib, "lag_extract_ex"):      # (older experiment builds lack it)
-        lib.lag_extract_ex.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int64, P(ctypes.c_int64), ctypes.c_uint32]
+    lib.lag_extract.argtypes = [vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int64, P(ctypes.c_int64),
+                                ctypes.c_uint32]
+    lib.lag_extract_ex.argtypes = [vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int64, P(ctypes.c_int64),
+                                   ctypes.c_uint32]
+    lib.lag_local_group.argtypes = [P(vp), ctypes.c_int32]
     lib.lag_stats.argtypes = [vp, P(lag_stats_t)]
     lib.lag_destroy.argtypes = [vp]
     lib.lag_last_error.argtypes = [vp]
@@ -98,7 +102,8 @@ def load(path: str = LIB_PATH):
     if hasattr(lib, "lag_gridfill"):
         lib.lag_gridfill.argtypes = [ctypes.c_int32, P(ctypes.c_int64), ctypes.c_int32, vp, vp, vp, vp, vp]
     for name in ("lag_init", "lag_seed", "lag_advect_cycle", "lag_extract", "lag_extract_ex", "lag_stats",
-                 "lag_destroy", "lag_nccl_unique_id", "lag_gridfill", "lag_ftle", "lag_stitch"):
+                 "lag_destroy", "lag_nccl_unique_id", "lag_gridfill", "lag_ftle", "lag_stitch",
+                 "lag_local_group"):
         if hasattr(lib, name):
             getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -146,11 +151,12 @@ def make_config(dim: int, global_nodes: Sequence[int], origin: Sequence[float],
                 mode: int = LAG_BTO, ghost: int = 0, device: int = 0, rank: int = 0,
                 nranks: int = 1, layout: Sequence[int] = (1, 1, 1),
                 nccl_id: Optional[bytes] = None, stream: Optional[int] = None,
-                exchange: int = 0) -> lag_config:
+                exchange: int = 0, row_pitch_bytes: int = 0) -> lag_config:
     c = lag_config()
     c.dim, c.mode, c.ghost, c.device = dim, mode, ghost, device
     c.rank, c.nranks = rank, nranks
     c.exchange = int(exchange)
+    c.row_pitch_bytes = int(row_pitch_bytes)
     for a in range(3):
         c.global_nodes[a] = int(global_nodes[a])
         c.origin[a] = float(origin[a])
@@ -181,28 +187,34 @@ def lag_advect_cycle(ctx, v_t, v_t1, dt: float) -> None:
     _check(load().lag_advect_cycle(ctx, _addr(v_t), _addr(v_t1), float(dt)), ctx)
 
 
-def lag_extract(ctx, start=None, end=None, status=None, capacity: Optional[int] = None,
-                flags: int = 0) -> int:
+def lag_extract(ctx, interval_index: int, start=None, end=None, status=None,
+                capacity: Optional[int] = None, flags: int = 0) -> int:
     """Returns n; outputs are written into the given buffers.  Latched async
     errors raise LagError after the outputs were written."""
     n = ctypes.c_int64(0)
     if capacity is None:
         caps = [x.shape[0] for x in (start, end, status) if x is not None]
         capacity = min(caps) if caps else 0
-    _check(load().lag_extract(ctx, _addr(start), _addr(end), _addr(status), int(capacity),
-                              ctypes.byref(n), int(flags)), ctx)
+    _check(load().lag_extract(ctx, int(interval_index), _addr(start), _addr(end), _addr(status),
+                              int(capacity), ctypes.byref(n), int(flags)), ctx)
     return n.value
 
 
-def lag_extract_ex(ctx, start=None, end=None, status=None, term_cycle=None,
+def lag_extract_ex(ctx, interval_index: int, start=None, end=None, status=None, term_cycle=None,
                    capacity: Optional[int] = None, flags: int = 0) -> int:
     n = ctypes.c_int64(0)
     if capacity is None:
         caps = [x.shape[0] for x in (start, end, status, term_cycle) if x is not None]
         capacity = min(caps) if caps else 0
-    _check(load().lag_extract_ex(ctx, _addr(start), _addr(end), _addr(status), _addr(term_cycle),
-                                 int(capacity), ctypes.byref(n), int(flags)), ctx)
+    _check(load().lag_extract_ex(ctx, int(interval_index), _addr(start), _addr(end), _addr(status),
+                                 _addr(term_cycle), int(capacity), ctypes.byref(n), int(flags)), ctx)
     return n.value
+
+
+def lag_local_group(ctxs) -> None:
+    """Connect LAG_XCHG_LOCAL contexts (ctxs[r] = rank r) into one group."""
+    arr = (ctypes.c_void_p * len(ctxs))(*[c.value if isinstance(c, ctypes.c_void_p) else c for c in ctxs])
+    _check(load().lag_local_group(arr, len(ctxs)))
 
 
 def lag_stats(ctx) -> dict:
@@ -291,6 +303,7 @@ class Context:
         self.dim = cfg.dim
         self.ctx = lag_init(cfg)
         self.n = 0
+        self.interval = 0               # next lag_extract interval_index
 
     def seed(self, stride: int) -> int:
         self.n = lag_seed(self.ctx, stride)
@@ -300,9 +313,17 @@ class Context:
         lag_advect_cycle(self.ctx, v_t, v_t1, dt)
 
     def extract(self, start=None, end=None, status=None, flags: int = 0, term_cycle=None) -> int:
-        if term_cycle is not None:
-            return lag_extract_ex(self.ctx, start, end, status, term_cycle, flags=flags)
-        return lag_extract(self.ctx, start, end, status, flags=flags)
+        try:
+            if term_cycle is not None:
+                n = lag_extract_ex(self.ctx, self.interval, start, end, status, term_cycle, flags=flags)
+            else:
+                n = lag_extract(self.ctx, self.interval, start, end, status, flags=flags)
+        except LagError as e:
+            if e.status in LATCHED:          # outputs written, interval extracted, error reported
+                self.interval += 1
+            raise
+        self.interval += 1
+        return n
 
     def stats(self) -> dict:
         return lag_stats(self.ctx)
@@ -320,3 +341,31 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+class LocalGroup:
+    """The blocks of a decomposition as LAG_XCHG_LOCAL COMM contexts on one
+    device (marshalling only): cfgs[r] is rank r's configuration."""
+
+    def __init__(self, cfgs):
+        self.blocks = [Context(c) for c in cfgs]
+        lag_local_group([b.ctx for b in self.blocks])
+
+    def seed(self, stride: int):
+        return [b.seed(stride) for b in self.blocks]
+
+    def advect(self, v_t, v_t1, dt: float) -> None:
+        """v_t[r], v_t1[r]: block r's device slices; the last call enqueues the cycle."""
+        for b, a0, a1 in zip(self.blocks, v_t, v_t1):
+            b.advect(a0, a1, dt)
+
+    def extract(self, outs, flags: int = 0):
+        """outs[r] = (start, end, status) device buffers of block r."""
+        return [b.extract(*o, flags=flags) for b, o in zip(self.blocks, outs)]
+
+    def stats(self):
+        return [b.stats() for b in self.blocks]
+
+    def close(self):
+        for b in self.blocks:
+            b.close()

@@ -29,7 +29,8 @@ import lag_inputs as L  # noqa: E402
 import paper_2004_02003_b200 as P  # noqa: E402
 
 
-def run_block(cfg, block, layout, rank, world, mode, slices, stride, nccl_id=None, exchange=0):
+def run_block(cfg, block, layout, rank, world, mode, slices, stride, nccl_id=None, exchange=0,
+              reseed_mid=None):
     g = cfg["grid"]
     ghost = 1 if mode == P.LAG_COMM else 0
     lo = [block.lo[a] - ghost if a < g.dim else 0 for a in range(3)]
@@ -55,6 +56,12 @@ def run_block(cfg, block, layout, rank, world, mode, slices, stride, nccl_id=Non
                        nccl_id=nccl_id, stream=s.cuda_stream, exchange=exchange)
     ctx = P.Context(pc)
     n = ctx.seed(stride)
+    if reseed_mid:
+        # a reseed in the middle of an interval (no write cycle): the hand-offs
+        # in flight must be dropped, so the interval that follows is a fresh one
+        for k in range(reseed_mid):
+            ctx.advect(dev[k], dev[k + 1], cfg["dt"])
+        n = ctx.seed(stride)
     for k in range(len(dev) - 1):
         ctx.advect(dev[k], dev[k + 1], cfg["dt"])
     start = torch.empty((n, g.dim), dtype=torch.float64, device="cuda")
@@ -99,6 +106,10 @@ def main():
     dist.broadcast_object_list(obj3, src=0)
     ovl = run_block(cfg, me, layout, rank, world, P.LAG_COMM, slices, stride, nccl_id=obj3[0],
                     exchange=P.LAG_XCHG_PEER_OVERLAP)
+    obj4 = [P.lag_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj4, src=0)
+    rsd = run_block(cfg, me, layout, rank, world, P.LAG_COMM, slices, stride, nccl_id=obj4[0],
+                    exchange=P.LAG_XCHG_PEER, reseed_mid=5)
     bto = run_block(cfg, me, layout, rank, world, P.LAG_BTO, slices, stride)
     comm_all = [None] * world
     bto_all = [None] * world
@@ -108,6 +119,8 @@ def main():
     dist.all_gather_object(bto_all, bto)
     ovl_all = [None] * world
     dist.all_gather_object(ovl_all, ovl)
+    rsd_all = [None] * world
+    dist.all_gather_object(rsd_all, rsd)
     ok = True
     report = dict(config=config, scale=scale, world=world, layout=list(layout), cycles=ncyc)
     if rank == 0:
@@ -137,6 +150,9 @@ def main():
         report["overlap_vs_nccl_bitwise_mismatching_arrays"] = om
         report["overlap_sent"] = sum(int(c[3]["sent"]) for c in ovl_all)
         ok &= om == 0 and report["overlap_sent"] == sent
+        rm = sum(int(not np.array_equal(x, y)) for c, rz in zip(peer_all, rsd_all) for x, y in zip(c[:3], rz[:3]))
+        report["peer_mid_reseed_vs_fresh_mismatching_arrays"] = rm
+        ok &= rm == 0
         report["sent"] = sent
         report["received"] = recv
         ok &= mism == 0 and sent == recv and sent > 0

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", P.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (lag_\w+)", out))
     assert set(declared_functions()) <= exported
-    assert P.lag_abi_version() == 2
+    assert P.lag_abi_version() == P.LAG_ABI_VERSION == 3
 
 
 def test_library_is_sm100a():
@@ -50,6 +50,10 @@ def test_library_is_sm100a():
     (dict(mode=1, ghost=1, nranks=2, layout=(2, 1, 1)), "nccl_id"),
     (dict(mode=1, ghost=1, nranks=2, layout=(3, 1, 1)), "layout"),
     (dict(global_nodes=(2 ** 12, 2 ** 12, 2 ** 12), block_hi=(2 ** 12, 2 ** 12, 2 ** 12)), "bits"),
+    (dict(row_pitch_bytes=12 * 7), "row_pitch"),          # shorter than a row of 8 nodes
+    (dict(row_pitch_bytes=100), "row_pitch"),             # not whole nodes
+    (dict(mode=1, ghost=1, nranks=65, layout=(65, 1, 1), global_nodes=(130, 8, 8), block_hi=(2, 8, 8),
+          exchange=3), "64"),
 ])
 def test_init_rejects_bad_configurations(kw, frag):
     base = dict(dim=3, global_nodes=(8, 8, 8), origin=(0, 0, 0), spacing=(1, 1, 1),

@@ -1,0 +1,220 @@
+"""COMM baseline on ONE GPU: the blocks of a decomposition as LAG_XCHG_LOCAL
+contexts of one process (lag_local_group).  The exchange (ghost layers from
+the neighbours' slice arrays, hand-offs appended from their slots, return to
+origin at the write cycle) runs through the same advect kernel, append and
+scatter code as the NCCL/peer transports, so this covers the COMM rows
+(halo fill, particle hand-off, return to origin) on the
+driver's 1-GPU box:
+
+  * COMM over all blocks == the single-block run of the whole domain,
+    BITWISE (decomposition invariance), with the ghost layers
+    poisoned with NaN until the exchange fills them;
+  * the single-block run vs the fp64 oracle (north-star rule);
+  * hand-offs happen (sent == received > 0) and every seed comes back to its
+    origin block at the write cycle, over several intervals (deferred reseed);
+  * padded rows (row_pitch_bytes) give bitwise the dense result.
+"""
+import numpy as np
+import pytest
+
+import lag_inputs as L
+import oracle
+from helpers import global_slices, gpu_block, compare
+
+pytestmark = pytest.mark.gpu
+
+
+def poisoned_block_slice(V, g, b, ghost, pad=0):
+    """Block slice with `ghost` layers, ghost nodes NaN (only the exchange may
+    fill them), rows padded by `pad` NaN nodes (row_pitch_bytes)."""
+    s = np.array(L.cut_block_slice(V, g, b, ghost), dtype=np.float32)
+    if ghost:
+        for ax in range(g.dim):
+            nax = s.ndim - 2 - ax
+            for k in list(range(ghost)) + list(range(s.shape[nax] - ghost, s.shape[nax])):
+                idx = [slice(None)] * s.ndim
+                idx[nax] = k
+                s[tuple(idx)] = np.nan
+    if pad:
+        shape = list(s.shape)
+        shape[-2] += pad
+        p = np.full(shape, np.nan, dtype=np.float32)
+        p[..., :s.shape[-2], :] = s
+        s = p
+    return s
+
+
+def run_local(cfg, layout, slices_per_interval, stride, pad=0, frozen=False, reseed_mid=None):
+    """All blocks of `layout` as one LAG_XCHG_LOCAL group on cuda:0.  Returns,
+    per interval, per block (start, end, status) and the group's stats."""
+    import torch
+    import paper_2004_02003_b200 as P
+    g = cfg["grid"]
+    blocks = L.decompose(g, layout)
+    s = torch.cuda.current_stream()
+    cfgs = []
+    for b in blocks:
+        ext = L.block_slice_extent(g, b, 1)
+        pitch = (ext[0] + pad) * g.dim * 4 if pad else 0
+        cfgs.append(P.make_config(g.dim, g.nodes, g.origin, g.spacing, b.lo, b.hi, mode=P.LAG_COMM,
+                                  ghost=1, rank=b.rank, nranks=len(blocks), layout=layout,
+                                  stream=s.cuda_stream, exchange=P.LAG_XCHG_LOCAL,
+                                  row_pitch_bytes=pitch))
+    grp = P.LocalGroup(cfgs)
+    results, stats = [], []
+    try:
+        ns = grp.seed(stride)
+        for it, sl in enumerate(slices_per_interval):
+            dev = [[torch.from_numpy(poisoned_block_slice(V, g, b, 1, pad)).cuda() for b in blocks] for V in sl]
+            for k in range(len(sl) - 1):
+                if reseed_mid is not None and it == 0 and k == reseed_mid:
+                    grp.seed(stride)                # mid-interval reseed: in-flight hand-offs dropped
+                    break
+                grp.advect(dev[k], dev[k] if frozen else dev[k + 1], cfg["dt"])
+            if reseed_mid is not None and it == 0:
+                continue
+            outs = [(torch.empty((n, g.dim), dtype=torch.float64, device="cuda"),
+                     torch.empty((n, g.dim), dtype=torch.float64, device="cuda"),
+                     torch.empty((n,), dtype=torch.uint8, device="cuda")) for n in ns]
+            stats.append(grp.stats())               # before the write cycle: hand-offs in flight
+            grp.extract(outs)
+            results.append([tuple(x.cpu().numpy() for x in o) for o in outs])
+    finally:
+        grp.close()
+    return blocks, results, stats
+
+
+def assemble(g, blocks, per_block, stride):
+    """Scatter per-block flow maps into the global seed order."""
+    gs = oracle.seeds(g, (0, 0, 0), g.nodes, stride)
+    key = {tuple(x): i for i, x in enumerate(gs.tolist())}
+    n = gs.shape[0]
+    start = np.full((n, g.dim), np.nan)
+    end = np.full((n, g.dim), np.nan)
+    status = np.full(n, 255, dtype=np.uint8)
+    for b, (s, e, st) in zip(blocks, per_block):
+        idx = np.array([key[tuple(x)] for x in oracle.seeds(g, b.lo, b.hi, stride).tolist()])
+        start[idx], end[idx], status[idx] = s, e, st
+    return start, end, status
+
+
+@pytest.mark.parametrize("config,scale,layout,cycles,dtmul", [
+    ("C2", 33, (2, 2, 2), 25, 4.0),
+    ("C5", 20, (2, 1, 1), 25, 4.0),
+    ("C1", 0, (2, 2, 1), 20, 0.25),
+    ("C4", 65, (2, 2, 2), 10, 4.0),
+])
+def test_local_comm_equals_single_block_and_oracle(config, scale, layout, cycles, dtmul):
+    cfg = L.make_config(config, scale=scale or None, nranks=int(np.prod(layout)))
+    cfg["dt"] *= dtmul                                # more hand-offs per interval
+    g = cfg["grid"]
+    stride = 2 if config == "C4" else cfg["stride"]
+    sl = global_slices(cfg, cycles)
+    blocks, res, stats = run_local(cfg, layout, [sl], stride)
+    whole = L.Block(0, (0, 0, 0), (0, 0, 0), g.nodes)
+    single = gpu_block(cfg, whole, sl, stride)
+    got = assemble(g, blocks, res[0], stride)
+    for a, b in zip(got, single[:3]):
+        assert np.array_equal(a, b)                   # bitwise decomposition invariance
+    orc = oracle.run_interval(g, (0, 0, 0), g.nodes, stride, sl, cfg["dt"], mode=oracle.BTO,
+                              faces=((0, 0, 0), g.nodes))
+    compare(cfg, orc, *single[:3], label=f"{config} single/comm")
+    sent = sum(s["sent"] for s in stats[0])
+    recv = sum(s["received"] for s in stats[0])
+    assert sent > 0 and recv > 0
+    assert all(s["device_error"] == 0 for s in stats[0])
+
+
+def test_local_comm_several_intervals_return_to_origin():
+    """Three intervals on one group: the write cycle returns every particle to
+    its origin block, the group reseeds after its last extract, and each
+    interval equals a fresh single-block run bitwise."""
+    cfg = L.make_config("C2", scale=29, nranks=8)
+    cfg["dt"] *= 4.0
+    g = cfg["grid"]
+    I = 12
+    allsl = global_slices(cfg, 3 * I)
+    per = [allsl[i * I:(i + 1) * I + 1] for i in range(3)]
+    blocks, res, _ = run_local(cfg, (2, 2, 2), per, 1)
+    whole = L.Block(0, (0, 0, 0), (0, 0, 0), g.nodes)
+    for it in range(3):
+        single = gpu_block(cfg, whole, per[it], 1)
+        got = assemble(g, blocks, res[it], 1)
+        for a, b in zip(got, single[:3]):
+            assert np.array_equal(a, b), f"interval {it}"
+        moved = np.abs(got[1] - got[0]).max()
+        assert moved > 2 * min(g.spacing)              # particles crossed block faces
+
+
+def test_local_comm_padded_rows_and_frozen_snapshot():
+    cfg = L.make_config("C2", scale=33, nranks=8)
+    cfg["dt"] *= 4.0
+    sl = global_slices(cfg, 10)
+    blocks, dense, _ = run_local(cfg, (2, 2, 2), [sl], 1)
+    _, padded, _ = run_local(cfg, (2, 2, 2), [sl], 1, pad=3)
+    for a, b in zip(dense[0], padded[0]):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    # frozen snapshot (v_t1 = v_t): equals the single block
+    g = cfg["grid"]
+    _, fz, _ = run_local(cfg, (2, 2, 2), [sl], 1, frozen=True)
+    whole = L.Block(0, (0, 0, 0), (0, 0, 0), g.nodes)
+    single = gpu_block(cfg, whole, sl, 1, same_tensor=True)
+    for a, b in zip(assemble(g, blocks, fz[0], 1), single[:3]):
+        assert np.array_equal(a, b)
+
+
+def test_local_comm_mid_interval_reseed_drops_in_flight_particles():
+    """lag_seed on every block in the middle of an interval discards the
+    particles in flight: the next interval equals a fresh run bitwise."""
+    cfg = L.make_config("C2", scale=25, nranks=8)
+    cfg["dt"] *= 4.0
+    g = cfg["grid"]
+    sl = global_slices(cfg, 16)
+    blocks, res, _ = run_local(cfg, (2, 2, 2), [sl[:9], sl[8:]], 1, reseed_mid=6)
+    single = gpu_block(cfg, L.Block(0, (0, 0, 0), (0, 0, 0), g.nodes), sl[8:], 1)
+    for a, b in zip(assemble(g, blocks, res[0], 1), single[:3]):
+        assert np.array_equal(a, b)
+
+
+def test_local_comm_errors():
+    import torch
+    import paper_2004_02003_b200 as P
+    cfg = L.make_config("C2", scale=17, nranks=2)
+    g = cfg["grid"]
+    blocks = L.decompose(g, (2, 1, 1))
+    s = torch.cuda.current_stream()
+    cfgs = [P.make_config(3, g.nodes, g.origin, g.spacing, b.lo, b.hi, mode=P.LAG_COMM, ghost=1,
+                          rank=b.rank, nranks=2, layout=(2, 1, 1), stream=s.cuda_stream,
+                          exchange=P.LAG_XCHG_LOCAL) for b in blocks]
+    # wrong rank order
+    c0, c1 = P.Context(cfgs[0]), P.Context(cfgs[1])
+    with pytest.raises(P.LagError) as e:
+        P.lag_local_group([c1.ctx, c0.ctx])
+    assert e.value.status == P.LAG_EINVAL
+    with pytest.raises(P.LagError) as e:           # seed without a group
+        c0.seed(1)
+    assert e.value.status == P.LAG_ESTATE
+    c0.close(); c1.close()
+    grp = P.LocalGroup(cfgs)
+    ns = grp.seed(1)
+    vs = [torch.zeros(tuple(reversed(L.block_slice_extent(g, b, 1))) + (3,), device="cuda") for b in blocks]
+    grp.blocks[0].advect(vs[0], vs[0], 0.01)
+    with pytest.raises(P.LagError) as e:           # twice in one group cycle
+        grp.blocks[0].advect(vs[0], vs[0], 0.01)
+    assert e.value.status == P.LAG_ESTATE
+    with pytest.raises(P.LagError) as e:           # host slice
+        grp.blocks[1].advect(vs[1].cpu(), vs[1].cpu(), 0.01)
+    assert e.value.status == P.LAG_EINVAL
+    grp.blocks[1].advect(vs[1], vs[1], 0.01)        # completes the cycle
+    out0 = [torch.empty((ns[0], 3), dtype=torch.float64, device="cuda") for _ in range(2)]
+    grp.blocks[0].extract(out0[0], out0[1])
+    with pytest.raises(P.LagError) as e:           # block 1 has not extracted yet
+        grp.blocks[0].advect(vs[0], vs[0], 0.01)
+    assert e.value.status == P.LAG_ESTATE
+    with pytest.raises(P.LagError) as e:           # interval index out of order
+        P.lag_extract(grp.blocks[1].ctx, 5)
+    assert e.value.status == P.LAG_ESTATE
+    grp.blocks[1].extract()
+    grp.advect(vs, vs, 0.01)                        # the group reseeded: a new interval runs
+    grp.close()

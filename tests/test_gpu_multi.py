@@ -38,3 +38,5 @@ def test_mgpu_comm_and_bto(nproc, config, scale):
     # exchange overlapped with the ghost-free tiles (ghosts poisoned with NaN
     # until the exchange fills them): bitwise the NCCL result
     assert rep["overlap_vs_nccl_bitwise_mismatching_arrays"] == 0 and rep["overlap_sent"] == rep["sent"]
+    # a reseed in the middle of an interval drops the hand-offs in flight
+    assert rep["peer_mid_reseed_vs_fresh_mismatching_arrays"] == 0

@@ -186,6 +186,11 @@ def test_errors_empty_block_and_order():
     with pytest.raises(P.LagError) as e:
         ctx.advect(v, v, -1.0)
     assert e.value.status == P.LAG_EINVAL
+    with pytest.raises(P.LagError) as e:     # write cycles come in order (interval 0 first)
+        P.lag_extract(ctx.ctx, 1)
+    assert e.value.status == P.LAG_ESTATE
+    assert P.lag_extract(ctx.ctx, 0) == 1
+    assert P.lag_extract(ctx.ctx, 1) == 1
     ctx.close()
 
 
@@ -335,26 +340,6 @@ def test_termination_cycles_match_oracle():
     assert (status != 0).sum() > 0
     assert np.array_equal(tc[same], orc.term_cycle[same])
     assert (tc[status == 0] == -1).all()
-
-
-@pytest.mark.parametrize("case", ["c2_blocks", "c5_block", "ragged"])
-def test_brick_kernel_opt_in(case, monkeypatch):
-    """The opt-in shared-memory brick kernel (LAG_BRICK=1, lag_brick.cuh:
-    per-brick velocity boxes staged by bulk copies, double-buffered) matches
-    the oracle like the default advect kernel: 8 BTO blocks, a block with
-    both global faces, and odd block offsets (ragged bricks, clipped rows)."""
-    monkeypatch.setenv("LAG_BRICK", "1")
-    if case == "c2_blocks":
-        cfg = L.make_config("C2", scale=33)
-        res = _run_config(cfg, cfg["interval"])
-        assert sum(r["term"] for r in res) > 0
-    elif case == "c5_block":
-        cfg = L.make_config("C5", scale=40, nranks=1)
-        _run_config(cfg, 25)
-    else:
-        cfg = L.make_config("C2", scale=29)
-        b = L.Block(0, (0, 0, 0), (3, 2, 5), (26, 23, 19))
-        _run_config(cfg, 8, stride=1, blocks=[b])
 
 
 def test_async_extract_matches_sync_and_keeps_errors_latched():
