@@ -330,75 +330,137 @@ def measure_secondary(name, rank, world, steps, warmup, flush):
 
 def measure_c2(steps, warmup, flush):
     """configs[1] on one GPU: C2 = ABC 128^3 as 8 blocks (2x2x2), stride 1,
-    interval 25, BTO — the 8 block contexts share the GPU, each on its own
-    stream, launched cycle by cycle.  Device time per cycle = a window from an
-    event after the L2 flush to the join of the 8 streams (max over blocks)."""
+    interval 25, BTO vs COMM.  BTO: 8 contexts, one stream each.  COMM: the
+    same 8 blocks as one LAG_XCHG_LOCAL group (ghost layers copied from the
+    neighbours' slices, hand-offs appended from their slots every cycle,
+    return to origin at the write cycle), one stream each.  Each arm's
+    interval is captured as three CUDA graphs (seed, the 25 cycles, the write
+    cycle) and replayed: at 262144 particles per block the cycle is
+    launch-bound, which the graph removes.  L2 is flushed
+    before every interval (the whole C2 working set, ~86 MB, fits in L2)."""
     import torch
     import lag_inputs as L
     import paper_2004_02003_b200 as P
     cfg = L.make_config("C2")
     g = cfg["grid"]
+    I = cfg["interval"]
     blocks = L.decompose(g, cfg["layout"])
-    main_s = torch.cuda.current_stream()
-    arms = []
-    for b in blocks:
-        st = torch.cuda.Stream()
-        ext = L.block_slice_extent(g, b, 0)
-        hi = [b.lo[a] + ext[a] for a in range(3)]
-        sl = [L.field_at_nodes(cfg["field"], g, k * cfg["dt"], lo=b.lo, hi=hi, device="cuda",
-                               backend="torch").contiguous() for k in range(cfg["interval"] + 1)]
-        ctx = P.Context(P.make_config(g.dim, g.nodes, g.origin, g.spacing, b.lo, b.hi,
-                                      stream=st.cuda_stream))
-        n = ctx.seed(cfg["stride"])
-        out = [torch.empty((n, 3), dtype=torch.float64, device="cuda"), None,
-               torch.empty((n,), dtype=torch.uint8, device="cuda")]
-        out[1] = torch.empty_like(out[0])
-        arms.append((st, sl, ctx, out))
-    torch.cuda.synchronize()
+    main_s = torch.cuda.Stream()          # graphs are captured on a non-default stream
 
-    def window(fn):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(main_s)
-        for st, sl, ctx, out in arms:
-            st.wait_event(e0)
-        for i, (st, sl, ctx, out) in enumerate(arms):
-            fn(i, st, sl, ctx, out)
-        for st, *_ in arms:
+    def build(mode):
+        ghost = 1 if mode == P.LAG_COMM else 0
+        streams = [torch.cuda.Stream() for _ in blocks]
+        cfgs, slices = [], []
+        for b, st in zip(blocks, streams):
+            lo = [b.lo[a] - ghost for a in range(3)]
+            ext = L.block_slice_extent(g, b, ghost)
+            hi = [lo[a] + ext[a] for a in range(3)]
+            slices.append([L.field_at_nodes(cfg["field"], g, k * cfg["dt"], lo=lo, hi=hi, device="cuda",
+                                            backend="torch").contiguous() for k in range(I + 1)])
+            cfgs.append(P.make_config(g.dim, g.nodes, g.origin, g.spacing, b.lo, b.hi, mode=mode,
+                                      ghost=ghost, rank=b.rank if mode == P.LAG_COMM else 0,
+                                      nranks=len(blocks) if mode == P.LAG_COMM else 1,
+                                      layout=cfg["layout"] if mode == P.LAG_COMM else (1, 1, 1),
+                                      stream=st.cuda_stream,
+                                      exchange=P.LAG_XCHG_LOCAL if mode == P.LAG_COMM else 0))
+        if mode == P.LAG_COMM:
+            grp = P.LocalGroup(cfgs)
+            ctxs = grp.blocks
+        else:
+            grp = None
+            ctxs = [P.Context(c) for c in cfgs]
+        ns = [c.seed(cfg["stride"]) for c in ctxs]
+        outs = [(torch.empty((n, 3), dtype=torch.float64, device="cuda"),
+                 torch.empty((n, 3), dtype=torch.float64, device="cuda"),
+                 torch.empty((n,), dtype=torch.uint8, device="cuda")) for n in ns]
+        torch.cuda.synchronize()
+
+        def fork():
             ev = torch.cuda.Event()
-            ev.record(st)
-            main_s.wait_event(ev)
-        e1.record(main_s)
-        return (e0, e1)
+            ev.record(main_s)
+            for st in streams:
+                st.wait_event(ev)
 
-    def run(nsteps):
-        wins = []
+        def join():
+            for st in streams:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                main_s.wait_event(ev)
+
+        def seed_all():
+            for c in ctxs:
+                c.seed(cfg["stride"])
+
+        def cycles_all():
+            for k in range(I):
+                for c, sl in zip(ctxs, slices):
+                    c.advect(sl[k], sl[k + 1], cfg["dt"])
+
+        def extract_all():
+            for c, o in zip(ctxs, outs):
+                c.extract(*o, flags=P.LAG_NO_RESEED | P.LAG_ASYNC)
+
+        graphs = []
+        for fn in (seed_all, cycles_all, extract_all):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=main_s):
+                fork()
+                fn()
+                join()
+            graphs.append(gr)
+        torch.cuda.synchronize()
+        return dict(ctxs=ctxs, grp=grp, graphs=graphs, n=sum(ns))
+
+    def run(arm, nsteps):
+        t_int, t_cyc = [], []
         for _ in range(nsteps):
             if flush is not None:
                 flush.zero_()
-            wins.append(window(lambda i, st, sl, ctx, out: ctx.seed(cfg["stride"])))
-            for c in range(cfg["interval"]):
-                if flush is not None:
-                    flush.zero_()
-                wins.append(window(lambda i, st, sl, ctx, out: ctx.advect(sl[c], sl[c + 1], cfg["dt"])))
-            wins.append(window(lambda i, st, sl, ctx, out: ctx.extract(
-                out[0], out[1], out[2], flags=P.LAG_NO_RESEED | P.LAG_ASYNC)))
-        torch.cuda.synchronize()
-        return sum(a.elapsed_time(b) for a, b in wins)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record(main_s)
+            arm["graphs"][0].replay()
+            ev[1].record(main_s)
+            arm["graphs"][1].replay()
+            ev[2].record(main_s)
+            arm["graphs"][2].replay()
+            ev[3].record(main_s)
+            torch.cuda.synchronize()
+            t_int.append(ev[0].elapsed_time(ev[3]))
+            t_cyc.append(ev[1].elapsed_time(ev[2]))
+        return t_int, t_cyc
 
-    run(warmup)
-    ps0 = sum(ctx.stats()["particle_steps"] for _, _, ctx, _ in arms)
-    ms = run(steps)
-    stats = [ctx.stats() for _, _, ctx, _ in arms]
-    if any(s["device_error"] for s in stats):
-        raise RuntimeError("latched device error in the C2 leg")
-    ps = sum(s["particle_steps"] for s in stats) - ps0
-    for _, _, ctx, _ in arms:
-        ctx.close()
-    return {"workload": "C2 (configs[1]): ABC 128^3 as 8 blocks (2x2x2) on one GPU, one context and "
-                        "stream per block, stride 1 (2097152 particles), interval 25, BTO",
-            "value": ps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps,
-            "discarded_last_interval": int(sum(s["term_boundary"] + s["exit_domain"] for s in stats)),
-            "comm": "not measured on one GPU (one NCCL rank per device); see the C5 'comm' arm at N >= 2"}
+    res = {}
+    for name, mode in (("bto", P.LAG_BTO), ("comm", P.LAG_COMM)):
+        arm = build(mode)
+        with torch.cuda.stream(main_s):
+            run(arm, warmup)
+            ps0 = sum(c.stats()["particle_steps"] for c in arm["ctxs"])
+            t_int, t_cyc = run(arm, steps)
+        stats = [c.stats() for c in arm["ctxs"]]
+        if any(st["device_error"] for st in stats):
+            raise RuntimeError(f"latched device error in the C2 {name} leg")
+        ps = sum(st["particle_steps"] for st in stats) - ps0
+        res[name] = {"value": ps / (sum(t_int) / 1e3), "unit": UNIT, "ms_per_step": sum(t_int) / steps,
+                     "ms_per_cycle": sum(t_cyc) / steps / I,
+                     "particle_steps_per_s_cycles_only": ps / (sum(t_cyc) / 1e3),
+                     "discarded_last_interval": int(sum(st["term_boundary"] + st["exit_domain"] for st in stats)),
+                     "sent_last_interval": int(sum(st["sent"] for st in stats)),
+                     "received_last_interval": int(sum(st["received"] for st in stats))}
+        if arm["grp"] is not None:
+            arm["grp"].close()
+        else:
+            for c in arm["ctxs"]:
+                c.close()
+        del arm
+        torch.cuda.synchronize()
+    return {"workload": "C2 (configs[1]): ABC 128^3 as 8 blocks (2x2x2) on one GPU, stride 1 "
+                        "(2097152 particles), interval 25; one stream per block; each interval replayed "
+                        "as CUDA graphs (seed | 25 cycles | write cycle); COMM = LAG_XCHG_LOCAL",
+            "bto": res["bto"], "comm": res["comm"],
+            "value": res["bto"]["value"], "unit": UNIT,
+            "bto_speedup_per_cycle": res["comm"]["ms_per_cycle"] / res["bto"]["ms_per_cycle"],
+            "bto_speedup_step": res["comm"]["ms_per_step"] / res["bto"]["ms_per_step"],
+            "l2": "flushed before every interval; the cycles of an interval run back to back"}
 
 
 def measured_peak():

@@ -95,9 +95,9 @@ typedef enum {
     LAG_XCHG_LOCAL = 3          /* several blocks on ONE device, driven by one host thread
                                    (lag_local_group): ghost layers are copied straight from
                                    the neighbours' slice arrays and hand-offs are appended
-                                   from the neighbours' slots, ordered by the group's single
-                                   stream (no NCCL, no flags, no spinning).  Bitwise equal
-                                   to the other transports.                                  */
+                                   from the neighbours' slots, ordered by stream events
+                                   (no NCCL, no flags, no spinning).  Bitwise equal to the
+                                   other transports.                                          */
 } lag_exchange;
 
 /* Per-basis-flow status returned by lag_extract. */
@@ -242,8 +242,11 @@ LAG_API lag_status lag_extract_ex(lag_ctx ctx, int64_t interval_index, double* s
 /*
  * lag_local_group — connect n COMM contexts created with exchange =
  * LAG_XCHG_LOCAL into one group: ctxs[r] must hold rank r of the same layout
- * (nranks = n <= 64), the same device and the same stream.  Call once, after
- * every lag_init and before the first lag_seed.  The group lives until its
+ * (nranks = n <= 64) on the same device; each may have its own stream (the
+ * blocks then advance concurrently; the group joins the streams with events
+ * around each exchange and write cycle, block 0's stream carries the
+ * exchange kernels).  Call once, after every lag_init and before the first
+ * lag_seed.  The group lives until its
  * last context is destroyed.  Not collective across processes: the whole
  * group is in this process (the single-GPU form of the COMM baseline, used
  * to run several blocks of a decomposition on one B200).

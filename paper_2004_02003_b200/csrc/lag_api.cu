@@ -757,6 +757,8 @@ extern "C" lag_status lag_extract_ex(lag_ctx ctx, int64_t interval_index, double
         bool all = false;
         lag_local_extracted(ctx, &all);
         if (all) {
+            // every block's gather is done before any block's list is reseeded
+            if ((st = lag_local_join_all(ctx)) != LAG_OK) return st;
             for (int q = 0; q < lag_local_size(ctx); ++q) {
                 lag_ctx_s* m = lag_local_member(ctx, q);
                 if (!m->reseed_pending) continue;

@@ -709,17 +709,20 @@ lag_status lag_comm_async_error(lag_ctx_s* ctx) {
 
 // ---------------------------------------------------------------------------
 // LAG_XCHG_LOCAL: the blocks of a decomposition as contexts of one process on
-// one device.  Per group cycle (enqueued by the call that completes it, on
-// the group's single stream, so stream order replaces every flag and wait):
+// one device, each on its own stream.  Per group cycle (enqueued by the call
+// that completes it; events replace every flag and wait):
+//   0. the group stream (block 0's) waits for every block's stream;
 //   1. one kernel copies every block's ghost layers of v_t1 (and of v_t when
 //      it is not the previous call's v_t1) from the neighbours' slice arrays;
-//   2. per block, append_body adds the hand-offs the neighbours' advect
-//      kernels left in their slots toward it (the previous cycle's, as in the
-//      NCCL transport) and zeroes those slot headers;
-//   3. per block, the advect kernel (lag_api.cu) writes leaving particles to
-//      its own slots.
-// The write cycle appends the last cycle's hand-offs once; each block then
-// gathers its basis flows from every block's lists (lag_api.cu).
+//   2. one kernel (blockIdx.y = block) appends to each block the hand-offs
+//      the neighbours' advect kernels left in their slots toward it (the
+//      previous cycle's, as in the NCCL transport) and zeroes those headers;
+//   3. every block's stream waits for that, then runs its advect kernel
+//      (lag_api.cu), which writes leaving particles to its own slots; the
+//      blocks advance concurrently.
+// The write cycle joins the streams, appends the last hand-offs once, and
+// each block gathers its basis flows from every block's lists (lag_api.cu);
+// the streams join again before the group reseeds.
 
 namespace lag {
 constexpr int kLocalMax = 64;
@@ -740,6 +743,14 @@ struct LocalCopyArgs {
     float* v1[kLocalMax];
     int sx[kLocalMax], sxy[kLocalMax];
 };
+
+// every block's append in one launch: blockIdx.y = block (AppendArgs are
+// fixed for the group's lifetime: lists, words, the neighbours' slots)
+__global__ void __launch_bounds__(256) local_append_kernel(const AppendArgs* __restrict__ app) {
+    const AppendArgs& a = app[blockIdx.y];
+    if (a.npeers == 0) return;
+    append_body(a, blockIdx.x, gridDim.x);
+}
 
 __global__ void __launch_bounds__(256) local_ghost_kernel(const LocalCopyArgs a) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * a.total;
@@ -774,6 +785,8 @@ struct LocalGroup {
     std::vector<LocalBox> boxes;
     LocalBox* d_boxes = nullptr;
     int64_t total = 0;
+    AppendArgs* d_app = nullptr;        // [n] per-block append arguments
+    std::vector<cudaEvent_t> ev;        // per block: join points
     int alive = 0;
 };
 }  // namespace lag
@@ -796,16 +809,39 @@ static AppendArgs local_append_args(lag_ctx_s* ctx) {
     return a;
 }
 
-static lag_status local_appends(lag_ctx_s* any) {
-    LocalGroup* g = any->group;
-    for (lag_ctx_s* ctx : g->m) {
-        if (!ctx || ctx->comm->peers.empty()) continue;
-        AppendArgs a = local_append_args(ctx);
-        append_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(a);
-        ++ctx->launches;
-        CKC(cudaGetLastError());
-        ctx->comm->pending = false;
+// The group stream waits for every block's stream (fan-in).
+static lag_status local_join_in(lag_ctx_s* ctx) {
+    LocalGroup* g = ctx->group;
+    cudaStream_t s0 = g->m[0]->stream;
+    for (size_t r = 1; r < g->m.size(); ++r) {
+        if (g->m[r]->stream == s0) continue;
+        CKC(cudaEventRecord(g->ev[r], g->m[r]->stream));
+        CKC(cudaStreamWaitEvent(s0, g->ev[r], 0));
     }
+    return LAG_OK;
+}
+
+// Every block's stream waits for the group stream (fan-out).
+static lag_status local_join_out(lag_ctx_s* ctx) {
+    LocalGroup* g = ctx->group;
+    cudaStream_t s0 = g->m[0]->stream;
+    CKC(cudaEventRecord(g->ev[0], s0));
+    for (size_t r = 1; r < g->m.size(); ++r)
+        if (g->m[r]->stream != s0) CKC(cudaStreamWaitEvent(g->m[r]->stream, g->ev[0], 0));
+    return LAG_OK;
+}
+
+// Appends of every block (one launch on the group stream).
+static lag_status local_appends(lag_ctx_s* ctx) {
+    LocalGroup* g = ctx->group;
+    lag_ctx_s* c0 = g->m[0];
+    bool any = false;
+    for (lag_ctx_s* c : g->m) any |= !c->comm->peers.empty();
+    if (!any) return LAG_OK;
+    local_append_kernel<<<dim3(std::max(1, c0->num_sms / 2), (unsigned)g->m.size()), 256, 0, c0->stream>>>(g->d_app);
+    ++ctx->launches;
+    CKC(cudaGetLastError());
+    for (lag_ctx_s* c : g->m) c->comm->pending = false;
     return LAG_OK;
 }
 
@@ -815,10 +851,10 @@ extern "C" lag_status lag_local_group(lag_ctx* ctxs, int32_t n) {
     for (int r = 0; r < n; ++r) {
         lag_ctx_s* c = ctxs[r];
         if (!c || c->cfg.mode != LAG_COMM || c->cfg.exchange != LAG_XCHG_LOCAL || c->cfg.rank != r ||
-            c->cfg.nranks != n || c->cfg.device != ctxs[0]->cfg.device || c->stream != ctxs[0]->stream ||
+            c->cfg.nranks != n || c->cfg.device != ctxs[0]->cfg.device ||
             c->cfg.dim != ctxs[0]->cfg.dim || c->cfg.ghost < 1) {
             lag_set_error(nullptr, "lag_local_group: context %d is not rank %d of an n = %d LAG_XCHG_LOCAL "
-                          "COMM group on the same device and stream", r, r, n);
+                          "COMM group on the same device", r, r, n);
             return LAG_EINVAL;
         }
         for (int a = 0; a < 3; ++a)
@@ -873,18 +909,27 @@ extern "C" lag_status lag_local_group(lag_ctx* ctxs, int32_t n) {
         }
     }
     ctx = ctxs[0];
-    if (!g->boxes.empty()) {
-        cudaError_t e = cudaMalloc(&g->d_boxes, sizeof(LocalBox) * g->boxes.size());
+    for (int r = 0; r < n; ++r) ctxs[r]->group = g;   // (local_append_args reads g->m)
+    std::vector<AppendArgs> app(n);
+    for (int r = 0; r < n; ++r) app[r] = local_append_args(ctxs[r]);
+    g->ev.assign(n, nullptr);
+    cudaError_t e = cudaSuccess;
+    for (int r = 0; r < n && e == cudaSuccess; ++r) e = cudaEventCreateWithFlags(&g->ev[r], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_app, sizeof(AppendArgs) * n);
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_app, app.data(), sizeof(AppendArgs) * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !g->boxes.empty()) {
+        e = cudaMalloc(&g->d_boxes, sizeof(LocalBox) * g->boxes.size());
         if (e == cudaSuccess)
             e = cudaMemcpy(g->d_boxes, g->boxes.data(), sizeof(LocalBox) * g->boxes.size(), cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) {
-            cudaFree(g->d_boxes);
-            delete g;
-            lag_set_error(nullptr, "lag_local_group: %s", cudaGetErrorString(e));
-            return LAG_ECUDA;
-        }
     }
-    for (int r = 0; r < n; ++r) ctxs[r]->group = g;
+    if (e != cudaSuccess) {
+        for (int r = 0; r < n; ++r) { ctxs[r]->group = nullptr; if (g->ev[r]) cudaEventDestroy(g->ev[r]); }
+        cudaFree(g->d_boxes);
+        cudaFree(g->d_app);
+        delete g;
+        lag_set_error(nullptr, "lag_local_group: %s", cudaGetErrorString(e));
+        return LAG_ECUDA;
+    }
     return LAG_OK;
 }
 
@@ -920,6 +965,9 @@ lag_status lag_local_record(lag_ctx_s* ctx, const lag_local_rec& rec, bool* comp
 lag_status lag_local_run_cycle(lag_ctx_s* ctx) {
     LocalGroup* g = ctx->group;
     const int n = (int)g->m.size();
+    lag_status st = local_join_in(ctx);
+    if (st != LAG_OK) return st;
+    lag_ctx_s* c0 = g->m[0];
     if (g->total > 0) {
         LocalCopyArgs a{};
         a.boxes = g->d_boxes;
@@ -934,11 +982,12 @@ lag_status lag_local_run_cycle(lag_ctx_s* ctx) {
             if (!g->rec[r].v0_prev) a.fill_v0 |= 1ull << r;
         }
         const int blocks = (int)std::min<int64_t>((2 * g->total + 255) / 256, (int64_t)ctx->num_sms * 8);
-        local_ghost_kernel<<<std::max(1, blocks), 256, 0, ctx->stream>>>(a);
+        local_ghost_kernel<<<std::max(1, blocks), 256, 0, c0->stream>>>(a);
         ++ctx->launches;
         CKC(cudaGetLastError());
     }
-    return local_appends(ctx);
+    if ((st = local_appends(ctx)) != LAG_OK) return st;
+    return local_join_out(ctx);
 }
 
 lag_ctx_s* lag_local_member(lag_ctx_s* ctx, int r) { return ctx->group->m[r]; }
@@ -952,7 +1001,16 @@ lag_status lag_local_flush(lag_ctx_s* ctx) {
         if (!c) { lag_set_error(ctx, "LAG_XCHG_LOCAL: a block of the group was destroyed"); return LAG_ESTATE; }
     bool pending = false;
     for (lag_ctx_s* c : g->m) pending |= c->comm->pending;
-    return pending ? local_appends(ctx) : LAG_OK;
+    // every block's last cycle is done before any block gathers from it
+    lag_status st = local_join_in(ctx);
+    if (st == LAG_OK && pending) st = local_appends(ctx);
+    if (st == LAG_OK) st = local_join_out(ctx);
+    return st;
+}
+
+lag_status lag_local_join_all(lag_ctx_s* ctx) {
+    lag_status st = local_join_in(ctx);
+    return st == LAG_OK ? local_join_out(ctx) : st;
 }
 
 bool lag_local_extracted(lag_ctx_s* ctx, bool* all) {
@@ -976,6 +1034,8 @@ void lag_local_leave(lag_ctx_s* ctx) {
     ctx->group = nullptr;
     if (--g->alive == 0) {
         cudaFree(g->d_boxes);
+        cudaFree(g->d_app);
+        for (cudaEvent_t e : g->ev) if (e) cudaEventDestroy(e);
         delete g;
     }
 }

@@ -98,6 +98,7 @@ lag_ctx_s* lag_local_member(lag_ctx_s* ctx, int r);
 const lag_local_rec& lag_local_recorded(lag_ctx_s* ctx, int r);
 int lag_local_size(lag_ctx_s* ctx);
 lag_status lag_local_flush(lag_ctx_s* ctx);       // first extract of the group: pending hand-offs
+lag_status lag_local_join_all(lag_ctx_s* ctx);    // every block's stream waits for every other
 bool lag_local_extracted(lag_ctx_s* ctx, bool* all);   // mark this block extracted
 bool lag_local_extracting(lag_ctx_s* ctx);        // some block extracted, not all
 void lag_local_leave(lag_ctx_s* ctx);

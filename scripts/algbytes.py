@@ -63,11 +63,50 @@ def measure(name, cycles=(0, 5, 12, 24)):
                                                      (2 * o["slice_sectors"]) for o in out])))
 
 
+def measure_c4(interval):
+    """C4 (Nyx-like 512^3 as 2x2x2, stride 4): block 0 = nodes [0, 256)^3.  A BTO
+    particle of block 0 gathers only nodes [0, 256]^3 (samples beyond the
+    block face stop before their gather), so the oracle runs on that
+    257^3 sub-grid with the real field values; the touched maps are those of
+    the full grid.  Samples cycles 0, mid and last of an interval."""
+    cfg = L.make_config("C4")
+    g = cfg["grid"]
+    sub = L.Grid(3, (257, 257, 257), g.origin, g.spacing)
+    nb = 12
+    it = oracle.Interval(sub, (0, 0, 0), (256, 256, 256), cfg["stride"])
+    want = sorted({0, interval // 2, interval - 1})
+    out = []
+    V0 = L.field_at_nodes(cfg["field"], g, 0.0, hi=(257, 257, 257), backend="torch").numpy()
+    for c in range(interval):
+        V1 = L.field_at_nodes(cfg["field"], g, (c + 1) * cfg["dt"], hi=(257, 257, 257), backend="torch").numpy()
+        touched = np.zeros((257, 257, 257), dtype=np.uint8) if c in want else None
+        n_active = it.active()
+        it.cycle(V0, V1, cfg["dt"], touched=touched)
+        if touched is not None:
+            s0 = sectors(touched & 1, nb)
+            s1 = sectors(touched & 2, nb)
+            full = (257 ** 3 * nb + 31) // 32
+            out.append(dict(cycle=c, n_active=n_active, sectors_v_t=s0, sectors_v_t1=s1,
+                            slice_sectors=full, bytes=32 * n_active + 32 * (s0 + s1),
+                            bytes_per_particle_step=(32 * n_active + 32 * (s0 + s1)) / max(1, n_active)))
+            print("C4", interval, out[-1], flush=True)
+        V0 = V1
+    return dict(config="C4", interval=interval, stride=cfg["stride"], block=[[0, 0, 0], [256, 256, 256]],
+                cycles=out, discarded=int(it.n - it.active()), seeded=int(it.n),
+                mean_bytes_per_particle_step=float(np.mean([o["bytes_per_particle_step"] for o in out])),
+                mean_touched_fraction=float(np.mean([(o["sectors_v_t"] + o["sectors_v_t1"]) /
+                                                     (2 * o["slice_sectors"]) for o in out])))
+
+
 def main():
     names = sys.argv[1:] or ["C5", "C3"]
     path = os.path.join(ROOT, "profiles", "algbytes.json")
     res = json.load(open(path)) if os.path.exists(path) else {}
     for n in names:
+        if n.startswith("C4@"):
+            res[n] = measure_c4(int(n[3:]))
+            json.dump(res, open(path, "w"), indent=1)
+            continue
         res[n] = measure(n)
     res["_source"] = ("scripts/algbytes.py: oracle touched-node maps (stage gathers of the method), "
                       "unique 32 B sectors of the AoS fp32 slices + 32 B per active particle")

@@ -44,16 +44,19 @@ def poisoned_block_slice(V, g, b, ghost, pad=0):
     return s
 
 
-def run_local(cfg, layout, slices_per_interval, stride, pad=0, frozen=False, reseed_mid=None):
-    """All blocks of `layout` as one LAG_XCHG_LOCAL group on cuda:0.  Returns,
-    per interval, per block (start, end, status) and the group's stats."""
+def run_local(cfg, layout, slices_per_interval, stride, pad=0, frozen=False, reseed_mid=None,
+              streams=False):
+    """All blocks of `layout` as one LAG_XCHG_LOCAL group on cuda:0 (one
+    stream, or one stream per block).  Returns, per interval, per block
+    (start, end, status) and the group's stats."""
     import torch
     import paper_2004_02003_b200 as P
     g = cfg["grid"]
     blocks = L.decompose(g, layout)
-    s = torch.cuda.current_stream()
     cfgs = []
+    own = [torch.cuda.Stream() for _ in blocks] if streams else None
     for b in blocks:
+        s = own[b.rank] if streams else torch.cuda.current_stream()
         ext = L.block_slice_extent(g, b, 1)
         pitch = (ext[0] + pad) * g.dim * 4 if pad else 0
         cfgs.append(P.make_config(g.dim, g.nodes, g.origin, g.spacing, b.lo, b.hi, mode=P.LAG_COMM,
@@ -76,8 +79,11 @@ def run_local(cfg, layout, slices_per_interval, stride, pad=0, frozen=False, res
             outs = [(torch.empty((n, g.dim), dtype=torch.float64, device="cuda"),
                      torch.empty((n, g.dim), dtype=torch.float64, device="cuda"),
                      torch.empty((n,), dtype=torch.uint8, device="cuda")) for n in ns]
+            if streams:                             # the outputs were allocated on the current stream
+                torch.cuda.synchronize()
             stats.append(grp.stats())               # before the write cycle: hand-offs in flight
             grp.extract(outs)
+            torch.cuda.synchronize()
             results.append([tuple(x.cpu().numpy() for x in o) for o in outs])
     finally:
         grp.close()
@@ -135,7 +141,7 @@ def test_local_comm_several_intervals_return_to_origin():
     I = 12
     allsl = global_slices(cfg, 3 * I)
     per = [allsl[i * I:(i + 1) * I + 1] for i in range(3)]
-    blocks, res, _ = run_local(cfg, (2, 2, 2), per, 1)
+    blocks, res, _ = run_local(cfg, (2, 2, 2), per, 1, streams=True)     # blocks run concurrently
     whole = L.Block(0, (0, 0, 0), (0, 0, 0), g.nodes)
     for it in range(3):
         single = gpu_block(cfg, whole, per[it], 1)
