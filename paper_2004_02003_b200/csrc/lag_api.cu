@@ -233,7 +233,7 @@ extern "C" lag_status lag_init(const lag_config* cfg, lag_ctx* out) {
     // occupancy-sized persistent grid for the advect kernel
     int occ = 1;
     if (D == 3)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<3, true, false, true> : advect_kernel<3, false, false, true>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<3, true, false> : advect_kernel<3, false, false>, kThreads, 0);
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cfg->mode == LAG_BTO ? advect_kernel<2, true, false> : advect_kernel<2, false, false>, kThreads, 0);
     ctx->advect_blocks_per_sm = occ > 0 ? occ : 1;
@@ -496,19 +496,8 @@ static lag_status advect_enqueue(lag_ctx_s* ctx, float* d0, float* d1, double dt
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
     const bool bto = ctx->cfg.mode == LAG_BTO;
-    // 3-D, every tile in one pass: stage-1 corner rows staged in shared
-    // memory by bulk copies (needs 16-byte aligned slice arrays)
-    const bool box = D == 3 && !overlap && ((((uintptr_t)d0) | ((uintptr_t)d1)) & 15) == 0;
     auto launch = [&](const AdvectArgs& aa, int nb) {
-        if (D == 3 && box && aa.pass == 0) {
-            if (aa.frozen) {
-                if (bto) advect_kernel<3, true, true, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
-                else advect_kernel<3, false, true, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
-            } else {
-                if (bto) advect_kernel<3, true, false, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
-                else advect_kernel<3, false, false, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
-            }
-        } else if (D == 3) {
+        if (D == 3) {
             if (aa.frozen) {
                 if (bto) advect_kernel<3, true, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
                 else advect_kernel<3, false, true><<<nb, kThreads, 0, ctx->stream>>>(aa);

@@ -420,121 +420,6 @@ __device__ __forceinline__ int tile_slow(const AdvectArgs& a, float4* trec, int 
     return __popc(kmask);
 }
 
-// ---------------------------------------------------------------------------
-// Stage-1 corner rows staged in shared memory by the bulk-copy engine (3-D).
-// A tile is 32 x-consecutive particles; while they share one (y, z) cell row
-// their stage-1 corners are the 4 node rows (dy, dz) in {0,1}^2 of at most 34
-// consecutive nodes per slice: 8 contiguous row segments of <= 432 B.  The
-// warp stages the NEXT tile's rows with cp.async.bulk (one elected lane, no
-// registers held, completion on a per-warp mbarrier) while it finishes the
-// current tile, so the stage-1 gather becomes 48 shared-memory loads instead
-// of 48 global loads whose L2 latency the warp would wait for.
-constexpr int kBoxNodes = 34;                    // nodes per staged row: cells xmin .. xmin + 32
-constexpr int kBoxRowF = 108;                    // floats per row buffer: 408 B + <= 12 B alignment, 16-B rounded
-constexpr int kBoxWarpF = 2 * 4 * kBoxRowF;      // per warp: [slice][row][kBoxRowF]
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint32_t mbar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbar) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
-    uint32_t done = 0;
-    do {
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(done) : "r"(mbar), "r"(phase) : "memory");
-    } while (!done);
-}
-
-struct BoxState {
-    int on;                     // the tile's rows are staged (every live lane's stage-1 cell is in them)
-    int x0;                     // gather-offset x of the first staged cell
-    uint32_t off;               // per row r: 4-byte alignment slack (floats) in bits [2r, 2r+2)
-};
-
-// Decide and issue the staging of a tile (record `r`, `cnt` live lanes) into
-// this warp's buffer.  The staged box is the cell row (ymin, zmin) of cells
-// xmin .. xmin + 32; it is used only if every live lane's stage-1 cell is
-// in it, the tile is not on its seed nodes (first cycle) and all its rows
-// lie inside the slice arrays.  Slice pointers are 16-B aligned (host check).
-template <bool FROZEN>
-__device__ __forceinline__ BoxState box_issue(const AdvectArgs& a, float4 r, int cnt, int lane,
-                                              uint32_t sbox, uint32_t mbar) {
-    BoxState b{0, 0, 0u};
-    const bool live = lane < cnt;
-    const uint32_t w = __float_as_uint(r.w);
-    const int g[3] = {(int)(w & a.mx), (int)((w >> a.bx) & a.my), (int)(w >> (a.bx + a.by))};
-    const float d[3] = {r.x, r.y, r.z};
-    int v[3];
-    bool ok = true, node = true;
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-        int tb;
-        floor_fma(d[ax], tb);
-        v[ax] = g[ax] + tb - (a.gmin[ax] + kMagicBits);
-        ok &= (unsigned)v[ax] <= (unsigned)a.gspan[ax];
-        node &= d[ax] == 0.f;
-    }
-    if (cnt == 0 || __all_sync(0xffffffffu, !live || node) || !__all_sync(0xffffffffu, !live || ok)) return b;
-    const int xmin = __reduce_min_sync(0xffffffffu, live ? v[0] : 0x7fffffff);
-    const int xmax = __reduce_max_sync(0xffffffffu, live ? v[0] : -0x7fffffff);
-    const int ymin = __reduce_min_sync(0xffffffffu, live ? v[1] : 0x7fffffff);
-    const int ymax = __reduce_max_sync(0xffffffffu, live ? v[1] : -0x7fffffff);
-    const int zmin = __reduce_min_sync(0xffffffffu, live ? v[2] : 0x7fffffff);
-    const int zmax = __reduce_max_sync(0xffffffffu, live ? v[2] : -0x7fffffff);
-    if (xmax - xmin > kBoxNodes - 2 || ymax != ymin || zmax != zmin) return b;
-    const int v0[3] = {xmin, ymin, zmin};
-    const long long node0 = (long long)vindex<3>(a, v0);
-    // last byte a staged row may touch must lie inside the slice arrays
-    const long long last = 12ll * (node0 + a.sx + a.sxy) + 12 * kBoxNodes + 16;
-    if (last > 12ll * a.slice_nodes) return b;
-    uint32_t off = 0;
-    uint32_t sz[4];
-    long long al[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const long long byte = 12ll * (node0 + (q & 1) * a.sx + (q >> 1) * a.sxy);
-        const uint32_t o = (uint32_t)(byte & 15);
-        al[q] = byte - o;
-        sz[q] = (o + 12 * kBoxNodes + 15) & ~15u;
-        off |= (o >> 2) << (2 * q);
-    }
-    if (lane == 0) {
-        const uint32_t bytes = (FROZEN ? 1 : 2) * (sz[0] + sz[1] + sz[2] + sz[3]);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mbar), "r"(bytes) : "memory");
-#pragma unroll
-        for (int s = 0; s < (FROZEN ? 1 : 2); ++s) {
-            const char* base = reinterpret_cast<const char*>(s ? a.v1 : a.v0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                             :: "r"(sbox + 4u * (uint32_t)((s * 4 + q) * kBoxRowF)), "l"(base + al[q]),
-                                "r"(sz[q]), "r"(mbar) : "memory");
-        }
-    }
-    b.on = 1;
-    b.x0 = xmin;
-    b.off = off;
-    return b;
-}
-
-// The stage-1 corner pairs of the lane's cell (gather-offset x = vx) from the
-// staged rows of slice s.
-__device__ __forceinline__ void gather_pairs_box(const float* buf, const BoxState& b, int vx, f2_t* P) {
-    const int lx = 3 * (vx - b.x0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const float* p = buf + q * kBoxRowF + (int)((b.off >> (2 * q)) & 3u) + lx;
-        float e[6];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) e[k] = p[k];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) P[q * 3 + c] = f2_pack(e[c], e[3 + c]);
-    }
-}
-
 // The advect loop over a virtual grid of `ncta` CTAs (this CTA = `cta`):
 // advect_kernel runs it on the whole grid; the COMM overlap pass 1
 // (advect_xchg_kernel, lag_api.cu) on the CTAs after its exchange CTAs.
@@ -545,9 +430,8 @@ __device__ __forceinline__ void gather_pairs_box(const float* buf, const BoxStat
 // updated position inside the block, every live particle kept.  Anything
 // else (a cell change, a face, a termination, a hand-off) is detected by one
 // warp vote and handled out of line (stage_locate, tile_slow).
-template <int DIM, bool BTO, bool FROZEN, bool BOX = false>
+template <int DIM, bool BTO, bool FROZEN>
 __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, const int ncta) {
-    static_assert(!BOX || DIM == 3, "row staging is 3-D");
     constexpr int NP = Pairs<DIM>::n;
     const int lane = threadIdx.x & 31;
     const int warp = (cta * kThreads + threadIdx.x) >> 5;
@@ -582,31 +466,13 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
     int cnt = tile < n_tiles ? a.tile_count[rtile] : 0;
     float4 r = tile < n_tiles ? a.state[(size_t)rtile * kTile + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
 
-    // BOX: per-warp staging buffer and its mbarrier (phase flips per staged tile)
-    __shared__ __align__(16) float s_box[BOX ? (kThreads / 32) * kBoxWarpF : 1];
-    __shared__ __align__(8) unsigned long long s_mbar[kThreads / 32];
-    const float* wbox = s_box + (BOX ? (threadIdx.x >> 5) * kBoxWarpF : 0);
-    const uint32_t sbox = smem_u32(wbox);
-    const uint32_t mbar = smem_u32(&s_mbar[threadIdx.x >> 5]);
-    uint32_t phase = 0;
-    BoxState box{0, 0, 0u};
-    if constexpr (BOX) {
-        if (lane == 0) mbar_init(mbar);
-        __syncwarp();
-        box = box_issue<FROZEN>(a, r, cnt, lane, sbox, mbar);
-    }
-
     while (tile < n_tiles) {
         const int ntile = tile + tstride;
         const int nrtile = ntile < n_tiles ? real_tile(ntile) : 0;
         const int ncnt = ntile < n_tiles ? a.tile_count[nrtile] : 0;
         const float4 nr = ntile < n_tiles ? a.state[(size_t)nrtile * kTile + lane]
                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (cnt == 0) {
-            if constexpr (BOX) box = box_issue<FROZEN>(a, nr, ncnt, lane, sbox, mbar);
-            tile = ntile; rtile = nrtile; cnt = ncnt; r = nr;
-            continue;
-        }
+        if (cnt == 0) { tile = ntile; rtile = nrtile; cnt = ncnt; r = nr; continue; }
         const bool live = lane < cnt;
         float4* trec = a.state + (size_t)rtile * kTile;
         const uint32_t w = __float_as_uint(r.w);
@@ -663,43 +529,16 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
             if constexpr (DIM == 2) k1[2] = 0.f;
             cur = -1;
         } else {
-            bool staged = false;
-            if constexpr (BOX) {
-                if (box.on) {                 // every live lane's cell is in the staged rows
-                    mbar_wait(mbar, phase);
-                    phase ^= 1u;
-                    staged = true;
-                    gather_pairs_box(wbox, box, live ? v1c[0] : box.x0, S);
-                    if constexpr (FROZEN) {
+            gather_pairs<DIM>(a.v0, idx1, a.sx, a.sxy, S);
+            if constexpr (FROZEN) {
 #pragma unroll
-                        for (int i = 0; i < NP; ++i) B[i] = S[i];
-                    } else {
-                        gather_pairs_box(wbox + 4 * kBoxRowF, box, live ? v1c[0] : box.x0, B);
-                    }
-                }
-            }
-            if (!staged) {
-                gather_pairs<DIM>(a.v0, idx1, a.sx, a.sxy, S);
-                if constexpr (FROZEN) {
-#pragma unroll
-                    for (int i = 0; i < NP; ++i) B[i] = S[i];
-                } else {
-                    gather_pairs<DIM>(a.v1, idx1, a.sx, a.sxy, B);
-                }
+                for (int i = 0; i < NP; ++i) B[i] = S[i];
+            } else {
+                gather_pairs<DIM>(a.v1, idx1, a.sx, a.sxy, B);
             }
             interp_pairs<DIM>(S, f1, k1);
 #pragma unroll
             for (int i = 0; i < NP; ++i) S[i] = f2_add(S[i], B[i]);   // S = v0 + v1 (stages 2, 3)
-        }
-        if constexpr (BOX) {
-            // the staged rows were read (S and B hold them): order those reads
-            // before the bulk copies that overwrite the buffer, then stage the
-            // next tile while this one finishes
-            if (box.on) {
-                asm volatile("fence.proxy.async.shared::cta;" :: "l"(S[0]), "l"(S[NP - 1]), "l"(B[0]), "l"(B[NP - 1]) : "memory");
-                __syncwarp();
-            }
-            box = box_issue<FROZEN>(a, nr, ncnt, lane, sbox, mbar);
         }
 
         float e[3], f[3];
@@ -781,10 +620,10 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
     }
 }
 
-template <int DIM, bool BTO, bool FROZEN, bool BOX = false>
+template <int DIM, bool BTO, bool FROZEN>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 advect_kernel(const AdvectArgs a) {
-    advect_body<DIM, BTO, FROZEN, BOX>(a, blockIdx.x, gridDim.x);
+    advect_body<DIM, BTO, FROZEN>(a, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
