@@ -285,15 +285,23 @@ def run_e2e(cfg, rank, world, steps, warmup):
             "timing": "wall clock around synchronize, max over ranks"}
 
 
-def algorithmic_bytes(name, psteps, cycles, slice_bytes):
+def algorithmic_bytes(name, psteps, cycles, slice_bytes, interval=None):
     """Algorithmic bytes of `cycles` advect launches: 32 B per particle-step
     (float4 read + write) + the slice sectors the method's stage gathers touch
     per cycle (profiles/algbytes.json, written by scripts/algbytes.py from the
-    oracle's touched-node maps; both whole slices if absent)."""
+    oracle's touched-node maps; both whole slices if absent).  The sampled
+    cycles are averaged over an interval with the first cycle (particles on
+    their seed nodes) weighted 1/interval."""
     vel = 2.0 * slice_bytes
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "algbytes.json")))[name]
-        vel = 32.0 * float(np.mean([c["sectors_v_t"] + c["sectors_v_t1"] for c in d["cycles"]]))
+        per = {c["cycle"]: 32.0 * (c["sectors_v_t"] + c["sectors_v_t1"]) for c in d["cycles"]}
+        later = [v for k, v in per.items() if k > 0]
+        I = interval or d.get("interval") or 25
+        if 0 in per and later:
+            vel = (per[0] + (I - 1) * float(np.mean(later))) / I
+        else:
+            vel = float(np.mean(list(per.values())))
     except Exception:
         pass
     return 32.0 * psteps + cycles * vel
@@ -315,7 +323,7 @@ def measure_secondary(name, rank, world, steps, warmup, flush):
     dev_ms_max = allreduce_max(dev_ms, world)
     total_ps = allreduce_sum(psteps, world)
     cycles = steps * arm.interval
-    alg = algorithmic_bytes(name, psteps, cycles, arm.slice_bytes)
+    alg = algorithmic_bytes(name, psteps, cycles, arm.slice_bytes, arm.interval)
     peak, _ = measured_peak()
     ach = alg / (adv_ms / 1e3) / 1e9
     out = {"workload": f"{name}: {cfg['field'].kind} field, {list(L.block_slice_extent(cfg['grid'], arm.block, 0))} "
@@ -463,6 +471,103 @@ def measure_c2(steps, warmup, flush):
             "l2": "flushed before every interval; the cycles of an interval run back to back"}
 
 
+def measure_c4(steps, warmup, flush):
+    """configs[3] per GPU: C4 = Nyx-like turbulence 512^3 as 2x2x2, block 0
+    (256^3 owned nodes, 257^3 slice nodes, 203.7 MB per slice), stride 4
+    (262144 particles), BTO, intervals 10 / 50 / 100 (the paper's sweep,
+    P:782-783).  Roofline bytes: profiles/algbytes.json C4@<interval>."""
+    import torch
+    import lag_inputs as L
+    import paper_2004_02003_b200 as P
+    peak, _ = measured_peak()
+    out = {"workload": "C4 (configs[3]): Nyx-like 64-mode turbulence, 512^3 as 2x2x2, block 0 "
+                       "(257^3 slice nodes) on one GPU, stride 4 (262144 particles), BTO"}
+    for I in (10, 50, 100):
+        cfg = L.make_config("C4", interval=I)
+        arm = Arm(cfg, 0, 1, P.LAG_BTO)
+        run_arm(arm, warmup, flush)
+        torch.cuda.synchronize()
+        t_adv, t_other, psteps = run_arm(arm, steps, flush)
+        adv_ms, dev_ms = sum(t_adv), sum(t_adv) + sum(t_other)
+        cycles = steps * I
+        alg = algorithmic_bytes(f"C4@{I}", psteps, cycles, arm.slice_bytes, I)
+        ach = alg / (adv_ms / 1e3) / 1e9
+        st = arm.ctx.stats()
+        out[f"interval_{I}"] = {
+            "value": psteps / (dev_ms / 1e3), "unit": UNIT, "ms_per_step": dev_ms / steps,
+            "ms_per_cycle": adv_ms / cycles,
+            "discarded_pct_last_interval": 100.0 * (st["term_boundary"] + st["exit_domain"]) / arm.n,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "alg_bytes_per_launch": alg / cycles}}
+        arm.ctx.close()
+        del arm
+        torch.cuda.empty_cache()
+    return out
+
+
+def c1_cpu_seconds():
+    """configs[0]: C1 double gyre 64x32, 2048 particles, 100 RK4 cycles in 5
+    intervals of 20 — the whole run through the fp64 oracle on 1 host core and
+    on all host cores (CPU seconds), and the same run on the GPU through the C
+    ABI (device time)."""
+    import ctypes
+    import torch
+    import lag_inputs as L
+    import oracle
+    import paper_2004_02003_b200 as P
+    cfg = L.make_config("C1")
+    g = cfg["grid"]
+    I, C = cfg["interval"], cfg["cycles"]
+    sl = [L.field_at_nodes(cfg["field"], g, k * cfg["dt"]) for k in range(C + 1)]
+    try:
+        gomp = ctypes.CDLL("libgomp.so.1")
+    except OSError:
+        gomp = None
+    oracle.build()
+    res = {}
+    ncpu = os.cpu_count() or 1
+    for cores in (1, ncpu):
+        if gomp is not None:
+            gomp.omp_set_num_threads(cores)
+        t0 = time.perf_counter()
+        for it in range(C // I):
+            iv = oracle.Interval(g, (0, 0, 0), g.nodes, 1)
+            for c in range(I):
+                iv.cycle(sl[it * I + c], sl[it * I + c + 1], cfg["dt"])
+        res[f"cpu_seconds_{cores}_cores"] = time.perf_counter() - t0
+    if gomp is not None:
+        gomp.omp_set_num_threads(ncpu)
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    # the same 100 cycles on the GPU
+    s = torch.cuda.current_stream()
+    dev = [torch.from_numpy(v).cuda() for v in sl]
+    ctx = P.Context(P.make_config(2, g.nodes, g.origin, g.spacing, (0, 0, 0), g.nodes, stream=s.cuda_stream))
+    n = ctx.seed(1)
+    end = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for it in range(C // I):
+        for c in range(I):
+            ctx.advect(dev[it * I + c], dev[it * I + c + 1], cfg["dt"])
+        ctx.extract(end=end, flags=P.LAG_ASYNC)
+    e1.record(s)
+    torch.cuda.synchronize()
+    res["gpu_seconds"] = e0.elapsed_time(e1) / 1e3
+    ctx.close()
+    res.update({"workload": "C1 (configs[0]): double gyre 64x32, 1 block, 2048 particles, 100 cycles, interval 20",
+                "particle_steps": 2048 * C, "host_cores": ncpu, "cpu_model": model,
+                "cpu": "fp64 C oracle (OpenMP over particles), whole run incl. reseeds"})
+    return res
+
+
 def measured_peak():
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -570,7 +675,7 @@ def main():
     # 32 B x active particles (float4 read + write) + the slice sectors the
     # method touches (stride 1: every node) — DESIGN.md §6
     cycles = args.steps * arm.interval
-    alg_bytes = algorithmic_bytes(cfg["name"], psteps, cycles, arm.slice_bytes)
+    alg_bytes = algorithmic_bytes(cfg["name"], psteps, cycles, arm.slice_bytes, arm.interval)
     achieved = alg_bytes / (adv_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
     st = arm.ctx.stats()
@@ -595,21 +700,28 @@ def main():
             c_ms = allreduce_max(sum(c_adv) + sum(c_other), world)
             c_total = allreduce_sum(c_ps, world)
             cst = carm.ctx.stats()
+            c_cyc = allreduce_max(sum(c_adv), world) / cycles
             comm[tname] = {"value": c_total / (c_ms / 1e3), "unit": UNIT,
                            "ms_per_step": c_ms / args.steps,
-                           "ms_per_cycle": allreduce_max(sum(c_adv), world) / cycles,
-                           "bto_speedup": (c_ms / dev_ms_max),
+                           "ms_per_cycle": c_cyc,
+                           # the paper's metric: average time per cycle (advection,
+                           # management, communication), write cycles excluded
+                           "bto_speedup": c_cyc / (adv_ms_max / cycles),
+                           "bto_speedup_step": c_ms / dev_ms_max,
                            "sent_last_interval": int(cst["sent"]),
                            "received_last_interval": int(cst["received"])}
             carm.ctx.close()
             del carm
         best = max(comm.values(), key=lambda d: d["value"])
         comm.update({"value": best["value"], "unit": UNIT, "bto_speedup": best["bto_speedup"],
+                     "bto_speedup_step": best["bto_speedup_step"],
                      "exchange": "per cycle: ghost layer (G=1, faces+edges+corners) of v_t1 + particle "
                                  "hand-offs; 'nccl' = one grouped NCCL send/recv, 'peer' = kernels read / "
                                  "write the neighbours' memory over NVLink (CUDA IPC), 'peer_overlap' = "
-                                 "peer with the exchange on a second stream under the advection of the "
-                                 "ghost-free tiles; value/speedup = fastest"})
+                                 "peer with the exchange run by the first CTAs of the advect kernel while "
+                                 "the other CTAs advect the ghost-free tiles; value/speedup = fastest; "
+                                 "bto_speedup = per-cycle time ratio (write cycles excluded, P:365-367), "
+                                 "bto_speedup_step = whole-interval ratio"})
       except Exception as exc:        # the headline BTO line must still print
         comm = {"error": repr(exc)[:300]}
 
@@ -626,6 +738,20 @@ def main():
             c2 = measure_c2(max(2, args.steps // 2), 2, flush)
         except Exception as exc:
             c2 = {"error": repr(exc)[:300]}
+
+    c4 = None
+    if world == 1 and not args.no_secondary:
+        try:
+            c4 = measure_c4(1, 1, flush)
+        except Exception as exc:
+            c4 = {"error": repr(exc)[:300]}
+
+    c1 = None
+    if world == 1 and not args.no_cpu:
+        try:
+            c1 = c1_cpu_seconds()
+        except Exception as exc:
+            c1 = {"error": repr(exc)[:300]}
 
     e2e = None
     if not args.no_e2e:
@@ -666,6 +792,8 @@ def main():
             "comm": comm,
             "secondary": secondary,
             "c2": c2,
+            "c4": c4,
+            "c1_cpu_seconds": c1,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
