@@ -33,7 +33,7 @@ advect_xchg_kernel(const AdvectArgs a, const XchgFused xf) {
         xchg_wait_pull(xf.x, xf.ap, blockIdx.x, xf.ncta);
         return;
     }
-    advect_body<DIM, false, FROZEN>(a, blockIdx.x - xf.ncta, gridDim.x - xf.ncta);
+    advect_body<DIM, false, FROZEN, true>(a, blockIdx.x - xf.ncta, gridDim.x - xf.ncta);
 }
 
 int lag_set_error(lag_ctx_s* ctx, const char* fmt, ...) {
@@ -534,7 +534,13 @@ static lag_status advect_enqueue(lag_ctx_s* ctx, float* d0, float* d1, double dt
         if (ev) cudaEventRecord(ev[2], ctx->stream);
         AdvectArgs a2 = a;
         a2.pass = 2;
-        launch(a2, blocks);
+        if (D == 3) {
+            if (a2.frozen) advect_kernel<3, false, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a2);
+            else advect_kernel<3, false, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a2);
+        } else {
+            if (a2.frozen) advect_kernel<2, false, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a2);
+            else advect_kernel<2, false, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a2);
+        }
     } else {
         launch(a, blocks);
     }

@@ -246,7 +246,7 @@ __device__ __forceinline__ bool in_unit_cell(const float fs[3]) {
 // A stage sample that left the stage-1 cell (rare): its cell v1 + floor(fs),
 // fractions, the fast-range test and, outside it, the full classification.
 // Latches non-finite samples (non-finite velocity reached the particle).
-template <int DIM, bool BTO>
+template <int DIM, bool BTO, bool PASSES>
 __device__ __forceinline__ int stage_moved(const AdvectArgs& a, const int v1[3], const float fs[3],
                                         uint8_t& st, bool& ghost_bad, uint32_t& errbits, float f[3]) {
     int v[3] = {0, 0, 0};
@@ -267,7 +267,7 @@ __device__ __forceinline__ int stage_moved(const AdvectArgs& a, const int v1[3],
         return 0;
     }
     if (!ok) st = classify_slow_v<DIM, BTO>(a, v, f, ghost_bad);
-    if constexpr (!BTO) {
+    if constexpr (!BTO && PASSES) {
         // overlap pass 1 (LAG_XCHG_PEER_OVERLAP): the tile was judged
         // ghost-free from its stage-1 cells, which holds while samples stay
         // within one cell of them (CFL < 1); a farther sample may read ghost
@@ -286,7 +286,7 @@ __device__ __forceinline__ int stage_moved(const AdvectArgs& a, const int v1[3],
 // cache holds that cell: nothing to do (one vote).  Otherwise the lanes that
 // left the cell, or whose cache holds another cell, locate their sample and
 // reload the cache (both slices for stages 2-3, v_t1 only for stage 4).
-template <int DIM, bool BTO, bool FROZEN, int SLICES>
+template <int DIM, bool BTO, bool FROZEN, bool PASSES, int SLICES>
 __device__ __forceinline__ void stage_locate(const AdvectArgs& a, bool active, const int v1[3], int idx1,
                                              const float fs[3], int& cur, uint8_t& st, bool& ghost_bad,
                                              uint32_t& errbits, float f[3], f2_t* S, f2_t* B) {
@@ -298,7 +298,7 @@ __device__ __forceinline__ void stage_locate(const AdvectArgs& a, bool active, c
     if (__any_sync(0xffffffffu, need)) {
         if (need) {
             int idx = idx1;
-            if (!same) idx = stage_moved<DIM, BTO>(a, v1, fs, st, ghost_bad, errbits, f);
+            if (!same) idx = stage_moved<DIM, BTO, PASSES>(a, v1, fs, st, ghost_bad, errbits, f);
             LAG_CHECK_GATHER(a, idx, st == ST_VALID);
             if (st == ST_VALID && idx != cur) {
                 if constexpr (SLICES == 2) {
@@ -430,7 +430,9 @@ __device__ __forceinline__ int tile_slow(const AdvectArgs& a, float4* trec, int 
 // updated position inside the block, every live particle kept.  Anything
 // else (a cell change, a face, a termination, a hand-off) is detected by one
 // warp vote and handled out of line (stage_locate, tile_slow).
-template <int DIM, bool BTO, bool FROZEN>
+// PASSES: the overlapped COMM transport's two passes (a.pass 1 / 2); every
+// other launch advances every tile in one pass and compiles without them.
+template <int DIM, bool BTO, bool FROZEN, bool PASSES = false>
 __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, const int ncta) {
     constexpr int NP = Pairs<DIM>::n;
     const int lane = threadIdx.x & 31;
@@ -438,7 +440,7 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
     int n_tiles = a.n_tiles_dev ? *a.n_tiles_dev : a.n_tiles;
     // overlap passes (COMM): loop over virtual tile indices, map to real tiles
     int n_def = 0, n_b = 0;
-    if constexpr (!BTO) {
+    if constexpr (!BTO && PASSES) {
         if (a.pass == 1) {
             n_tiles = (int)*a.n_tiles_b;
         } else if (a.pass == 2) {
@@ -448,7 +450,7 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         }
     }
     auto real_tile = [&](int v) -> int {
-        if constexpr (!BTO) {
+        if constexpr (!BTO && PASSES) {
             if (a.pass == 2) return v < n_def ? (int)a.defer_list[v] : n_b + (v - n_def);
         }
         return v;
@@ -499,7 +501,7 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         if (__any_sync(0xffffffffu, live && !ok1)) {         // closed top face: clamp (rare)
             if (live && !ok1) classify_slow_v<DIM, BTO>(a, v1c, f1, ghost_bad);
         }
-        if constexpr (!BTO) {
+        if constexpr (!BTO && PASSES) {
             if (a.pass == 1) {                // a sample could reach a ghost node: after the exchange
                 bool safe = true;
 #pragma unroll
@@ -545,21 +547,21 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         // ---- stage 2: q2 = x + dt/2 k1, alpha = 1/2 ----
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) e[ax] = ax < DIM ? fmaf(a.hdth[ax], k1[ax], f1[ax]) : 0.f;
-        stage_locate<DIM, BTO, FROZEN, 2>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
+        stage_locate<DIM, BTO, FROZEN, PASSES, 2>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
         float T2[3];
         interp_pairs<DIM>(S, f, T2);                          // T2 = 2 k2
 
         // ---- stage 3: q3 = x + dt/2 k2 = x + dt/4 T2, alpha = 1/2 ----
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) e[ax] = ax < DIM ? fmaf(a.qdth[ax], T2[ax], f1[ax]) : 0.f;
-        stage_locate<DIM, BTO, FROZEN, 2>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
+        stage_locate<DIM, BTO, FROZEN, PASSES, 2>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
         float T3[3];
         interp_pairs<DIM>(S, f, T3);                          // T3 = 2 k3
 
         // ---- stage 4: q4 = x + dt k3 = x + dt/2 T3, alpha = 1 ----
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) e[ax] = ax < DIM ? fmaf(a.hdth[ax], T3[ax], f1[ax]) : 0.f;
-        stage_locate<DIM, BTO, FROZEN, 1>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
+        stage_locate<DIM, BTO, FROZEN, PASSES, 1>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
         float k4[3];
         interp_pairs<DIM>(B, f, k4);
 
@@ -620,10 +622,10 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
     }
 }
 
-template <int DIM, bool BTO, bool FROZEN>
+template <int DIM, bool BTO, bool FROZEN, bool PASSES = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 advect_kernel(const AdvectArgs a) {
-    advect_body<DIM, BTO, FROZEN>(a, blockIdx.x, gridDim.x);
+    advect_body<DIM, BTO, FROZEN, PASSES>(a, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
