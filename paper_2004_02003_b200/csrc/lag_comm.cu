@@ -156,7 +156,9 @@ __global__ void halo_pack_kernel(BoxArgs a) {
     }
 }
 
-__global__ void halo_unpack_kernel(BoxArgs a) {
+// the received ghost layers (grid-stride) and the received particles
+// (append_body) in one launch
+__global__ void __launch_bounds__(256) halo_unpack_append_kernel(BoxArgs a, AppendArgs ap) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int k = find_box(a.boxes, a.nbox, i);
@@ -168,6 +170,7 @@ __global__ void halo_unpack_kernel(BoxArgs a) {
         float* dst = b.slice ? a.v1 : a.v0w;
         dst[(int64_t)a.dim * ((b.x0 + x) + (int64_t)a.sx * (b.y0 + y) + (int64_t)a.sxy * (b.z0 + z)) + comp] = a.buf[i];
     }
+    append_body(ap, blockIdx.x, gridDim.x);
 }
 
 struct RouteArgs {
@@ -548,10 +551,11 @@ static lag_status exchange(lag_ctx_s* ctx, float* v0, float* v1, bool halo, bool
         BoxArgs b{};
         b.v0 = v0; b.v1 = v1; b.v0w = v0; b.boxes = cm->d_recv_boxes; b.nbox = nbox;
         b.buf = cm->halo_recv; b.sx = ctx->sx; b.sxy = ctx->sxy; b.dim = D; b.total = rfl;
-        const int blocks = (int)std::min<int64_t>((rfl + 255) / 256, (int64_t)ctx->num_sms * 8);
-        halo_unpack_kernel<<<blocks, 256, 0, ctx->stream>>>(b);
+        const AppendArgs ap = append_args(ctx, -1);
+        halo_unpack_append_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(b, ap);
         ++ctx->launches;
         CKC(cudaGetLastError());
+        return LAG_OK;
     }
     return launch_append(ctx);
 }

@@ -58,8 +58,13 @@ namespace lag {
 enum : int { T_INBOX = 0, T_INBOX_PAR = 1, T_OUTBOX = 2, T_HALO = 3, T_RECV = 4, T_SEND = 4 + kOff,
              T_WORDS = 4 + 2 * kOff };
 
-__global__ void __launch_bounds__(256) peer_pack_signal_kernel(XchgArgs x) {
+// pack + signal, then wait + pull + append, in one launch: every CTA must be
+// resident (a CTA waiting for the neighbours' signal must not keep one of
+// ours that has not packed from running), so the grid is capped at the
+// resident capacity
+__global__ void __launch_bounds__(256) peer_exchange_kernel(XchgArgs x, AppendArgs ap) {
     xchg_pack_signal(x, blockIdx.x, gridDim.x);
+    xchg_wait_pull(x, ap, blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(256) peer_wait_pull_kernel(XchgArgs x, AppendArgs ap) {
@@ -257,14 +262,15 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
         f->ap = ap;
         return LAG_OK;
     }
-    const int cap = ctx->num_sms * 2;
+    const int cap = ctx->num_sms * 2;          // resident: 2 CTAs of 256 threads per SM
     if (halo) {
-        const int ga = (int)std::max<int64_t>(1, std::min<int64_t>((x.sfl + 255) / 256, cap));
-        peer_pack_signal_kernel<<<ga, 256, 0, st>>>(x);
-        ++ctx->launches;
+        const int64_t work = std::max(x.sfl, x.rtotal);
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, cap));
+        peer_exchange_kernel<<<g, 256, 0, st>>>(x, ap);
+    } else {
+        const int gb = (int)std::max<int64_t>(1, std::min<int64_t>((x.rtotal + 255) / 256, cap));
+        peer_wait_pull_kernel<<<gb, 256, 0, st>>>(x, ap);
     }
-    const int gb = (int)std::max<int64_t>(1, std::min<int64_t>((x.rtotal + 255) / 256, cap));
-    peer_wait_pull_kernel<<<gb, 256, 0, st>>>(x, ap);
     ++ctx->launches;
     CKC(cudaGetLastError());
     return LAG_OK;
