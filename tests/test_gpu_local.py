@@ -224,3 +224,102 @@ def test_local_comm_errors():
     grp.blocks[1].extract()
     grp.advect(vs, vs, 0.01)                        # the group reseeded: a new interval runs
     grp.close()
+
+
+@pytest.mark.slow
+def test_local_comm_c2_full_size():
+    """configs[1] at full size on one GPU, in bench.py's launch configuration
+    (8 blocks of 128^3, one stream per block, stride 1, one interval of 25
+    cycles at the config's dt): the COMM group equals the single-block run
+    bitwise, and 4096 sampled seeds of that run match the oracle."""
+    cfg = L.make_config("C2")
+    g = cfg["grid"]
+    sl = global_slices(cfg, cfg["interval"])
+    blocks, res, stats = run_local(cfg, cfg["layout"], [sl], 1, streams=True)
+    assert sum(s["sent"] for s in stats[0]) > 0
+    whole = L.Block(0, (0, 0, 0), (0, 0, 0), g.nodes)
+    single = gpu_block(cfg, whole, sl, 1)
+    got = assemble(g, blocks, res[0], 1)
+    for a, b in zip(got, single[:3]):
+        assert np.array_equal(a, b)
+    gs = oracle.seeds(g, (0, 0, 0), g.nodes, 1)
+    pick = np.unique(np.random.default_rng(11).choice(gs.shape[0], 4096, replace=False))
+    orc = oracle.run_interval(g, (0, 0, 0), g.nodes, 1, sl, cfg["dt"], mode=oracle.BTO, g_seeds=gs[pick],
+                              faces=((0, 0, 0), g.nodes))
+    compare(cfg, orc, single[0][pick], single[1][pick], single[2][pick], label="C2 full single/comm")
+
+
+def test_cuda_graph_replay_equals_direct_calls():
+    """bench.py replays captured intervals (CUDA graphs): a captured interval
+    (seed | cycles | asynchronous write cycle), replayed twice, gives the same
+    flow maps as direct calls — for a BTO context and for a LAG_XCHG_LOCAL
+    group with one stream per block."""
+    import torch
+    import paper_2004_02003_b200 as P
+    cfg = L.make_config("C2", scale=33, nranks=8)
+    cfg["dt"] *= 4.0
+    g = cfg["grid"]
+    I = 8
+    sl = global_slices(cfg, I)
+    blocks = L.decompose(g, cfg["layout"])
+    direct = assemble(g, blocks, run_local(cfg, cfg["layout"], [sl], 1, streams=True)[1][0], 1)
+    cap = torch.cuda.Stream()
+    streams = [torch.cuda.Stream() for _ in blocks]
+    cfgs = [P.make_config(3, g.nodes, g.origin, g.spacing, b.lo, b.hi, mode=P.LAG_COMM, ghost=1, rank=b.rank,
+                          nranks=8, layout=cfg["layout"], stream=st.cuda_stream, exchange=P.LAG_XCHG_LOCAL)
+            for b, st in zip(blocks, streams)]
+    grp = P.LocalGroup(cfgs)
+    ns = grp.seed(1)
+    dev = [[torch.from_numpy(poisoned_block_slice(V, g, b, 1)).cuda() for b in blocks] for V in sl]
+    outs = [(torch.empty((n, 3), dtype=torch.float64, device="cuda"), torch.empty((n, 3), dtype=torch.float64, device="cuda"),
+             torch.empty((n,), dtype=torch.uint8, device="cuda")) for n in ns]
+    torch.cuda.synchronize()
+
+    def interval():
+        ev = torch.cuda.Event()
+        ev.record(cap)
+        for st in streams:
+            st.wait_event(ev)
+        grp.seed(1)
+        for k in range(I):
+            grp.advect(dev[k], dev[k + 1], cfg["dt"])
+        grp.extract(outs, flags=P.LAG_NO_RESEED | P.LAG_ASYNC)
+        for st in streams:
+            e = torch.cuda.Event()
+            e.record(st)
+            cap.wait_event(e)
+
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=cap):
+        interval()
+    for _ in range(2):
+        for o in outs:
+            for x in o:
+                x.fill_(0)
+        torch.cuda.synchronize()
+        gr.replay()
+        torch.cuda.synchronize()
+        got = assemble(g, blocks, [tuple(x.cpu().numpy() for x in o) for o in outs], 1)
+        for a, b in zip(got, direct):
+            assert np.array_equal(a, b)
+    grp.close()
+    # a BTO context: the captured interval equals direct calls
+    b = L.Block(0, (0, 0, 0), (0, 0, 0), g.nodes)
+    ref = gpu_block(cfg, b, sl, 1)
+    ctx = P.Context(P.make_config(3, g.nodes, g.origin, g.spacing, b.lo, b.hi, stream=cap.cuda_stream))
+    n = ctx.seed(1)
+    d1 = [torch.from_numpy(np.ascontiguousarray(L.cut_block_slice(V, g, b, 0))).cuda() for V in sl]
+    o = (torch.empty((n, 3), dtype=torch.float64, device="cuda"), torch.empty((n, 3), dtype=torch.float64, device="cuda"),
+         torch.empty((n,), dtype=torch.uint8, device="cuda"))
+    torch.cuda.synchronize()
+    gr2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr2, stream=cap):
+        ctx.seed(1)
+        for k in range(I):
+            ctx.advect(d1[k], d1[k + 1], cfg["dt"])
+        ctx.extract(*o, flags=P.LAG_NO_RESEED | P.LAG_ASYNC)
+    gr2.replay()
+    torch.cuda.synchronize()
+    for x, y in zip(o, ref[:3]):
+        assert np.array_equal(x.cpu().numpy(), y)
+    ctx.close()
