@@ -552,7 +552,8 @@ static lag_status exchange(lag_ctx_s* ctx, float* v0, float* v1, bool halo, bool
         b.v0 = v0; b.v1 = v1; b.v0w = v0; b.boxes = cm->d_recv_boxes; b.nbox = nbox;
         b.buf = cm->halo_recv; b.sx = ctx->sx; b.sxy = ctx->sxy; b.dim = D; b.total = rfl;
         const AppendArgs ap = append_args(ctx, -1);
-        halo_unpack_append_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(b, ap);
+        const int blocks = (int)std::max<int64_t>(ctx->num_sms, std::min<int64_t>((rfl + 255) / 256, (int64_t)ctx->num_sms * 8));
+        halo_unpack_append_kernel<<<blocks, 256, 0, ctx->stream>>>(b, ap);
         ++ctx->launches;
         CKC(cudaGetLastError());
         return LAG_OK;
