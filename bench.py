@@ -182,7 +182,7 @@ class Arm:
         self.cfg = cfg
         g = cfg["grid"]
         self.block = L.decompose(g, cfg["layout"])[rank]
-        self.ghost = 1 if mode == P.LAG_COMM else 0
+        self.ghost = 1 if mode == P.LAG_COMM and world > 1 else 0     # no neighbour, no ghost layers
         self.interval = cfg["interval"]
         self.stream = torch.cuda.current_stream()
         lo = [self.block.lo[a] - self.ghost if a < g.dim else 0 for a in range(3)]

@@ -123,7 +123,8 @@ typedef struct {
     int64_t block_lo[3];         /* owned node range [lo, hi), 0 <= lo < hi <= N          */
     int64_t block_hi[3];
     int32_t ghost;               /* G ghost node layers per side in the slice arrays;
-                                    COMM requires G >= 1; BTO reads none                  */
+                                    COMM with nranks > 1 requires G >= 1; BTO (and a
+                                    single-block COMM run) reads none                     */
     int32_t device;              /* CUDA device ordinal                                   */
     int32_t rank;                /* COMM: this block's rank (x-fastest in layout)         */
     int32_t nranks;              /* COMM: number of ranks = prod(layout)                  */

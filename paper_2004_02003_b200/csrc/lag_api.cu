@@ -115,7 +115,7 @@ static lag_status validate(const lag_config* c) {
     }
     if (c->ghost < 0 || c->ghost > 8) { lag_set_error(ctx, "ghost must be in [0, 8]"); return LAG_EINVAL; }
     if (c->mode == LAG_COMM) {
-        if (c->ghost < 1) { lag_set_error(ctx, "COMM mode needs ghost >= 1"); return LAG_EINVAL; }
+        if (c->ghost < 1 && c->nranks > 1) { lag_set_error(ctx, "COMM mode with neighbours needs ghost >= 1"); return LAG_EINVAL; }
         int64_t prod = 1;
         for (int a = 0; a < 3; ++a) {
             if (c->layout[a] < 1 || (a >= c->dim && c->layout[a] != 1)) { lag_set_error(ctx, "bad layout"); return LAG_EINVAL; }

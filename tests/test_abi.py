@@ -45,7 +45,7 @@ def test_library_is_sm100a():
     (dict(spacing=(float("nan"), 1.0, 1.0)), "spacing"),
     (dict(origin=(float("inf"), 0.0, 0.0)), "origin"),
     (dict(mode=7), "mode"),
-    (dict(mode=1, ghost=0), "ghost"),
+    (dict(mode=1, ghost=0, nranks=2, layout=(2, 1, 1), nccl_id=b"x" * 128), "ghost"),
     (dict(ghost=-1), "ghost"),
     (dict(mode=1, ghost=1, nranks=2, layout=(2, 1, 1)), "nccl_id"),
     (dict(mode=1, ghost=1, nranks=2, layout=(3, 1, 1)), "layout"),
