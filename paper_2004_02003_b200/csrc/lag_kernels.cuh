@@ -517,8 +517,10 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         LAG_CHECK_GATHER(a, idx1, live);
         int cur = idx1;                                      // cell held by the corner cache
         float k1[3];
-        if (__all_sync(0xffffffffu, !live || ((d[0] == 0.f) & (d[1] == 0.f) & (d[2] == 0.f)))) {
-            // every particle sits on its seed node (first cycle of an interval):
+        if (a.cycle == 0 && __all_sync(0xffffffffu, !live || ((d[0] == 0.f) & (d[1] == 0.f) & (d[2] == 0.f)))) {
+            // every particle sits on its seed node (first cycle of an interval;
+            // later cycles do not test it: a particle at rest on a node takes
+            // the general path, which handles f = 0 as well):
             // the trilinear value at a node is the node value (f = 0, or f = 1
             // on a clamped top face) — 3 loads; stage 2 gathers its own cell
             // (cur = -1 forces it)
