@@ -716,6 +716,7 @@ extern "C" lag_status lag_extract_ex(lag_ctx ctx, int64_t interval_index, double
         ExtractArgs eq = e;
         if (local) {
             const lag_ctx_s* m = lag_local_member(ctx, q);
+            if (!m) { lag_set_error(ctx, "LAG_XCHG_LOCAL: block %d of the group was destroyed", q); return LAG_ESTATE; }
             eq.state = m->state; eq.tile_count = m->tile_count; eq.n_tiles = m->cap_tiles;
             eq.n_tiles_dev = (const int32_t*)(m->words + W_NTILES);
             eq.dead_rec = m->dead_rec; eq.dead_info = m->dead_info;
@@ -767,7 +768,7 @@ extern "C" lag_status lag_extract_ex(lag_ctx ctx, int64_t interval_index, double
             if ((st = lag_local_join_all(ctx)) != LAG_OK) return st;
             for (int q = 0; q < lag_local_size(ctx); ++q) {
                 lag_ctx_s* m = lag_local_member(ctx, q);
-                if (!m->reseed_pending) continue;
+                if (!m || !m->reseed_pending) continue;
                 m->reseed_pending = false;
                 st = lag_seed(m, m->stride, nullptr);
                 if (st != LAG_OK) {

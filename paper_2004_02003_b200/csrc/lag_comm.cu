@@ -423,7 +423,8 @@ static lag_status comm_setup(lag_ctx_s* ctx) {
     cm->d_route_pos = cm->d_route_count + c.nranks;
     CKC(cudaMalloc(&cm->d_seg, sizeof(uint32_t) * (c.nranks + 1)));
     CKC(cudaMalloc(&cm->d_all, sizeof(uint32_t) * c.nranks * (c.nranks + 1)));
-    cm->route_cap = ctx->cap;
+    // return-to-origin buffers (LAG_XCHG_LOCAL gathers from the group's lists instead)
+    cm->route_cap = c.exchange == LAG_XCHG_LOCAL ? 1 : ctx->cap;
     CKC(cudaMalloc(&cm->route, sizeof(RouteRec) * std::max<int64_t>(1, cm->route_cap)));
     CKC(cudaMalloc(&cm->route_recv, sizeof(RouteRec) * std::max<int64_t>(1, cm->route_cap)));
     for (const Peer& p : cm->peers) { cm->prank.push_back(p.rank); cm->poff.push_back(p.off); cm->pback.push_back(p.back); }
@@ -817,9 +818,10 @@ static AppendArgs local_append_args(lag_ctx_s* ctx) {
 // The group stream waits for every block's stream (fan-in).
 static lag_status local_join_in(lag_ctx_s* ctx) {
     LocalGroup* g = ctx->group;
+    if (!g->m[0]) { lag_set_error(ctx, "LAG_XCHG_LOCAL: block 0 of the group was destroyed"); return LAG_ESTATE; }
     cudaStream_t s0 = g->m[0]->stream;
     for (size_t r = 1; r < g->m.size(); ++r) {
-        if (g->m[r]->stream == s0) continue;
+        if (!g->m[r] || g->m[r]->stream == s0) continue;
         CKC(cudaEventRecord(g->ev[r], g->m[r]->stream));
         CKC(cudaStreamWaitEvent(s0, g->ev[r], 0));
     }
@@ -829,10 +831,11 @@ static lag_status local_join_in(lag_ctx_s* ctx) {
 // Every block's stream waits for the group stream (fan-out).
 static lag_status local_join_out(lag_ctx_s* ctx) {
     LocalGroup* g = ctx->group;
+    if (!g->m[0]) { lag_set_error(ctx, "LAG_XCHG_LOCAL: block 0 of the group was destroyed"); return LAG_ESTATE; }
     cudaStream_t s0 = g->m[0]->stream;
     CKC(cudaEventRecord(g->ev[0], s0));
     for (size_t r = 1; r < g->m.size(); ++r)
-        if (g->m[r]->stream != s0) CKC(cudaStreamWaitEvent(g->m[r]->stream, g->ev[0], 0));
+        if (g->m[r] && g->m[r]->stream != s0) CKC(cudaStreamWaitEvent(g->m[r]->stream, g->ev[0], 0));
     return LAG_OK;
 }
 
@@ -857,7 +860,7 @@ extern "C" lag_status lag_local_group(lag_ctx* ctxs, int32_t n) {
         lag_ctx_s* c = ctxs[r];
         if (!c || c->cfg.mode != LAG_COMM || c->cfg.exchange != LAG_XCHG_LOCAL || c->cfg.rank != r ||
             c->cfg.nranks != n || c->cfg.device != ctxs[0]->cfg.device ||
-            c->cfg.dim != ctxs[0]->cfg.dim || c->cfg.ghost < 1) {
+            c->cfg.dim != ctxs[0]->cfg.dim || (c->cfg.ghost < 1 && n > 1)) {
             lag_set_error(nullptr, "lag_local_group: context %d is not rank %d of an n = %d LAG_XCHG_LOCAL "
                           "COMM group on the same device", r, r, n);
             return LAG_EINVAL;
@@ -867,8 +870,10 @@ extern "C" lag_status lag_local_group(lag_ctx* ctxs, int32_t n) {
                 lag_set_error(nullptr, "lag_local_group: context %d has another grid or layout", r);
                 return LAG_EINVAL;
             }
-        if (c->group || c->seeded) {
-            lag_set_error(nullptr, "lag_local_group: context %d is already grouped or seeded", r);
+        if (c->group || c->seeded || c->comm->slots) {
+            // (a failed earlier call may have set up some blocks: destroy the
+            // contexts and create them again)
+            lag_set_error(nullptr, "lag_local_group: context %d is already grouped, set up or seeded", r);
             return LAG_ESTATE;
         }
     }
