@@ -38,17 +38,25 @@ struct AppendArgs {
 __device__ __forceinline__ void append_body(const AppendArgs& a, int cta, int ncta) {
     __shared__ uint32_t pre[kMaxOff + 1];
     __shared__ uint32_t old_tiles, total_s;
+    // the headers and the tile count are read in parallel (one load
+    // latency, not one per neighbour), then thread 0 takes the prefix sum
+    if (threadIdx.x < (unsigned)a.npeers) {
+        const int p = threadIdx.x;
+        uint32_t c = *reinterpret_cast<const volatile uint32_t*>(a.recv[p]);
+        if (c > a.cap[p]) { c = a.cap[p]; atomicOr(a.words + W_ERR, ERR_OVERFLOW); }
+        pre[p + 1] = c;
+    }
+    if (threadIdx.x == 32) old_tiles = *reinterpret_cast<const volatile uint32_t*>(a.words + W_NTILES);
+    __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t s = 0;
         for (int p = 0; p < a.npeers; ++p) {
+            const uint32_t c = pre[p + 1];
             pre[p] = s;
-            uint32_t c = *reinterpret_cast<const volatile uint32_t*>(a.recv[p]);
-            if (c > a.cap[p]) { c = a.cap[p]; atomicOr(a.words + W_ERR, ERR_OVERFLOW); }
             s += c;
         }
         if (a.discard) s = 0;
         pre[a.npeers] = s;
-        old_tiles = *reinterpret_cast<const volatile uint32_t*>(a.words + W_NTILES);
         const uint32_t room = (uint32_t)(a.cap_tiles - (int)old_tiles) * kTile;
         if (s > room) { atomicOr(a.words + W_ERR, ERR_OVERFLOW); s = room; }
         total_s = s;

@@ -732,6 +732,7 @@ lag_status lag_comm_async_error(lag_ctx_s* ctx) {
 
 namespace lag {
 constexpr int kLocalMax = 64;
+constexpr int kLocalAppendCtas = 8;   // a block receives a few hundred hand-offs per cycle
 struct LocalBox {               // ghost box of block dst filled from block src's interior
     int dst, src;
     int dx0, dy0, dz0;          // dst slice coordinates
@@ -742,6 +743,9 @@ struct LocalBox {               // ghost box of block dst filled from block src'
 struct LocalCopyArgs {
     const LocalBox* boxes;
     int nbox;
+    int nybox;                  // grid rows running ghost boxes (nbox, or 2 nbox with v_t boxes)
+    const AppendArgs* app;      // [n] per-block append arguments (rows nybox .. nybox + n - 1)
+    int app_ctas;               // CTAs per block's append
     int dim;
     int64_t total;              // floats over all boxes (one slice)
     unsigned long long fill_v0; // bit r: block r's v_t needs its ghosts too
@@ -758,26 +762,31 @@ __global__ void __launch_bounds__(256) local_append_kernel(const AppendArgs* __r
     append_body(a, blockIdx.x, gridDim.x);
 }
 
+// blockIdx.y = ghost box (v_t1 boxes, then the v_t boxes of the blocks whose
+// v_t is not the previous call's v_t1); the CTAs of a row stride over the
+// box's floats (32-bit index math: a box is far below 2^31 floats)
 __global__ void __launch_bounds__(256) local_ghost_kernel(const LocalCopyArgs a) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * a.total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int slice = i >= a.total ? 0 : 1;         // first v_t1, then v_t
-        const int64_t j = slice ? i : i - a.total;
-        int lo = 0, hi = a.nbox - 1;                    // box with off <= j (offsets ascending)
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (a.boxes[mid].off <= j) lo = mid; else hi = mid - 1;
-        }
-        const LocalBox& b = a.boxes[lo];
-        if (!slice && !((a.fill_v0 >> b.dst) & 1ull)) continue;
-        const int64_t k = j - b.off;
-        const int comp = (int)(k % a.dim);
-        const int64_t node = k / a.dim;
-        const int x = (int)(node % b.nx), y = (int)((node / b.nx) % b.ny), z = (int)(node / ((int64_t)b.nx * b.ny));
-        const float* src = slice ? a.v1[b.src] : a.v0[b.src];
-        float* dst = slice ? a.v1[b.dst] : a.v0[b.dst];
-        dst[(int64_t)a.dim * ((b.dx0 + x) + (int64_t)a.sx[b.dst] * (b.dy0 + y) + (int64_t)a.sxy[b.dst] * (b.dz0 + z)) + comp] =
-            src[(int64_t)a.dim * ((b.sx0 + x) + (int64_t)a.sx[b.src] * (b.sy0 + y) + (int64_t)a.sxy[b.src] * (b.sz0 + z)) + comp];
+    const int y = blockIdx.y;
+    if (y >= a.nybox) {                                 // grid row of a block's append
+        if ((int)blockIdx.x >= a.app_ctas) return;
+        const AppendArgs& ap = a.app[y - a.nybox];
+        if (ap.npeers) append_body(ap, blockIdx.x, a.app_ctas);
+        return;
+    }
+    const int slice = y < a.nbox ? 1 : 0;
+    const LocalBox& b = a.boxes[slice ? y : y - a.nbox];
+    if (!slice && !((a.fill_v0 >> b.dst) & 1ull)) return;
+    const int dim = a.dim;
+    const int nf = b.nx * b.ny * b.nz * dim;
+    const int rowf = b.nx * dim;
+    const float* src = slice ? a.v1[b.src] : a.v0[b.src];
+    float* dst = slice ? a.v1[b.dst] : a.v0[b.dst];
+    const int ssx = a.sx[b.src], ssxy = a.sxy[b.src], dsx = a.sx[b.dst], dsxy = a.sxy[b.dst];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nf; k += gridDim.x * blockDim.x) {
+        const int row = k / rowf, within = k - row * rowf;
+        const int yy = row % b.ny, zz = row / b.ny;
+        dst[(int64_t)dim * (b.dx0 + (int64_t)dsx * (b.dy0 + yy) + (int64_t)dsxy * (b.dz0 + zz)) + within] =
+            src[(int64_t)dim * (b.sx0 + (int64_t)ssx * (b.sy0 + yy) + (int64_t)ssxy * (b.sz0 + zz)) + within];
     }
 }
 
@@ -791,6 +800,7 @@ struct LocalGroup {
     std::vector<LocalBox> boxes;
     LocalBox* d_boxes = nullptr;
     int64_t total = 0;
+    int max_box_floats = 0;
     AppendArgs* d_app = nullptr;        // [n] per-block append arguments
     std::vector<cudaEvent_t> ev;        // per block: join points
     int alive = 0;
@@ -846,7 +856,7 @@ static lag_status local_appends(lag_ctx_s* ctx) {
     bool any = false;
     for (lag_ctx_s* c : g->m) any |= !c->comm->peers.empty();
     if (!any) return LAG_OK;
-    local_append_kernel<<<dim3(std::max(1, c0->num_sms / 2), (unsigned)g->m.size()), 256, 0, c0->stream>>>(g->d_app);
+    local_append_kernel<<<dim3(kLocalAppendCtas, (unsigned)g->m.size()), 256, 0, c0->stream>>>(g->d_app);
     ++ctx->launches;
     CKC(cudaGetLastError());
     for (lag_ctx_s* c : g->m) c->comm->pending = false;
@@ -915,6 +925,7 @@ extern "C" lag_status lag_local_group(lag_ctx* ctxs, int32_t n) {
             b.nx = rb.nx; b.ny = rb.ny; b.nz = rb.nz;
             b.off = g->total;
             g->total += (int64_t)b.nx * b.ny * b.nz * ctxs[0]->cfg.dim;
+            g->max_box_floats = std::max(g->max_box_floats, b.nx * b.ny * b.nz * ctxs[0]->cfg.dim);
             g->boxes.push_back(b);
         }
     }
@@ -978,25 +989,28 @@ lag_status lag_local_run_cycle(lag_ctx_s* ctx) {
     lag_status st = local_join_in(ctx);
     if (st != LAG_OK) return st;
     lag_ctx_s* c0 = g->m[0];
-    if (g->total > 0) {
-        LocalCopyArgs a{};
-        a.boxes = g->d_boxes;
-        a.nbox = (int)g->boxes.size();
-        a.dim = ctx->cfg.dim;
-        a.total = g->total;
-        for (int r = 0; r < n; ++r) {
-            a.v0[r] = g->rec[r].v0;
-            a.v1[r] = g->rec[r].v1;
-            a.sx[r] = g->m[r]->sx;
-            a.sxy[r] = g->m[r]->sxy;
-            if (!g->rec[r].v0_prev) a.fill_v0 |= 1ull << r;
-        }
-        const int blocks = (int)std::min<int64_t>((2 * g->total + 255) / 256, (int64_t)ctx->num_sms * 8);
-        local_ghost_kernel<<<std::max(1, blocks), 256, 0, c0->stream>>>(a);
-        ++ctx->launches;
-        CKC(cudaGetLastError());
+    // one launch: grid rows [0, nybox) copy ghost boxes, the next n rows
+    // append each block's hand-offs
+    LocalCopyArgs a{};
+    a.boxes = g->d_boxes;
+    a.nbox = (int)g->boxes.size();
+    a.dim = ctx->cfg.dim;
+    a.total = g->total;
+    for (int r = 0; r < n; ++r) {
+        a.v0[r] = g->rec[r].v0;
+        a.v1[r] = g->rec[r].v1;
+        a.sx[r] = g->m[r]->sx;
+        a.sxy[r] = g->m[r]->sxy;
+        if (!g->rec[r].v0_prev) a.fill_v0 |= 1ull << r;
     }
-    if ((st = local_appends(ctx)) != LAG_OK) return st;
+    a.nybox = a.nbox * (a.fill_v0 ? 2 : 1);
+    a.app = g->d_app;
+    a.app_ctas = kLocalAppendCtas;
+    const int bx = std::max(kLocalAppendCtas, std::min((g->max_box_floats + 255) / 256, 64));
+    local_ghost_kernel<<<dim3(bx, (unsigned)(a.nybox + n)), 256, 0, c0->stream>>>(a);
+    ++ctx->launches;
+    CKC(cudaGetLastError());
+    for (lag_ctx_s* c : g->m) c->comm->pending = false;
     return local_join_out(ctx);
 }
 
