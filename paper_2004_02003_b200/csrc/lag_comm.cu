@@ -136,41 +136,43 @@ struct BoxArgs {
     int64_t total;       // floats over all boxes
 };
 
-__device__ __forceinline__ int find_box(const Box* b, int nbox, int64_t i) {
-    int k = 0;
-    while (k + 1 < nbox && b[k + 1].off <= i) ++k;
-    return k;
+// One grid row per box (blockIdx.y), the row's CTAs striding over the box's
+// floats: the buffer holds box after box (Box::off), each x-fastest with the
+// components innermost (32-bit index math: a box is far below 2^31 floats).
+__device__ __forceinline__ int64_t box_node(const BoxArgs& a, const Box& b, int k, int& comp) {
+    const int rowf = b.nx * a.dim;
+    const int row = k / rowf, within = k - row * rowf;
+    const int y = row % b.ny, z = row / b.ny;
+    comp = within;
+    return (int64_t)a.dim * (b.x0 + (int64_t)a.sx * (b.y0 + y) + (int64_t)a.sxy * (b.z0 + z));
 }
 
-__global__ void halo_pack_kernel(BoxArgs a) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int k = find_box(a.boxes, a.nbox, i);
-        const Box b = a.boxes[k];
-        const int64_t j = i - b.off;
-        const int comp = (int)(j % a.dim);
-        const int64_t node = j / a.dim;
-        const int x = (int)(node % b.nx), y = (int)((node / b.nx) % b.ny), z = (int)(node / ((int64_t)b.nx * b.ny));
-        const float* src = b.slice ? a.v1 : a.v0;
-        a.buf[i] = src[(int64_t)a.dim * ((b.x0 + x) + (int64_t)a.sx * (b.y0 + y) + (int64_t)a.sxy * (b.z0 + z)) + comp];
+__global__ void __launch_bounds__(256) halo_pack_kernel(BoxArgs a) {
+    const Box& b = a.boxes[blockIdx.y];
+    const int nf = b.nx * b.ny * b.nz * a.dim;
+    const float* src = b.slice ? a.v1 : a.v0;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nf; k += gridDim.x * blockDim.x) {
+        int within;
+        const int64_t o = box_node(a, b, k, within);
+        a.buf[b.off + k] = src[o + within];
     }
 }
 
-// the received ghost layers (grid-stride) and the received particles
-// (append_body) in one launch
-__global__ void __launch_bounds__(256) halo_unpack_append_kernel(BoxArgs a, AppendArgs ap) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int k = find_box(a.boxes, a.nbox, i);
-        const Box b = a.boxes[k];
-        const int64_t j = i - b.off;
-        const int comp = (int)(j % a.dim);
-        const int64_t node = j / a.dim;
-        const int x = (int)(node % b.nx), y = (int)((node / b.nx) % b.ny), z = (int)(node / ((int64_t)b.nx * b.ny));
-        float* dst = b.slice ? a.v1 : a.v0w;
-        dst[(int64_t)a.dim * ((b.x0 + x) + (int64_t)a.sx * (b.y0 + y) + (int64_t)a.sxy * (b.z0 + z)) + comp] = a.buf[i];
+// the received ghost layers (grid rows [0, nbox)) and the received particles
+// (grid row nbox, append_body on its first `app_ctas` CTAs) in one launch
+__global__ void __launch_bounds__(256) halo_unpack_append_kernel(BoxArgs a, AppendArgs ap, int app_ctas) {
+    if ((int)blockIdx.y == a.nbox) {
+        if ((int)blockIdx.x < app_ctas) append_body(ap, blockIdx.x, app_ctas);
+        return;
     }
-    append_body(ap, blockIdx.x, gridDim.x);
+    const Box& b = a.boxes[blockIdx.y];
+    const int nf = b.nx * b.ny * b.nz * a.dim;
+    float* dst = b.slice ? a.v1 : a.v0w;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nf; k += gridDim.x * blockDim.x) {
+        int within;
+        const int64_t o = box_node(a, b, k, within);
+        dst[o + within] = a.buf[b.off + k];
+    }
 }
 
 struct RouteArgs {
@@ -514,6 +516,14 @@ static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity) {
 }
 
 // One NCCL group: optional halo boxes (v1 [+ v0]) and the pending particle slots.
+// CTAs per box row: enough for the largest box at one float per thread (<= 64)
+static int box_ctas(const Comm* cm) {
+    int64_t mx = 1;
+    for (const Box& b : cm->send_boxes) mx = std::max<int64_t>(mx, (int64_t)b.nx * b.ny * b.nz);
+    for (const Box& b : cm->recv_boxes) mx = std::max<int64_t>(mx, (int64_t)b.nx * b.ny * b.nz);
+    return (int)std::max<int64_t>(1, std::min<int64_t>((3 * mx + 255) / 256, 64));
+}
+
 static lag_status exchange(lag_ctx_s* ctx, float* v0, float* v1, bool halo, bool halo_v0) {
     Comm* cm = ctx->comm;
     const int D = ctx->cfg.dim;
@@ -526,8 +536,7 @@ static lag_status exchange(lag_ctx_s* ctx, float* v0, float* v1, bool halo, bool
         BoxArgs b{};
         b.v0 = v0; b.v1 = v1; b.v0w = v0; b.boxes = cm->d_send_boxes; b.nbox = nbox;
         b.buf = cm->halo_send; b.sx = ctx->sx; b.sxy = ctx->sxy; b.dim = D; b.total = sfl;
-        const int blocks = (int)std::min<int64_t>((sfl + 255) / 256, (int64_t)ctx->num_sms * 8);
-        halo_pack_kernel<<<blocks, 256, 0, ctx->stream>>>(b);
+        halo_pack_kernel<<<dim3(box_ctas(cm), (unsigned)nbox), 256, 0, ctx->stream>>>(b);
         ++ctx->launches;
         CKC(cudaGetLastError());
     }
@@ -553,8 +562,8 @@ static lag_status exchange(lag_ctx_s* ctx, float* v0, float* v1, bool halo, bool
         b.v0 = v0; b.v1 = v1; b.v0w = v0; b.boxes = cm->d_recv_boxes; b.nbox = nbox;
         b.buf = cm->halo_recv; b.sx = ctx->sx; b.sxy = ctx->sxy; b.dim = D; b.total = rfl;
         const AppendArgs ap = append_args(ctx, -1);
-        const int blocks = (int)std::max<int64_t>(ctx->num_sms, std::min<int64_t>((rfl + 255) / 256, (int64_t)ctx->num_sms * 8));
-        halo_unpack_append_kernel<<<blocks, 256, 0, ctx->stream>>>(b, ap);
+        const int app_ctas = 16;
+        halo_unpack_append_kernel<<<dim3(std::max(app_ctas, box_ctas(cm)), (unsigned)(nbox + 1)), 256, 0, ctx->stream>>>(b, ap, app_ctas);
         ++ctx->launches;
         CKC(cudaGetLastError());
         return LAG_OK;
