@@ -6,8 +6,9 @@ For one configuration and block layout, on one GPU:
   * COMM: the same blocks as one LAG_XCHG_LOCAL group (ghost copy + hand-off
     appends every cycle, return to origin at the write cycle), one stream
     per block;
-  * per cycle the device time of the whole layout (event window from a fork
-    after the L2 flush to the join of every block's stream) for both arms:
+  * per cycle the device time of the whole layout (the cycle of every block
+    captured as a CUDA graph, fork to the blocks' streams and join back,
+    replayed once between two events after an L2 flush) for both arms:
     BTO/COMM speed-up = mean COMM cycle time / mean BTO cycle time (write
     cycles excluded, P:365-367);
   * per interval: Eq. 5 over the seeds valid in the COMM map, with BTO holes
@@ -77,16 +78,28 @@ def main():
         a["n"] = [c.seed(stride) for c in a["ctxs"]]
 
     def window(arm, fn):
+        """One cycle of every block, captured as a CUDA graph (fork from the
+        capture stream to the blocks' streams, join back) and replayed once
+        between two events: the device time of the layout's cycle without
+        the host's launch overhead (eight blocks' calls would otherwise be
+        host-bound)."""
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=main_s):
+            ev = torch.cuda.Event()
+            ev.record(main_s)
+            for st in arm["streams"]:
+                st.wait_event(ev)
+            fn()
+            for st in arm["streams"]:
+                e = torch.cuda.Event()
+                e.record(st)
+                main_s.wait_event(e)
+        flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(main_s)
-        for st in arm["streams"]:
-            st.wait_event(e0)
-        fn()
-        for st in arm["streams"]:
-            ev = torch.cuda.Event()
-            ev.record(st)
-            main_s.wait_event(ev)
+        gr.replay()
         e1.record(main_s)
+        arm.setdefault("graphs", []).append(gr)      # alive until the events are read
         return e0, e1
 
     # global seed lattice (x fastest) and each block's seeds in it
@@ -132,7 +145,6 @@ def main():
                         sl.append((s0, cut(V1, b, G)))
                     prev[name] = [x[1] for x in sl]
                     torch.cuda.current_stream().synchronize()
-                    flush.zero_()
 
                     def adv(arm=arm, sl=sl):
                         for c, (s0, s1) in zip(arm["ctxs"], sl):
@@ -141,6 +153,8 @@ def main():
             torch.cuda.synchronize()
         for name in ev:
             cyc[name] += [a.elapsed_time(b) for a, b in ev[name]]
+        for arm in arms.values():
+            arm["graphs"] = []
         # write cycle: both maps in global seed order
         maps = {}
         for name, arm in arms.items():
@@ -192,7 +206,8 @@ def main():
                            "greatest_max_L2": gmax, "average_max_L2": amax,
                            "excluded_outside_hull": int(sum(r["excluded"] for r in rows))}
     out["method"] = ("one GPU; BTO = one context per block, COMM = LAG_XCHG_LOCAL group of the same "
-                     "blocks; per-cycle device time of the whole layout (L2 flushed before each cycle); "
+                     "blocks; per-cycle device time of the whole layout (each cycle captured as a CUDA graph "
+                     "and replayed once, L2 flushed before each cycle); "
                      "Eq. 5/6 over seeds valid in COMM, holes by Delaunay+barycentric (Qhull QJ, first "
                      f"{args.delaunay_intervals} intervals) and GridFill (all intervals)")
     print(json.dumps({k: v for k, v in out.items() if k != "per_interval"}), flush=True)

@@ -15,11 +15,35 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def main():
     files = sys.argv[1:] or sorted(glob.glob(os.path.join(ROOT, "profiles", "tradeoff_*.json")))
-    rows = []
+    # the flow maps are deterministic (bitwise), so a timing refresh (file
+    # ending in _t.json) keeps the agreement columns of the full run of the
+    # same row and replaces only its per-cycle times
+    full = {}
+    for f in files:
+        if f.endswith("tradeoff_table.json") or f.endswith("_t.json"):
+            continue
+        d = json.load(open(f))
+        full[(d["config"], tuple(d["layout"]), d["interval"], d.get("dtmul", 1.0))] = d
+    merged = []
     for f in files:
         if f.endswith("tradeoff_table.json"):
             continue
         d = json.load(open(f))
+        key = (d["config"], tuple(d["layout"]), d["interval"], d.get("dtmul", 1.0))
+        if f.endswith("_t.json"):
+            base = full.get(key)
+            if base:                       # agreement of the full run (more intervals), timing of the refresh
+                for m in ("delaunay", "gridfill"):
+                    if m in base:
+                        d[m] = base[m]
+                d["discarded_pct"] = base["discarded_pct"]
+                d["intervals"] = base["intervals"]
+            d["_timing_from"] = os.path.relpath(f, ROOT)
+            merged.append((f, d))
+        elif not os.path.exists(f[:-5] + "_t.json"):
+            merged.append((f, d))
+    rows = []
+    for f, d in merged:
         row = {"config": d["config"], "layout": "x".join(map(str, d["layout"])), "stride": d["stride"],
                "interval": d["interval"], "dtmul": d.get("dtmul", 1.0), "intervals": d["intervals"],
                "seeds": d["seeds"], "bto_us_per_cycle": 1e3 * d["bto_ms_per_cycle"],

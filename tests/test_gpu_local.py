@@ -323,3 +323,31 @@ def test_cuda_graph_replay_equals_direct_calls():
     for x, y in zip(o, ref[:3]):
         assert np.array_equal(x.cpu().numpy(), y)
     ctx.close()
+
+
+def test_bto_padded_rows_equal_dense():
+    """row_pitch_bytes: BTO on slices whose rows carry NaN
+    padding nodes gives bitwise the dense result (padding is never read)."""
+    import torch
+    import paper_2004_02003_b200 as P
+    cfg = L.make_config("C2", scale=29, nranks=8)
+    g = cfg["grid"]
+    sl = global_slices(cfg, 6)
+    b = L.decompose(g, cfg["layout"])[3]
+    ref = gpu_block(cfg, b, sl, 1)
+    ext = L.block_slice_extent(g, b, 0)
+    pad = 5
+    dev = [torch.from_numpy(poisoned_block_slice(V, g, b, 0, pad)).cuda() for V in sl]
+    ctx = P.Context(P.make_config(3, g.nodes, g.origin, g.spacing, b.lo, b.hi,
+                                  stream=torch.cuda.current_stream().cuda_stream,
+                                  row_pitch_bytes=(ext[0] + pad) * 12))
+    n = ctx.seed(1)
+    for k in range(len(dev) - 1):
+        ctx.advect(dev[k], dev[k + 1], cfg["dt"])
+    out = (torch.empty((n, 3), dtype=torch.float64, device="cuda"), torch.empty((n, 3), dtype=torch.float64, device="cuda"),
+           torch.empty((n,), dtype=torch.uint8, device="cuda"))
+    ctx.extract(*out)
+    assert ctx.stats()["device_error"] == 0
+    for x, y in zip(out, ref[:3]):
+        assert np.array_equal(x.cpu().numpy(), y)
+    ctx.close()
