@@ -173,7 +173,8 @@ LAG_API lag_status lag_init(const lag_config* cfg, lag_ctx* out);
  * node g with g_a = 0 (mod stride) and block_lo_a <= g_a < block_hi_a (x-fastest
  * seed order), discarding any previous particles (reading R4 in
  * DESIGN.md).  *n_seeds_out = number of seeds.
- * Errors: LAG_EINVAL (stride < 1), LAG_EEMPTY (no lattice node in the block).
+ * Errors: LAG_EINVAL (stride < 1), LAG_EEMPTY (no lattice node in the block),
+ * LAG_ESTATE (a LAG_XCHG_LOCAL context not yet in a lag_local_group).
  */
 LAG_API lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out);
 
@@ -193,8 +194,9 @@ LAG_API lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out);
  * step per cycle): identical results, corners gathered once.
  * LAG_XCHG_LOCAL: collective over the group in the same sense: each block's
  * call records its (device) slices; the call that completes the group's cycle
- * enqueues the whole cycle of every block (ghost copy, appends, advection) on
- * the group's stream.  The slices must stay unmodified until then.
+ * enqueues the whole cycle of every block (one exchange launch for the ghost
+ * copies and appends on block 0's stream, then each block's advection on its
+ * own stream, joined by events).  The slices must stay unmodified until then.
  * Errors: LAG_ESTATE (no lag_seed; LOCAL: a block called twice in one group
  * cycle, or before every block extracted), LAG_EINVAL (dt <= 0 or
  * non-finite, NULL slice; LOCAL: host slice), LAG_ECUDA, LAG_ENCCL (an NCCL
@@ -247,12 +249,13 @@ LAG_API lag_status lag_extract_ex(lag_ctx ctx, int64_t interval_index, double* s
  * blocks then advance concurrently; the group joins the streams with events
  * around each exchange and write cycle, block 0's stream carries the
  * exchange kernels).  Call once, after every lag_init and before the first
- * lag_seed.  The group lives until its
- * last context is destroyed.  Not collective across processes: the whole
- * group is in this process (the single-GPU form of the COMM baseline, used
- * to run several blocks of a decomposition on one B200).
+ * lag_seed.  The group lives until its last context is destroyed.  Not
+ * collective across processes: the whole group is in this process (the
+ * single-GPU form of the COMM baseline, used to run several blocks of a
+ * decomposition on one B200).
  * Errors: LAG_EINVAL (mismatched contexts, wrong transport, n out of range),
- * LAG_ESTATE (already grouped or already seeded), LAG_ENOMEM, LAG_ECUDA.
+ * LAG_ESTATE (already grouped, set up by an earlier failed call, or seeded),
+ * LAG_ENOMEM, LAG_ECUDA.
  */
 LAG_API lag_status lag_local_group(lag_ctx* ctxs, int32_t n);
 
