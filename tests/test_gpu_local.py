@@ -351,3 +351,30 @@ def test_bto_padded_rows_equal_dense():
     for x, y in zip(out, ref[:3]):
         assert np.array_equal(x.cpu().numpy(), y)
     ctx.close()
+
+
+def test_local_comm_cfl_above_one_latches_ghost_error():
+    """A stage sample more than one ghost layer outside the block (CFL >= 1)
+    cannot be interpolated from the exchanged data: the particle stops and
+    LAG_EGHOST is latched and reported by the write cycle (include/lag.h)."""
+    import torch
+    import paper_2004_02003_b200 as P
+    cfg = L.make_config("C2", scale=17, nranks=2)
+    cfg["dt"] *= 20.0                                    # CFL ~ 3 cells per cycle
+    g = cfg["grid"]
+    blocks = L.decompose(g, (2, 1, 1))
+    sl = global_slices(cfg, 2)
+    cfgs = [P.make_config(3, g.nodes, g.origin, g.spacing, b.lo, b.hi, mode=P.LAG_COMM, ghost=1, rank=b.rank,
+                          nranks=2, layout=(2, 1, 1), stream=torch.cuda.current_stream().cuda_stream,
+                          exchange=P.LAG_XCHG_LOCAL) for b in blocks]
+    grp = P.LocalGroup(cfgs)
+    grp.seed(1)
+    dev = [[torch.from_numpy(poisoned_block_slice(V, g, b, 1)).cuda() for b in blocks] for V in sl]
+    grp.advect(dev[0], dev[1], cfg["dt"])
+    st = grp.stats()
+    assert any(s["device_error"] == P.LAG_EGHOST for s in st)
+    with pytest.raises(P.LagError) as e:
+        for b in grp.blocks:
+            b.extract()
+    assert e.value.status == P.LAG_EGHOST
+    grp.close()
