@@ -62,9 +62,9 @@ enum : int { T_INBOX = 0, T_INBOX_PAR = 1, T_OUTBOX = 2, T_HALO = 3, T_RECV = 4,
 // resident (a CTA waiting for the neighbours' signal must not keep one of
 // ours that has not packed from running), so the grid is capped at the
 // resident capacity
-__global__ void __launch_bounds__(256) peer_exchange_kernel(XchgArgs x, AppendArgs ap) {
+__global__ void __launch_bounds__(256) peer_exchange_kernel(XchgArgs x, AppendArgs ap, int npull) {
     xchg_pack_signal(x, blockIdx.x, gridDim.x);
-    xchg_wait_pull(x, ap, blockIdx.x, gridDim.x);
+    if ((int)blockIdx.x < npull) xchg_wait_pull(x, ap, blockIdx.x, npull);
 }
 
 __global__ void __launch_bounds__(256) peer_wait_pull_kernel(XchgArgs x, AppendArgs ap) {
@@ -266,7 +266,9 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
     if (halo) {
         const int64_t work = std::max(x.sfl, x.rtotal);
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, cap));
-        peer_exchange_kernel<<<g, 256, 0, st>>>(x, ap);
+        // waiters: enough for one round of remote loads (8 in flight per thread)
+        const int npull = (int)std::max<int64_t>(std::min<int64_t>(8, g), std::min<int64_t>((x.rtotal + 2047) / 2048, g));
+        peer_exchange_kernel<<<g, 256, 0, st>>>(x, ap, npull);
     } else {
         const int gb = (int)std::max<int64_t>(1, std::min<int64_t>((x.rtotal + 255) / 256, cap));
         peer_wait_pull_kernel<<<gb, 256, 0, st>>>(x, ap);

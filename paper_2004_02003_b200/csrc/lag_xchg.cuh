@@ -18,13 +18,14 @@ struct PeerBox {            // one ghost box to fill from a remote outbox
     int slice;
 };
 
-// Per-cycle exchange in two multi-CTA kernels (the advect kernel signals the
-// hand-offs itself):
+// Per-cycle exchange (the advect kernel signals the hand-offs itself):
 //   A: pack my ghost sources (grid-stride); the last CTA to finish fences and
 //      signals halo(seq) to every neighbour;
-//   B: every CTA waits (bounded) for all neighbours' halo(seq) and
-//      particles(seq-1), then pulls its share of the ghost layers with remote
-//      loads; CTA 0 also appends the previous cycle's hand-offs.
+//   B: the first `npull` CTAs wait (bounded) for all neighbours' halo(seq)
+//      and particles(seq-1), pull their share of the ghost layers with remote
+//      loads and append the previous cycle's hand-offs.  Few waiters: a few
+//      hundred CTAs polling one flag word queue up its L2 slice and delay the
+//      neighbour's remote store to it by several microseconds.
 struct XchgArgs {
     float* v0;
     float* v1;
@@ -65,12 +66,15 @@ __device__ __forceinline__ void xchg_pack_signal(const XchgArgs& x, int cta, int
     }
     __syncthreads();                                  // the CTA's packs are visible to thread 0
     if (threadIdx.x == 0 && x.signal_halo) {
-        __threadfence_system();                       // cumulative: orders the CTA's packs
+        // release at GPU scope (the packs and the counter live on this GPU);
+        // the last CTA's system-scope fence then releases everything it has
+        // observed to the neighbours (causality is transitive), so only one
+        // CTA pays the system-scope fence
+        __threadfence();
         if (atomicAdd(x.done_ctas, 1u) == (uint32_t)ncta - 1) {   // last CTA: halo(seq) ready
             *x.done_ctas = 0u;
             __threadfence_system();
             for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(x.halo_flag[p]) = x.seq;
-            __threadfence_system();
         }
     }
 }
