@@ -152,7 +152,7 @@ typedef struct {
     int32_t device_error;    /* latched async condition as a lag_status (0 = none)          */
     int32_t pad_;
     double  phase_ms[3];     /* with env LAG_PHASE_TIMING=1: cumulative device time of the
-                                pre-advect exchange, the advect kernel, the post-advect signal */
+                                pre-advect exchange, the advect kernel, the post-advect step  */
 } lag_stats_t;
 
 /*
@@ -172,7 +172,9 @@ LAG_API lag_status lag_init(const lag_config* cfg, lag_ctx* out);
  * lag_seed — start a new interval: place one particle on every global lattice
  * node g with g_a = 0 (mod stride) and block_lo_a <= g_a < block_hi_a (x-fastest
  * seed order), discarding any previous particles (reading R4 in
- * DESIGN.md).  *n_seeds_out = number of seeds.
+ * DESIGN.md).  *n_seeds_out = number of seeds.  COMM: every rank of the
+ * decomposition reseeds at the same cycle (a reseed in the middle of an
+ * interval drops the hand-offs in flight on every rank alike).
  * Errors: LAG_EINVAL (stride < 1), LAG_EEMPTY (no lattice node in the block),
  * LAG_ESTATE (a LAG_XCHG_LOCAL context not yet in a lag_local_group).
  */

@@ -399,7 +399,7 @@ static void fold_phases(lag_ctx_s* ctx) {
         float ms;
         for (int j = 0; j < 3; ++j)
             // overlap (LAG_XCHG_PEER_OVERLAP): snapshot, pass 1 (exchange CTAs +
-            // ghost-free tiles), pass 2 + signal
+            // ghost-free tiles), pass 2
             if (cudaEventElapsedTime(&ms, ctx->ph_ev[i][j], ctx->ph_ev[i][j + 1]) == cudaSuccess) ctx->ph_ms[j] += ms;
     }
     ctx->ph_n = 0;
@@ -517,10 +517,9 @@ static lag_status advect_enqueue(lag_ctx_s* ctx, float* d0, float* d1, double dt
     };
     if (overlap) {
         // pass 1: exchange CTAs + ghost-free tiles; pass 2 (stream-ordered after
-        // it): deferred tiles and this cycle's arrivals; its last warp signals
+        // it): deferred tiles and this cycle's arrivals
         AdvectArgs a1 = a;
         a1.pass = 1;
-        a1.n_sig = 0;
         const int nb1 = std::max(blocks, kXchgCtas + 1);
         if (ev) cudaEventRecord(ev[1], ctx->stream);
         if (D == 3) {

@@ -14,6 +14,11 @@ struct Box {            // local slice coordinates
 };
 
 
+// whose headers the append resets: the NCCL transport's outgoing slots (sent
+// this cycle), the consumed inbox (LOCAL transport), or none (peer
+// transport: the sender resets its own slots once the receiver has read them)
+enum : int { RESET_SLOTS = 0, RESET_RECV = 1, RESET_NONE = 2 };
+
 struct AppendArgs {
     float4* state;
     uint8_t* tile_count;
@@ -26,7 +31,7 @@ struct AppendArgs {
     float4* slots;                  // outgoing slots: headers reset here (NCCL)
     int32_t slot_base[kMaxOff];
     int noff;
-    int zero_recv;                  // peer/local transport: reset the consumed inbox headers instead
+    int reset;                      // headers reset after the append: RESET_* below
     int discard;                    // drop the records (a reseed in the middle of an interval)
 };
 
@@ -79,9 +84,9 @@ __device__ __forceinline__ void append_body(const AppendArgs& a, int cta, int nc
         __threadfence();
         if (atomicAdd(a.words + W_APPEND_DONE, 1u) == (uint32_t)ncta - 1) {      // last CTA
             a.words[W_APPEND_DONE] = 0u;
-            if (a.zero_recv) {
+            if (a.reset == RESET_RECV) {
                 for (int p = 0; p < a.npeers; ++p) *reinterpret_cast<uint32_t*>(a.recv[p]) = 0u;
-            } else {
+            } else if (a.reset == RESET_SLOTS) {
                 for (int k = 0; k < a.noff; ++k) *reinterpret_cast<uint32_t*>(a.slots + a.slot_base[k]) = 0u;
             }
             a.words[W_NTILES] = old_tiles + new_tiles;

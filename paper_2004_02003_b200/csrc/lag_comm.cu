@@ -31,21 +31,20 @@ using namespace lag;
 struct PeerState;
 lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>& prank,
                          const std::vector<int>& poff, const std::vector<int>& pback,
-                         const std::vector<uint32_t>& cap_recv, int64_t halo_send_floats,
+                         const std::vector<uint32_t>& cap_send, int64_t halo_send_floats,
                          const std::vector<int64_t>& send_box_off, const std::vector<int64_t>& send_box_by_off,
                          const std::vector<int>& recv_box_x0y0z0nxnynz, int64_t halo_recv_floats,
                          PeerState** out);
 void lag_peer_destroy(PeerState* ps);
 float4* lag_peer_remote_slot(PeerState* ps, int i, int prank, int pback, int q);
-float4* lag_peer_inbox_slot(PeerState* ps, int q, int poff);
+float4* lag_peer_my_slot(PeerState* ps, int q, int poff);
 float* lag_peer_outbox(PeerState* ps, int q);
 unsigned long long& lag_peer_seq(PeerState* ps);
-uint32_t* lag_peer_done_counter(PeerState* ps);
 unsigned long long* lag_peer_remote_flag(PeerState* ps, int i, int kind, int pback);
 lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_boxes, int nsend,
                              int64_t sfl, float* v0, float* v1, bool with_v0, bool halo,
                              const std::vector<int>& poff, const std::vector<int>& pback,
-                             unsigned long long need_part, const void* append_args);
+                             const void* append_args);
 
 #define CKC(call)                                                                  \
     do {                                                                           \
@@ -435,7 +434,7 @@ static lag_status comm_setup(lag_ctx_s* ctx) {
         std::vector<int64_t> send_off, send_by_off(kMaxOff, 0);
         std::vector<int> rbox;
         for (const Peer& p : cm->peers) {
-            caps.push_back(p.cap_recv);
+            caps.push_back(p.cap_send);
             const Box& sb = cm->send_boxes[(size_t)p.send_box];
             send_off.push_back(sb.off);
             send_by_off[p.off] = sb.off;
@@ -470,19 +469,11 @@ static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity);
 lag_status lag_comm_reset(lag_ctx_s* ctx) {
     Comm* cm = ctx->comm;
     local_unrecord(ctx);
-    if (cm->peer && cm->pending) {
-        // peer transports, reseed in the middle of an interval: the last
-        // cycle's hand-offs are being stored into my inbox by the neighbours'
-        // advect kernels; wait for their "particles(seq)" signal and drop them
-        // (zero the inbox headers) so the next interval does not append them
-        const unsigned long long seq = lag_peer_seq(cm->peer);
-        AppendArgs ap = append_args(ctx, (int)(seq & 1));
-        ap.discard = 1;
-        lag_status st = lag_peer_exchange(ctx, cm->peer, cm->d_send_boxes, (int)cm->peers.size(), 0,
-                                          nullptr, nullptr, false, false, cm->poff, cm->pback, seq, &ap);
-        if (st != LAG_OK) return st;
-    }
-    // empty outgoing slots; nothing pending (seed_kernel sets W_NTILES)
+    // peer transports, reseed in the middle of an interval: the last cycle's
+    // hand-offs stay in the senders' own slots and are never read (the next
+    // exchange appends only while an interval is pending on this rank, and
+    // lag_seed is collective); each slot is reset before it is written again.
+    // Empty outgoing slots (NCCL); nothing pending (seed_kernel sets W_NTILES)
     CKC(cudaMemsetAsync(cm->slots, 0, sizeof(float4) * std::max<int64_t>(1, cm->slot_total), ctx->stream));
     cm->pending = false;
     cm->n_returned = 0;
@@ -497,6 +488,9 @@ static lag_status launch_append(lag_ctx_s* ctx, int peer_parity = -1) {
     return LAG_OK;
 }
 
+// peer_parity >= 0: the neighbours' own slots of that parity (peer
+// transports, read remotely; the senders reset them); otherwise the slots
+// NCCL delivered, and my sent slots are reset
 static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity) {
     Comm* cm = ctx->comm;
     AppendArgs a{};
@@ -504,11 +498,12 @@ static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity) {
     a.counters = ctx->counters; a.cap_tiles = ctx->cap_tiles;
     a.npeers = (int)cm->peers.size();
     for (size_t i = 0; i < cm->peers.size(); ++i) {
-        a.recv[i] = peer_parity >= 0 ? lag_peer_inbox_slot(cm->peer, peer_parity, cm->peers[i].off)
-                                     : cm->peers[i].recv_slot;
-        a.cap[i] = cm->peers[i].cap_recv;
+        const Peer& p = cm->peers[i];
+        a.recv[i] = peer_parity >= 0 ? lag_peer_remote_slot(cm->peer, (int)i, p.rank, p.back, peer_parity)
+                                     : p.recv_slot;
+        a.cap[i] = p.cap_recv;
     }
-    a.zero_recv = peer_parity >= 0 ? 1 : 0;
+    a.reset = peer_parity >= 0 ? RESET_NONE : RESET_SLOTS;
     a.slots = cm->slots;
     a.noff = kMaxOff;                               // all 27 offset headers (2-D uses 9..17)
     for (int k = 0; k < kMaxOff; ++k) a.slot_base[k] = cm->slot_base[k];
@@ -575,9 +570,10 @@ static lag_status exchange(lag_ctx_s* ctx, float* v0, float* v1, bool halo, bool
 static lag_status peer_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool with_v0) {
     Comm* cm = ctx->comm;
     const unsigned long long seq = ++lag_peer_seq(cm->peer);
-    const AppendArgs ap = append_args(ctx, (int)((seq & 1) ^ 1));   // hand-offs of cycle seq-1
+    // hand-offs of cycle seq-1, unless this is the first cycle of an interval
+    const AppendArgs ap = append_args(ctx, (int)((seq - 1) % 3));
     return lag_peer_exchange(ctx, cm->peer, cm->d_send_boxes, (int)cm->peers.size(), cm->halo_send_floats,
-                             v0, v1, with_v0, true, cm->poff, cm->pback, seq - 1, &ap);
+                             v0, v1, with_v0, true, cm->poff, cm->pback, cm->pending ? &ap : nullptr);
 }
 
 bool lag_comm_overlap(lag_ctx_s* ctx) {
@@ -602,23 +598,16 @@ void lag_comm_fill_args(lag_ctx_s* ctx, AdvectArgs* a) {
         a->slot_capv[k] = cm->slot_capv[k];
         a->slot_ptr[k] = cm->slots + cm->slot_base[k];
     }
-    a->n_sig = 0;
-    if (cm->peer) {
+    if (cm->peer) {                  // my own slots of this cycle's parity (read by the neighbours)
         const unsigned long long seq = lag_peer_seq(cm->peer);
-        const int q = (int)(seq & 1);
-        for (size_t i = 0; i < cm->peers.size(); ++i) {
-            a->slot_ptr[cm->peers[i].off] = lag_peer_remote_slot(cm->peer, (int)i, cm->peers[i].rank, cm->peers[i].back, q);
-            a->sig_flag[i] = lag_peer_remote_flag(cm->peer, (int)i, 1, cm->peers[i].back);
-        }
-        a->n_sig = (int)cm->peers.size();
-        a->sig_value = seq;
-        a->done_warps = lag_peer_done_counter(cm->peer);
+        for (size_t i = 0; i < cm->peers.size(); ++i)
+            a->slot_ptr[cm->peers[i].off] = lag_peer_my_slot(cm->peer, (int)(seq % 3), cm->peers[i].off);
     }
 }
 
 lag_status lag_comm_post_advect(lag_ctx_s* ctx) {
     Comm* cm = ctx->comm;
-    cm->pending = !cm->peers.empty();       // peer transport: signalled by the advect kernel
+    cm->pending = !cm->peers.empty();       // this cycle's hand-offs wait in the slots
     return LAG_OK;
 }
 
@@ -633,9 +622,9 @@ lag_status lag_comm_return_to_origin(lag_ctx_s* ctx) {
         lag_status st;
         if (cm->peer) {
             const unsigned long long seq = lag_peer_seq(cm->peer);
-            const AppendArgs ap = append_args(ctx, (int)(seq & 1));
+            const AppendArgs ap = append_args(ctx, (int)(seq % 3));
             st = lag_peer_exchange(ctx, cm->peer, cm->d_send_boxes, (int)cm->peers.size(), 0,
-                                   nullptr, nullptr, false, false, cm->poff, cm->pback, seq, &ap);
+                                   nullptr, nullptr, false, false, cm->poff, cm->pback, &ap);
         } else {
             st = exchange(ctx, nullptr, nullptr, false, false);
         }
@@ -829,7 +818,7 @@ static AppendArgs local_append_args(lag_ctx_s* ctx) {
         a.recv[i] = pc->slots + pc->slot_base[p.back];
         a.cap[i] = (uint32_t)pc->slot_capv[p.back];
     }
-    a.zero_recv = 1;                                    // each slot has exactly one reader: me
+    a.reset = RESET_RECV;                               // each slot has exactly one reader: me
     a.noff = 0;
     return a;
 }

@@ -62,13 +62,7 @@ struct AdvectArgs {
     float4* slot_rec;
     int32_t slot_base[27];
     int32_t slot_capv[27];
-    float4* slot_ptr[27];           // slot of offset k: local (NCCL) or the owner's inbox (peer/local)
-    // peer transport: the last warp to retire signals "particles of cycle
-    // sig_value ready" into each neighbour's flag word
-    unsigned long long* sig_flag[26];
-    int32_t n_sig;
-    unsigned long long sig_value;
-    uint32_t* done_warps;
+    float4* slot_ptr[27];           // slot of offset k: local (NCCL, peer) or the owner's inbox (LOCAL)
     // COMM exchange overlap (LAG_XCHG_PEER_OVERLAP): pass 1 advects tiles
     // [0, *n_tiles_b) whose stage samples cannot reach a ghost node and defers
     // the others; pass 2 advects the deferred tiles and the tiles appended by
@@ -328,7 +322,7 @@ template <int DIM, bool BTO>
 __device__ __forceinline__ int tile_slow(const AdvectArgs& a, float4* trec, int lane, bool live, bool inblk,
                                       const int g[3], const float4 r, const float dn[3], uint8_t st,
                                       bool ghost_bad, uint32_t& errbits, uint32_t& nterm,
-                                      uint32_t& nexit, uint32_t& nsent, bool& did_remote) {
+                                      uint32_t& nexit, uint32_t& nsent) {
     bool migrate = false;
     int nb = 0;
     if (live && st == ST_VALID) {
@@ -395,7 +389,6 @@ __device__ __forceinline__ int tile_slow(const AdvectArgs& a, float4* trec, int 
                 sb[1 + pos] = make_float4(dn[0], dn[1], dn[2], r.w);
             else
                 errbits |= ERR_OVERFLOW;
-            did_remote = true;
         }
         if (lane == 0) nsent += __popc(mmask);
     }
@@ -459,7 +452,6 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
 
     uint32_t steps = 0, nterm = 0, nexit = 0, nsent = 0;  // per warp and launch: < 2^32
     uint32_t errbits = 0;
-    bool did_remote = false;
 
     // software pipeline: the next tile's count and record are in flight while
     // the current tile computes
@@ -590,7 +582,7 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
             if (live) trec[lane] = make_float4(dn[0], dn[1], dn[2], r.w);
         } else {
             const int kept = tile_slow<DIM, BTO>(a, trec, lane, live, inblk, g, r, dn, st, ghost_bad, errbits,
-                                                 nterm, nexit, nsent, did_remote);
+                                                 nterm, nexit, nsent);
             if (lane == 0) a.tile_count[rtile] = (uint8_t)kept;
         }
         steps += (uint32_t)cnt;
@@ -606,22 +598,6 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
     }
     errbits = __reduce_or_sync(0xffffffffu, errbits);
     if (lane == 0 && errbits) atomicOr(a.err, errbits);
-    if constexpr (!BTO) {
-        if (a.n_sig) {
-            if (__any_sync(0xffffffffu, did_remote)) __threadfence_system();   // my remote hand-offs are performed
-            __syncwarp();
-            if (lane == 0) {
-                const uint32_t total = (ncta * kThreads) >> 5;
-                if (atomicAdd(a.done_warps, 1u) == total - 1) {  // last warp of the grid
-                    *a.done_warps = 0u;
-                    __threadfence_system();
-                    for (int k = 0; k < a.n_sig; ++k)
-                        *reinterpret_cast<volatile unsigned long long*>(a.sig_flag[k]) = a.sig_value;
-                    __threadfence_system();
-                }
-            }
-        }
-    }
 }
 
 template <int DIM, bool BTO, bool FROZEN, bool PASSES = false>

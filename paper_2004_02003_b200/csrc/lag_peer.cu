@@ -5,19 +5,29 @@
 // Every rank owns one CUDA-IPC allocation, mapped by its neighbours:
 //   flags  [2][27] u64  — "halo ready" / "particles ready" sequence numbers,
 //                         one word per sending neighbour (its offset index)
-//   inbox  [2 parities][sum over peers of (1 + cap) float4] — particle slots
-//                         the neighbours' advect kernels fill with remote stores
+//   pslot  [3 parities][sum over peers of (1 + cap) float4] — my outgoing
+//                         particle slots (header + records), one per
+//                         neighbour, filled by my advect kernel with local
+//                         atomics and stores, read by the neighbour
 //   outbox [2 parities][2 slices][halo floats] — my packed ghost sources, read
 //                         by the neighbours with remote loads
-// Per cycle (seq = 1, 2, ...; parity q = seq & 1):
+// Per cycle (seq = 1, 2, ...; ghost parity q = seq & 1, slot parity seq % 3):
 //   pack my faces -> outbox[q]; signal halo(seq) to each neighbour;
-//   wait until every neighbour signalled halo >= seq and particles >= seq-1
-//   (bounded spin, latched error on timeout); ghost layers <- neighbours'
-//   outbox[q] (remote loads); append inbox[q^1] (previous cycle's hand-offs);
-//   advect writes leaving particles into the owner's inbox[q] (remote atomics
-//   + stores); signal particles(seq).
-// Two parities suffice: a neighbour reuses parity q at seq+2 only after it
-// waited for my halo(seq+1), which I signal after consuming parity q.
+//   wait until every neighbour signalled halo >= seq (bounded spin, latched
+//   error on timeout) — its exchange(seq) runs after its advect(seq-1), so
+//   the flag also says that advect's hand-offs are written; reset my
+//   pslot[(seq+1) % 3] headers; ghost layers <- neighbours' outbox[q] and
+//   hand-offs <- neighbours' pslot[(seq-1) % 3] toward me (remote loads);
+//   advect writes leaving particles into my pslot[seq % 3].
+// Three slot parities: the advect of cycle seq writes parity seq % 3 while
+// (overlap transport) the exchange of the same cycle reads the neighbours'
+// parity (seq-1) % 3 and resets mine of parity (seq+1) % 3, last read by the
+// neighbour in its exchange(seq-1), which ended before it signalled halo(seq).
+// Two ghost parities suffice: a neighbour reuses outbox parity q at seq+2
+// only after it waited for my halo(seq+1), which I signal after pulling.
+// Write cycle: the flush kernel signals particles(seq), waits for the
+// neighbours' particles(seq) and appends their pslot[seq % 3]; the first
+// exchange of the next interval appends nothing.
 #include "lag_internal.h"
 #include "lag_append.cuh"
 #include "lag_xchg.cuh"
@@ -55,8 +65,9 @@ using namespace lag;
 namespace lag {
 
 // per-rank layout table published to every rank (int64 words)
-enum : int { T_INBOX = 0, T_INBOX_PAR = 1, T_OUTBOX = 2, T_HALO = 3, T_RECV = 4, T_SEND = 4 + kOff,
+enum : int { T_PSLOT = 0, T_PSLOT_PAR = 1, T_OUTBOX = 2, T_HALO = 3, T_SLOT = 4, T_SEND = 4 + kOff,
              T_WORDS = 4 + 2 * kOff };
+constexpr int kSlotParities = 3;
 
 // pack + signal, then wait + pull + append, in one launch: every CTA must be
 // resident (a CTA waiting for the neighbours' signal must not keep one of
@@ -81,7 +92,7 @@ struct PeerState {
     std::vector<char*> remote;                // per peer: mapped neighbour allocation
     std::vector<int64_t> table;               // nranks * T_WORDS
     unsigned long long* flags = nullptr;      // mine
-    float4* inbox[2] = {nullptr, nullptr};
+    float4* pslot[kSlotParities] = {nullptr, nullptr, nullptr};
     float* outbox = nullptr;                  // [2][2][halo]
     std::vector<lag::PeerBox> boxes;          // v1 boxes then v0 boxes
     lag::PeerBox* d_boxes = nullptr;
@@ -89,13 +100,12 @@ struct PeerState {
     int64_t halo_send_floats = 0;
     std::vector<int64_t> my_table;            // my own layout words
     unsigned long long seq = 0;
-    uint32_t* done_warps = nullptr;           // advect completion counter
-    uint32_t* done_ctas = nullptr;            // pack-kernel completion counter
+    uint32_t* done_ctas = nullptr;            // pack completion counter
 };
 
 lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>& prank,
                          const std::vector<int>& poff, const std::vector<int>& pback,
-                         const std::vector<uint32_t>& cap_recv, int64_t halo_send_floats,
+                         const std::vector<uint32_t>& cap_send, int64_t halo_send_floats,
                          const std::vector<int64_t>& send_box_off, const std::vector<int64_t>& send_box_by_off,
                          const std::vector<int>& recv_box_x0y0z0nxnynz, int64_t halo_recv_floats,
                          PeerState** out) {
@@ -103,33 +113,31 @@ lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>
     PeerState* ps = new PeerState();
     const int R = ctx->cfg.nranks;
     const int np = (int)prank.size();
-    // my layout: flags | inbox[2] | outbox[2][2]
-    int64_t inbox_f4 = 0;
-    std::vector<int64_t> recv_off(kOff, -1);
-    for (int i = 0; i < np; ++i) { recv_off[pback[i] >= 0 ? poff[i] : 0] = inbox_f4; inbox_f4 += cap_recv[i] + 1; }
-    const size_t flags_bytes = 2 * kOff * sizeof(unsigned long long);
-    const size_t inbox_off = 512;                       // after the 2 x 27 u64 flags (432 B)
-    static_assert(2 * kOff * sizeof(unsigned long long) <= 512, "flags overlap the inbox");
-    const size_t inbox_bytes = (size_t)std::max<int64_t>(1, inbox_f4) * sizeof(float4);
-    const size_t outbox_off = inbox_off + 2 * inbox_bytes;
+    // my layout: flags | pslot[3] | outbox[2][2]
+    int64_t slot_f4 = 0;
+    std::vector<int64_t> slot_off(kOff, -1);            // my slot toward the neighbour at offset k
+    for (int i = 0; i < np; ++i) { slot_off[poff[i]] = slot_f4; slot_f4 += cap_send[i] + 1; }
+    const size_t pslot_off = 512;                       // after the 2 x 27 u64 flags (432 B)
+    static_assert(2 * kOff * sizeof(unsigned long long) <= 512, "flags overlap the slots");
+    const size_t pslot_bytes = (size_t)std::max<int64_t>(1, slot_f4) * sizeof(float4);
+    const size_t outbox_off = pslot_off + kSlotParities * pslot_bytes;
     const size_t outbox_bytes = (size_t)std::max<int64_t>(1, halo_send_floats) * sizeof(float);
     ps->bytes = outbox_off + 4 * outbox_bytes;
-    (void)flags_bytes;
     CKC(cudaMalloc(&ps->mem, ps->bytes));
     CKC(cudaMemset(ps->mem, 0, ps->bytes));
     ps->flags = reinterpret_cast<unsigned long long*>(ps->mem);
-    ps->inbox[0] = reinterpret_cast<float4*>(ps->mem + inbox_off);
-    ps->inbox[1] = reinterpret_cast<float4*>(ps->mem + inbox_off + inbox_bytes);
+    for (int q = 0; q < kSlotParities; ++q)
+        ps->pslot[q] = reinterpret_cast<float4*>(ps->mem + pslot_off + q * pslot_bytes);
     ps->outbox = reinterpret_cast<float*>(ps->mem + outbox_off);
     ps->halo_recv_floats = halo_recv_floats;
     ps->halo_send_floats = std::max<int64_t>(1, halo_send_floats);
     // publish layout + IPC handle
     std::vector<int64_t> mine(T_WORDS, -1);
-    mine[T_INBOX] = (int64_t)inbox_off;
-    mine[T_INBOX_PAR] = (int64_t)inbox_bytes;
+    mine[T_PSLOT] = (int64_t)pslot_off;
+    mine[T_PSLOT_PAR] = (int64_t)pslot_bytes;
     mine[T_OUTBOX] = (int64_t)outbox_off;
     mine[T_HALO] = halo_send_floats;
-    for (int k = 0; k < kOff; ++k) { mine[T_RECV + k] = recv_off[k]; mine[T_SEND + k] = send_box_by_off[k]; }
+    for (int k = 0; k < kOff; ++k) { mine[T_SLOT + k] = slot_off[k]; mine[T_SEND + k] = send_box_by_off[k]; }
     ps->my_table = mine;
     cudaIpcMemHandle_t h;
     CKC(cudaIpcGetMemHandle(&h, ps->mem));
@@ -175,9 +183,8 @@ lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>
             ps->boxes.push_back(b);
         }
     }
-    CKC(cudaMalloc(&ps->done_warps, 2 * sizeof(uint32_t)));
-    CKC(cudaMemset(ps->done_warps, 0, 2 * sizeof(uint32_t)));
-    ps->done_ctas = ps->done_warps + 1;
+    CKC(cudaMalloc(&ps->done_ctas, sizeof(uint32_t)));
+    CKC(cudaMemset(ps->done_ctas, 0, sizeof(uint32_t)));
     CKC(cudaMalloc(&ps->d_boxes, sizeof(PeerBox) * std::max<size_t>(1, ps->boxes.size())));
     if (!ps->boxes.empty())
         CKC(cudaMemcpy(ps->d_boxes, ps->boxes.data(), sizeof(PeerBox) * ps->boxes.size(), cudaMemcpyHostToDevice));
@@ -190,40 +197,39 @@ void lag_peer_destroy(PeerState* ps) {
     if (!ps) return;
     for (char* p : ps->remote) if (p) cudaIpcCloseMemHandle(p);
     cudaFree(ps->d_boxes);
-    cudaFree(ps->done_warps);
+    cudaFree(ps->done_ctas);
     cudaFree(ps->mem);
     delete ps;
 }
 
-// remote inbox slot (parity q) that I (sending toward peer i) fill
-float4* lag_peer_remote_slot(PeerState* ps, int i, int prank, int pback, int q) {
-    const int64_t* t = &ps->table[(size_t)prank * T_WORDS];
-    return reinterpret_cast<float4*>(ps->remote[i] + t[T_INBOX] + (size_t)q * t[T_INBOX_PAR]) + t[T_RECV + pback];
+// my outgoing slot (parity q) toward the neighbour at offset index poff
+float4* lag_peer_my_slot(PeerState* ps, int q, int poff) {
+    return ps->pslot[q % kSlotParities] + ps->my_table[T_SLOT + poff];
 }
 
-float4* lag_peer_inbox_slot(PeerState* ps, int q, int poff) {
-    // my inbox slot (parity q) filled by the neighbour at offset index poff
-    const int64_t* t = ps->my_table.data();
-    return ps->inbox[q] + t[T_RECV + poff];
+// neighbour i's outgoing slot (parity q) toward me (my offset index at it = pback)
+float4* lag_peer_remote_slot(PeerState* ps, int i, int prank, int pback, int q) {
+    const int64_t* t = &ps->table[(size_t)prank * T_WORDS];
+    return reinterpret_cast<float4*>(ps->remote[i] + t[T_PSLOT] + (size_t)(q % kSlotParities) * t[T_PSLOT_PAR]) +
+           t[T_SLOT + pback];
 }
 
 float* lag_peer_outbox(PeerState* ps, int q) { return ps->outbox + (size_t)q * 2 * ps->halo_send_floats; }
 
 unsigned long long& lag_peer_seq(PeerState* ps) { return ps->seq; }
 
-uint32_t* lag_peer_done_counter(PeerState* ps) { return ps->done_warps; }
-
 unsigned long long* lag_peer_remote_flag(PeerState* ps, int i, int kind, int pback) {
     return reinterpret_cast<unsigned long long*>(ps->remote[i]) + kind * kOff + pback;
 }
 
-// The fused exchange (see peer_exchange_kernel).  pack/halo: this cycle's
-// ghost exchange; need_part: hand-offs to wait for; append_parity: inbox
-// parity to append (-1: none).
+// The fused exchange (see peer_exchange_kernel).  halo: this cycle's ghost
+// exchange (seq = the cycle, already incremented); otherwise the write-cycle
+// flush of cycle seq's hand-offs (signal particles(seq), wait for the
+// neighbours' signal).  append_args: the neighbours' slots to append, or null.
 lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_boxes, int nsend,
                              int64_t sfl, float* v0, float* v1, bool with_v0, bool halo,
                              const std::vector<int>& poff, const std::vector<int>& pback,
-                             unsigned long long need_part, const void* append_args) {
+                             const void* append_args) {
     const int np = (int)poff.size();
     cudaStream_t st = ctx->stream;
     XchgArgs x{};
@@ -242,7 +248,15 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
     }
     x.my_flags = ps->flags;
     x.need_halo = halo ? seq : 0;
-    x.need_part = need_part;
+    x.need_part = halo ? 0 : seq;
+    if (halo) {                                // my slots the advect fills next cycle
+        x.nzero = np;
+        for (int i = 0; i < np; ++i)
+            x.zero_slot[i] = reinterpret_cast<uint32_t*>(lag_peer_my_slot(ps, (int)((seq + 1) % kSlotParities), poff[i]));
+    } else {
+        x.signal_part = 1;
+        for (int i = 0; i < np; ++i) x.part_flag[i] = lag_peer_remote_flag(ps, i, 1, pback[i]);
+    }
     x.timeout_cycles = 8000000000LL;
     x.err = ctx->words + W_ERR;
     x.recv_boxes = ps->d_boxes;

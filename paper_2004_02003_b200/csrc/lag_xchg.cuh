@@ -18,14 +18,15 @@ struct PeerBox {            // one ghost box to fill from a remote outbox
     int slice;
 };
 
-// Per-cycle exchange (the advect kernel signals the hand-offs itself):
+// Per-cycle exchange (the hand-offs wait in the senders' own slots):
 //   A: pack my ghost sources (grid-stride); the last CTA to finish fences and
 //      signals halo(seq) to every neighbour;
 //   B: the first `npull` CTAs wait (bounded) for all neighbours' halo(seq)
-//      and particles(seq-1), pull their share of the ghost layers with remote
-//      loads and append the previous cycle's hand-offs.  Few waiters: a few
-//      hundred CTAs polling one flag word queue up its L2 slice and delay the
-//      neighbour's remote store to it by several microseconds.
+//      (which implies their hand-offs of cycle seq-1 are written: stream
+//      order), pull their share of the ghost layers and of those hand-offs
+//      with remote loads and append them.  Few waiters: a few hundred CTAs
+//      polling one flag word queue up its L2 slice and delay the neighbour's
+//      remote store to it by several microseconds.
 struct XchgArgs {
     float* v0;
     float* v1;
@@ -49,6 +50,14 @@ struct XchgArgs {
     int sx, sxy, dim;
     unsigned long long seq;
     int do_append;
+    // my outgoing particle slots the advect kernel fills next cycle: reset
+    // once every neighbour has signalled this cycle (it has read them)
+    uint32_t* zero_slot[kMaxPeers];
+    int nzero;
+    // write cycle: signal "particles(seq) ready" to every neighbour first
+    // (halo(seq+1) implies it on the per-cycle path)
+    unsigned long long* part_flag[kMaxPeers];
+    int signal_part;
 };
 
 __device__ __forceinline__ void xchg_pack_signal(const XchgArgs& x, int cta, int ncta) {
@@ -80,6 +89,10 @@ __device__ __forceinline__ void xchg_pack_signal(const XchgArgs& x, int cta, int
 }
 
 __device__ __forceinline__ void xchg_wait_pull(const XchgArgs& x, const AppendArgs& ap, int cta, int ncta) {
+    if (x.signal_part && cta == 0 && threadIdx.x == 0) {
+        __threadfence_system();                       // releases the previous kernels' slot writes
+        for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(x.part_flag[p]) = x.seq;
+    }
     if (threadIdx.x < x.npeers) {
         const volatile unsigned long long* fh = x.my_flags + 0 * kOff + x.back[threadIdx.x];
         const volatile unsigned long long* fp = x.my_flags + 1 * kOff + x.back[threadIdx.x];
@@ -91,6 +104,7 @@ __device__ __forceinline__ void xchg_wait_pull(const XchgArgs& x, const AppendAr
         __threadfence_system();
     }
     __syncthreads();
+    if (cta == 0 && threadIdx.x < x.nzero) *x.zero_slot[threadIdx.x] = 0u;
     // remote loads: 8 in flight per thread (a few CTAs cover the ghost layers
     // when they run inside the advect kernel's pass 1)
     const int64_t step = (int64_t)ncta * blockDim.x;
