@@ -496,24 +496,26 @@ static lag_status advect_enqueue(lag_ctx_s* ctx, float* d0, float* d1, double dt
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
     const bool bto = ctx->cfg.mode == LAG_BTO;
-    auto launch = [&](const AdvectArgs& aa, int nb) {
+    // programmatic dependent launch: the CTAs are scheduled while the
+    // previous kernel (e.g. the peer exchange) drains and wait in
+    // griddep_wait() for its end, so the launch latency overlaps it
+    cudaLaunchAttribute pdl{};
+    pdl.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl.val.programmaticStreamSerializationAllowed = 1;
+    auto launch = [&](const AdvectArgs& aa, int nb) -> cudaError_t {
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(nb); lc.blockDim = dim3(kThreads); lc.dynamicSmemBytes = 0; lc.stream = ctx->stream;
+        lc.attrs = &pdl; lc.numAttrs = 1;
         if (D == 3) {
-            if (aa.frozen) {
-                if (bto) advect_kernel<3, true, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
-                else advect_kernel<3, false, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
-            } else {
-                if (bto) advect_kernel<3, true, false><<<nb, kThreads, 0, ctx->stream>>>(aa);
-                else advect_kernel<3, false, false><<<nb, kThreads, 0, ctx->stream>>>(aa);
-            }
-        } else {
-            if (aa.frozen) {
-                if (bto) advect_kernel<2, true, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
-                else advect_kernel<2, false, true><<<nb, kThreads, 0, ctx->stream>>>(aa);
-            } else {
-                if (bto) advect_kernel<2, true, false><<<nb, kThreads, 0, ctx->stream>>>(aa);
-                else advect_kernel<2, false, false><<<nb, kThreads, 0, ctx->stream>>>(aa);
-            }
+            if (aa.frozen) return bto ? cudaLaunchKernelEx(&lc, advect_kernel<3, true, true>, aa)
+                                      : cudaLaunchKernelEx(&lc, advect_kernel<3, false, true>, aa);
+            return bto ? cudaLaunchKernelEx(&lc, advect_kernel<3, true, false>, aa)
+                       : cudaLaunchKernelEx(&lc, advect_kernel<3, false, false>, aa);
         }
+        if (aa.frozen) return bto ? cudaLaunchKernelEx(&lc, advect_kernel<2, true, true>, aa)
+                                  : cudaLaunchKernelEx(&lc, advect_kernel<2, false, true>, aa);
+        return bto ? cudaLaunchKernelEx(&lc, advect_kernel<2, true, false>, aa)
+                   : cudaLaunchKernelEx(&lc, advect_kernel<2, false, false>, aa);
     };
     if (overlap) {
         // pass 1: exchange CTAs + ghost-free tiles; pass 2 (stream-ordered after
@@ -541,7 +543,7 @@ static lag_status advect_enqueue(lag_ctx_s* ctx, float* d0, float* d1, double dt
             else advect_kernel<2, false, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a2);
         }
     } else {
-        launch(a, blocks);
+        CK(launch(a, blocks));
     }
     ++ctx->launches;
     CK(cudaGetLastError());
@@ -557,6 +559,8 @@ static lag_status advect_enqueue(lag_ctx_s* ctx, float* d0, float* d1, double dt
             ctx->stage_use[k] = ctx->cycles_total;
         }
     ctx->last_v1_slot = s1;
+    ctx->prev_d0 = d0;
+    ctx->prev_d1 = d1;
     ++ctx->cycles_in_interval;
     ++ctx->cycles_total;
     return LAG_OK;

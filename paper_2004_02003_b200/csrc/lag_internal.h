@@ -63,6 +63,8 @@ struct lag_ctx_s {
     cudaStream_t cstream = nullptr;
     int last_v1_slot = -1;                        // buffer holding the previous call's host v_t1
     const void* last_v1 = nullptr;
+    const float* prev_d0 = nullptr;            // device slices the last advect kernel read
+    const float* prev_d1 = nullptr;
     // COMM
     lag::Comm* comm = nullptr;
     lag::LocalGroup* group = nullptr;          // LAG_XCHG_LOCAL

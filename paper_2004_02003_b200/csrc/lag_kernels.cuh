@@ -74,6 +74,15 @@ struct AdvectArgs {
     int32_t smin[3], sspan[3];      // ghost-free cells (gather offsets): samples stay off ghost nodes
 };
 
+// Programmatic dependent launch (kernels launched with the
+// programmatic-stream-serialization attribute, lag_api.cu / lag_peer.cu):
+// the next kernel in the stream may be scheduled once every CTA of this one
+// has called griddep_launch(); griddep_wait() blocks until the previous
+// kernel has completed and its memory is visible (a no-op when the kernel
+// was launched without the attribute or after a non-kernel stream item).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // floor(e) on the FMA pipe (no FRND): for |e| < 2^22, e + 1.5*2^23 rounded
 // toward -inf is 1.5*2^23 + floor(e) exactly, so its bits hold floor(e) in
 // the low mantissa (bits - 0x4B400000 = floor(e)) and t - 1.5*2^23 is floor(e).
@@ -603,6 +612,14 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
 template <int DIM, bool BTO, bool FROZEN, bool PASSES = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 advect_kernel(const AdvectArgs a) {
+    // wait for the previous kernel (the exchange that appended to the lists),
+    // then let the next one be scheduled: it takes the SMs this persistent
+    // grid leaves in its tail.  Triggering only after the wait keeps every
+    // kernel after the one two places before it (the next exchange must not
+    // pack into the outbox parity the neighbour may still be pulling until
+    // this cycle's exchange has seen the neighbour's signal).
+    griddep_wait();
+    griddep_launch();
     advect_body<DIM, BTO, FROZEN, PASSES>(a, blockIdx.x, gridDim.x);
 }
 

@@ -74,6 +74,7 @@ constexpr int kSlotParities = 3;
 // ours that has not packed from running), so the grid is capped at the
 // resident capacity
 __global__ void __launch_bounds__(256) peer_exchange_kernel(XchgArgs x, AppendArgs ap, int npull) {
+    griddep_launch();                 // the advect kernel may be scheduled (it waits for this grid)
     xchg_pack_signal(x, blockIdx.x, gridDim.x);
     if ((int)blockIdx.x < npull) xchg_wait_pull(x, ap, blockIdx.x, npull);
 }
@@ -267,6 +268,8 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
     x.sx = ctx->sx; x.sxy = ctx->sxy; x.dim = ctx->cfg.dim;
     x.seq = seq;
     x.do_append = append_args ? 1 : 0;
+    for (const float* w : {halo ? v1 : nullptr, (halo && with_v0) ? v0 : nullptr})
+        if (w && (w == ctx->prev_d0 || w == ctx->prev_d1)) x.pull_wait = 1;
     x.done_ctas = ps->done_ctas;
     AppendArgs ap{};
     if (append_args) ap = *reinterpret_cast<const AppendArgs*>(append_args);
@@ -282,7 +285,13 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, cap));
         // waiters: enough for one round of remote loads (8 in flight per thread)
         const int npull = (int)std::max<int64_t>(std::min<int64_t>(8, g), std::min<int64_t>((x.rtotal + 2047) / 2048, g));
-        peer_exchange_kernel<<<g, 256, 0, st>>>(x, ap, npull);
+        cudaLaunchAttribute attr{};
+        attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr.val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(g); lc.blockDim = dim3(256); lc.dynamicSmemBytes = 0; lc.stream = st;
+        lc.attrs = &attr; lc.numAttrs = 1;
+        CKC(cudaLaunchKernelEx(&lc, peer_exchange_kernel, x, ap, npull));
     } else {
         const int gb = (int)std::max<int64_t>(1, std::min<int64_t>((x.rtotal + 255) / 256, cap));
         peer_wait_pull_kernel<<<gb, 256, 0, st>>>(x, ap);

@@ -20,7 +20,10 @@ struct PeerBox {            // one ghost box to fill from a remote outbox
 
 // Per-cycle exchange (the hand-offs wait in the senders' own slots):
 //   A: pack my ghost sources (grid-stride); the last CTA to finish fences and
-//      signals halo(seq) to every neighbour;
+//      signals halo(seq) to every neighbour.  Launched as a programmatic
+//      dependent of the previous advect kernel, the packing and the ghost
+//      pull (inputs: the new slices) overlap that kernel's tail; the signal
+//      and the append wait for its end (griddep_wait);
 //   B: the first `npull` CTAs wait (bounded) for all neighbours' halo(seq)
 //      (which implies their hand-offs of cycle seq-1 are written: stream
 //      order), pull their share of the ghost layers and of those hand-offs
@@ -58,6 +61,9 @@ struct XchgArgs {
     // (halo(seq+1) implies it on the per-cycle path)
     unsigned long long* part_flag[kMaxPeers];
     int signal_part;
+    // a slice the ghost pull writes was read by the previous advect kernel
+    // (the same buffer passed again): pull only after that kernel ended
+    int pull_wait;
 };
 
 __device__ __forceinline__ void xchg_pack_signal(const XchgArgs& x, int cta, int ncta) {
@@ -82,6 +88,7 @@ __device__ __forceinline__ void xchg_pack_signal(const XchgArgs& x, int cta, int
         __threadfence();
         if (atomicAdd(x.done_ctas, 1u) == (uint32_t)ncta - 1) {   // last CTA: halo(seq) ready
             *x.done_ctas = 0u;
+            griddep_wait();                           // and my previous advect's hand-offs (see below)
             __threadfence_system();
             for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(x.halo_flag[p]) = x.seq;
         }
@@ -105,6 +112,7 @@ __device__ __forceinline__ void xchg_wait_pull(const XchgArgs& x, const AppendAr
     }
     __syncthreads();
     if (cta == 0 && threadIdx.x < x.nzero) *x.zero_slot[threadIdx.x] = 0u;
+    if (x.pull_wait) griddep_wait();
     // remote loads: 8 in flight per thread (a few CTAs cover the ghost layers
     // when they run inside the advect kernel's pass 1)
     const int64_t step = (int64_t)ncta * blockDim.x;
@@ -135,6 +143,7 @@ __device__ __forceinline__ void xchg_wait_pull(const XchgArgs& x, const AppendAr
         for (int u = 0; u < 8; ++u)
             if (dst[u]) *dst[u] = val[u];
     }
+    griddep_wait();                                   // the previous advect kernel's particle lists
     if (x.do_append) append_body(ap, cta, ncta);                         // hand-offs of cycle seq-1 (all CTAs)
 }
 
