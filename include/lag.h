@@ -86,7 +86,7 @@ typedef enum {
 typedef enum { LAG_BTO = 0, LAG_COMM = 1 } lag_mode;
 typedef enum {
     LAG_XCHG_NCCL = 0,          /* grouped NCCL send/recv before the advect kernel            */
-    LAG_XCHG_PEER = 1,          /* the kernels read the neighbours' memory (CUDA IPC)         */
+    LAG_XCHG_PEER = 1,          /* the kernels pull ghosts and hand-offs from the neighbours' memory (CUDA IPC) */
     LAG_XCHG_PEER_OVERLAP = 2,  /* LAG_XCHG_PEER fused with the advection: the first CTAs of
                                    the advect kernel run the exchange while the others
                                    advect the tiles whose stage samples cannot reach a ghost
