@@ -32,6 +32,7 @@ struct AppendArgs {
     int32_t slot_base[kMaxOff];
     int noff;
     int reset;                      // headers reset after the append: RESET_* below
+    const unsigned long long* cnt[kMaxOff];   // non-null: the record count of recv[p] (peer transport)
     int discard;                    // drop the records (a reseed in the middle of an interval)
 };
 
@@ -47,7 +48,8 @@ __device__ __forceinline__ void append_body(const AppendArgs& a, int cta, int nc
     // latency, not one per neighbour), then thread 0 takes the prefix sum
     if (threadIdx.x < (unsigned)a.npeers) {
         const int p = threadIdx.x;
-        uint32_t c = *reinterpret_cast<const volatile uint32_t*>(a.recv[p]);
+        uint32_t c = a.cnt[p] ? (uint32_t)*reinterpret_cast<const volatile unsigned long long*>(a.cnt[p])
+                              : *reinterpret_cast<const volatile uint32_t*>(a.recv[p]);
         if (c > a.cap[p]) { c = a.cap[p]; atomicOr(a.words + W_ERR, ERR_OVERFLOW); }
         pre[p + 1] = c;
     }

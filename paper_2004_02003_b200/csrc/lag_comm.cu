@@ -41,6 +41,7 @@ float4* lag_peer_my_slot(PeerState* ps, int q, int poff);
 float* lag_peer_outbox(PeerState* ps, int q);
 unsigned long long& lag_peer_seq(PeerState* ps);
 unsigned long long* lag_peer_remote_flag(PeerState* ps, int i, int kind, int pback);
+const unsigned long long* lag_peer_my_count(PeerState* ps, int par, int poff);
 lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_boxes, int nsend,
                              int64_t sfl, float* v0, float* v1, bool with_v0, bool halo,
                              const std::vector<int>& poff, const std::vector<int>& pback,
@@ -464,7 +465,7 @@ void lag_comm_destroy(lag_ctx_s* ctx) {
 }
 
 static void local_unrecord(lag_ctx_s* ctx);
-static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity);
+static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity, int cnt_parity = 0);
 
 lag_status lag_comm_reset(lag_ctx_s* ctx) {
     Comm* cm = ctx->comm;
@@ -489,9 +490,10 @@ static lag_status launch_append(lag_ctx_s* ctx, int peer_parity = -1) {
 }
 
 // peer_parity >= 0: the neighbours' own slots of that parity (peer
-// transports, read remotely; the senders reset them); otherwise the slots
-// NCCL delivered, and my sent slots are reset
-static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity) {
+// transports, read remotely; the senders reset them), with the counts they
+// published in my count words of parity cnt_parity; otherwise the slots NCCL
+// delivered, and my sent slots are reset
+static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity, int cnt_parity) {
     Comm* cm = ctx->comm;
     AppendArgs a{};
     a.state = ctx->state; a.tile_count = ctx->tile_count; a.words = ctx->words;
@@ -501,6 +503,7 @@ static AppendArgs append_args(lag_ctx_s* ctx, int peer_parity) {
         const Peer& p = cm->peers[i];
         a.recv[i] = peer_parity >= 0 ? lag_peer_remote_slot(cm->peer, (int)i, p.rank, p.back, peer_parity)
                                      : p.recv_slot;
+        a.cnt[i] = peer_parity >= 0 ? lag_peer_my_count(cm->peer, cnt_parity, p.off) : nullptr;
         a.cap[i] = p.cap_recv;
     }
     a.reset = peer_parity >= 0 ? RESET_NONE : RESET_SLOTS;
@@ -571,7 +574,7 @@ static lag_status peer_pre_advect(lag_ctx_s* ctx, float* v0, float* v1, bool wit
     Comm* cm = ctx->comm;
     const unsigned long long seq = ++lag_peer_seq(cm->peer);
     // hand-offs of cycle seq-1, unless this is the first cycle of an interval
-    const AppendArgs ap = append_args(ctx, (int)((seq - 1) % 3));
+    const AppendArgs ap = append_args(ctx, (int)((seq - 1) % 3), (int)(seq & 1));
     return lag_peer_exchange(ctx, cm->peer, cm->d_send_boxes, (int)cm->peers.size(), cm->halo_send_floats,
                              v0, v1, with_v0, true, cm->poff, cm->pback, cm->pending ? &ap : nullptr);
 }
@@ -622,7 +625,7 @@ lag_status lag_comm_return_to_origin(lag_ctx_s* ctx) {
         lag_status st;
         if (cm->peer) {
             const unsigned long long seq = lag_peer_seq(cm->peer);
-            const AppendArgs ap = append_args(ctx, (int)(seq % 3));
+            const AppendArgs ap = append_args(ctx, (int)(seq % 3), (int)((seq + 1) & 1));
             st = lag_peer_exchange(ctx, cm->peer, cm->d_send_boxes, (int)cm->peers.size(), 0,
                                    nullptr, nullptr, false, false, cm->poff, cm->pback, &ap);
         } else {

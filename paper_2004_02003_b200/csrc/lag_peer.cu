@@ -3,8 +3,9 @@
 // the kernels themselves, with no NCCL call on the per-cycle path.
 //
 // Every rank owns one CUDA-IPC allocation, mapped by its neighbours:
-//   flags  [2][27] u64  — "halo ready" / "particles ready" sequence numbers,
-//                         one word per sending neighbour (its offset index)
+//   flags  [4][27] u64  — "halo ready" / "particles ready" sequence numbers
+//                         and the hand-off counts of two parities, one word
+//                         per sending neighbour (its offset index)
 //   pslot  [3 parities][sum over peers of (1 + cap) float4] — my outgoing
 //                         particle slots (header + records), one per
 //                         neighbour, filled by my advect kernel with local
@@ -68,6 +69,9 @@ namespace lag {
 enum : int { T_PSLOT = 0, T_PSLOT_PAR = 1, T_OUTBOX = 2, T_HALO = 3, T_SLOT = 4, T_SEND = 4 + kOff,
              T_WORDS = 4 + 2 * kOff };
 constexpr int kSlotParities = 3;
+// flag words, one per sending neighbour (its offset index): halo(seq),
+// particles(seq) (write cycle), hand-off counts (two parities: seq & 1)
+enum : int { F_HALO = 0, F_PART = 1, F_CNT = 2, kFlagKinds = 4 };
 
 // pack + signal, then wait + pull + append, in one launch: every CTA must be
 // resident (a CTA waiting for the neighbours' signal must not keep one of
@@ -118,8 +122,8 @@ lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>
     int64_t slot_f4 = 0;
     std::vector<int64_t> slot_off(kOff, -1);            // my slot toward the neighbour at offset k
     for (int i = 0; i < np; ++i) { slot_off[poff[i]] = slot_f4; slot_f4 += cap_send[i] + 1; }
-    const size_t pslot_off = 512;                       // after the 2 x 27 u64 flags (432 B)
-    static_assert(2 * kOff * sizeof(unsigned long long) <= 512, "flags overlap the slots");
+    const size_t pslot_off = 1024;                      // after the 4 x 27 u64 flag words (864 B)
+    static_assert(kFlagKinds * kOff * sizeof(unsigned long long) <= 1024, "flags overlap the slots");
     const size_t pslot_bytes = (size_t)std::max<int64_t>(1, slot_f4) * sizeof(float4);
     const size_t outbox_off = pslot_off + kSlotParities * pslot_bytes;
     const size_t outbox_bytes = (size_t)std::max<int64_t>(1, halo_send_floats) * sizeof(float);
@@ -223,6 +227,11 @@ unsigned long long* lag_peer_remote_flag(PeerState* ps, int i, int kind, int pba
     return reinterpret_cast<unsigned long long*>(ps->remote[i]) + kind * kOff + pback;
 }
 
+// my count word (parity par) written by the neighbour at offset index poff
+const unsigned long long* lag_peer_my_count(PeerState* ps, int par, int poff) {
+    return ps->flags + (F_CNT + (par & 1)) * kOff + poff;
+}
+
 // The fused exchange (see peer_exchange_kernel).  halo: this cycle's ghost
 // exchange (seq = the cycle, already incremented); otherwise the write-cycle
 // flush of cycle seq's hand-offs (signal particles(seq), wait for the
@@ -244,19 +253,29 @@ lag_status lag_peer_exchange(lag_ctx_s* ctx, PeerState* ps, const void* send_box
     x.signal_halo = halo ? 1 : 0;
     x.npeers = np;
     for (int i = 0; i < np; ++i) {
-        x.halo_flag[i] = lag_peer_remote_flag(ps, i, 0, pback[i]);
+        x.halo_flag[i] = lag_peer_remote_flag(ps, i, F_HALO, pback[i]);
         x.back[i] = poff[i];
     }
     x.my_flags = ps->flags;
     x.need_halo = halo ? seq : 0;
     x.need_part = halo ? 0 : seq;
+    // counts published with the signal: per cycle, of the slots the advect
+    // filled last cycle (parity seq-1), in count parity seq; at the write
+    // cycle, of this cycle's slots, in count parity seq+1
+    const int slot_par = (int)((halo ? seq + kSlotParities - 1 : seq) % kSlotParities);
+    const int cnt_par = (int)((halo ? seq : seq + 1) & 1);
+    x.send_cnt = 1;
+    for (int i = 0; i < np; ++i) {
+        x.my_hdr[i] = reinterpret_cast<const uint32_t*>(lag_peer_my_slot(ps, slot_par, poff[i]));
+        x.cnt_word[i] = lag_peer_remote_flag(ps, i, F_CNT + cnt_par, pback[i]);
+    }
     if (halo) {                                // my slots the advect fills next cycle
         x.nzero = np;
         for (int i = 0; i < np; ++i)
             x.zero_slot[i] = reinterpret_cast<uint32_t*>(lag_peer_my_slot(ps, (int)((seq + 1) % kSlotParities), poff[i]));
     } else {
         x.signal_part = 1;
-        for (int i = 0; i < np; ++i) x.part_flag[i] = lag_peer_remote_flag(ps, i, 1, pback[i]);
+        for (int i = 0; i < np; ++i) x.part_flag[i] = lag_peer_remote_flag(ps, i, F_PART, pback[i]);
     }
     x.timeout_cycles = 8000000000LL;
     x.err = ctx->words + W_ERR;

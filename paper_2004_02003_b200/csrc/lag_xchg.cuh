@@ -64,7 +64,23 @@ struct XchgArgs {
     // a slice the ghost pull writes was read by the previous advect kernel
     // (the same buffer passed again): pull only after that kernel ended
     int pull_wait;
+    // hand-off counts travel with the signal: the signalling thread copies my
+    // slot headers (the parity the neighbours append now) into their count
+    // words, so the receiver's append skips one remote round trip
+    int send_cnt;
+    const uint32_t* my_hdr[kMaxPeers];
+    unsigned long long* cnt_word[kMaxPeers];
 };
+
+// the signalling thread: counts, then the release fence, then the flags
+__device__ __forceinline__ void xchg_publish(const XchgArgs& x, unsigned long long* const* flag) {
+    if (x.send_cnt)
+        for (int p = 0; p < x.npeers; ++p)
+            *reinterpret_cast<volatile unsigned long long*>(x.cnt_word[p]) =
+                *reinterpret_cast<const volatile uint32_t*>(x.my_hdr[p]);
+    __threadfence_system();
+    for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(flag[p]) = x.seq;
+}
 
 __device__ __forceinline__ void xchg_pack_signal(const XchgArgs& x, int cta, int ncta) {
     for (int64_t i = (int64_t)cta * blockDim.x + threadIdx.x; i < x.sfl;
@@ -89,17 +105,13 @@ __device__ __forceinline__ void xchg_pack_signal(const XchgArgs& x, int cta, int
         if (atomicAdd(x.done_ctas, 1u) == (uint32_t)ncta - 1) {   // last CTA: halo(seq) ready
             *x.done_ctas = 0u;
             griddep_wait();                           // and my previous advect's hand-offs (see below)
-            __threadfence_system();
-            for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(x.halo_flag[p]) = x.seq;
+            xchg_publish(x, x.halo_flag);
         }
     }
 }
 
 __device__ __forceinline__ void xchg_wait_pull(const XchgArgs& x, const AppendArgs& ap, int cta, int ncta) {
-    if (x.signal_part && cta == 0 && threadIdx.x == 0) {
-        __threadfence_system();                       // releases the previous kernels' slot writes
-        for (int p = 0; p < x.npeers; ++p) *reinterpret_cast<volatile unsigned long long*>(x.part_flag[p]) = x.seq;
-    }
+    if (x.signal_part && cta == 0 && threadIdx.x == 0) xchg_publish(x, x.part_flag);   // write cycle
     if (threadIdx.x < x.npeers) {
         const volatile unsigned long long* fh = x.my_flags + 0 * kOff + x.back[threadIdx.x];
         const volatile unsigned long long* fp = x.my_flags + 1 * kOff + x.back[threadIdx.x];
@@ -112,11 +124,21 @@ __device__ __forceinline__ void xchg_wait_pull(const XchgArgs& x, const AppendAr
     }
     __syncthreads();
     if (cta == 0 && threadIdx.x < x.nzero) *x.zero_slot[threadIdx.x] = 0u;
+    // the append (remote hand-off records) and the ghost pull (remote face
+    // values) run side by side: a quarter of the CTAs append
+    int na = x.do_append ? max(1, ncta / 4) : 0;
+    if (ncta - na < 1) na = 0;                        // too few CTAs: each does both
+    if (cta < na) {
+        griddep_wait();                               // the previous advect kernel's particle lists
+        append_body(ap, cta, na);
+        return;
+    }
+    const int pc = cta - na, npc = ncta - na;
     if (x.pull_wait) griddep_wait();
     // remote loads: 8 in flight per thread (a few CTAs cover the ghost layers
     // when they run inside the advect kernel's pass 1)
-    const int64_t step = (int64_t)ncta * blockDim.x;
-    for (int64_t i0 = (int64_t)cta * blockDim.x + threadIdx.x; i0 < x.rtotal; i0 += 8 * step) {
+    const int64_t step = (int64_t)npc * blockDim.x;
+    for (int64_t i0 = (int64_t)pc * blockDim.x + threadIdx.x; i0 < x.rtotal; i0 += 8 * step) {
         float val[8];
         float* dst[8];
 #pragma unroll
@@ -143,8 +165,10 @@ __device__ __forceinline__ void xchg_wait_pull(const XchgArgs& x, const AppendAr
         for (int u = 0; u < 8; ++u)
             if (dst[u]) *dst[u] = val[u];
     }
-    griddep_wait();                                   // the previous advect kernel's particle lists
-    if (x.do_append) append_body(ap, cta, ncta);                         // hand-offs of cycle seq-1 (all CTAs)
+    if (x.do_append && na == 0) {
+        griddep_wait();                               // the previous advect kernel's particle lists
+        append_body(ap, cta, ncta);
+    }                         // hand-offs of cycle seq-1 (all CTAs)
 }
 
 // exchange role of the advect kernel's pass 1 (LAG_XCHG_PEER_OVERLAP)
