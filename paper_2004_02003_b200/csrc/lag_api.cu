@@ -28,11 +28,16 @@ static thread_local std::string g_init_error = "no error";
 template <int DIM, bool FROZEN>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 advect_xchg_kernel(const AdvectArgs a, const XchgFused xf) {
+    // a programmatic dependent of the previous pass 2: the exchange CTAs pack
+    // and pull at once and wait for it only to signal and append (lag_xchg.cuh);
+    // the advect CTAs wait for it first (its tile lists, this cycle's snapshot)
+    griddep_launch();
     if ((int)blockIdx.x < xf.ncta) {
         xchg_pack_signal(xf.x, blockIdx.x, xf.ncta);
         xchg_wait_pull(xf.x, xf.ap, blockIdx.x, xf.ncta);
         return;
     }
+    griddep_wait();
     advect_body<DIM, false, FROZEN, true>(a, blockIdx.x - xf.ncta, gridDim.x - xf.ncta);
 }
 
@@ -326,6 +331,8 @@ extern "C" lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out
     SeedArgs sa{};
     sa.state = ctx->state; sa.tile_count = ctx->tile_count; sa.n_tiles = ctx->n_tiles; sa.stride = stride;
     sa.n_tiles_word = ctx->cfg.mode == LAG_COMM ? ctx->words + W_NTILES : nullptr;
+    sa.snap_b = ctx->cfg.mode == LAG_COMM ? ctx->words + W_NTILES_B : nullptr;
+    sa.snap_defer = ctx->cfg.mode == LAG_COMM ? ctx->words + W_DEFER : nullptr;
     for (int a = 0; a < 3; ++a) { sa.first[a] = ctx->first[a]; sa.ns[a] = ctx->ns[a]; }
     sa.by = ctx->brick[0]; sa.bz = ctx->brick[1];
     sa.bx = ctx->bits[0]; sa.by_bits = ctx->bits[1];
@@ -418,11 +425,9 @@ static lag_status advect_enqueue(lag_ctx_s* ctx, float* d0, float* d1, double dt
     const bool overlap = ctx->cfg.mode == LAG_COMM && lag_comm_overlap(ctx);
     XchgFused xf{};
     if (overlap) {
-        // tile count before this cycle's append, empty deferral list; the
-        // exchange is not launched here: pass 1's first CTAs run it
-        CK(cudaMemcpyAsync(ctx->words + W_NTILES_B, ctx->words + W_NTILES, sizeof(uint32_t),
-                           cudaMemcpyDeviceToDevice, ctx->stream));
-        CK(cudaMemsetAsync(ctx->words + W_DEFER, 0, sizeof(uint32_t), ctx->stream));
+        // the exchange is not launched here: pass 1's first CTAs run it
+        // (the tile count before its append and the empty deferral list of
+        // this cycle were set by the previous pass 2 or by the seed kernel)
         ctx->xchg_fused = &xf;
         st = lag_comm_pre_advect(ctx, d0, d1, v0_prev);
         ctx->xchg_fused = nullptr;
@@ -483,9 +488,12 @@ static lag_status advect_enqueue(lag_ctx_s* ctx, float* d0, float* d1, double dt
             else if (cmax < cmin) { a.smin[ax] = 1 << 29; a.sspan[ax] = 0; }      // nothing ghost-free
             else { a.smin[ax] = cmin - a.gmin[ax]; a.sspan[ax] = cmax - cmin; }
         }
-        a.n_tiles_b = ctx->words + W_NTILES_B;
+        const int par = (int)(ctx->cycles_total & 1);
+        a.n_tiles_b = ctx->words + W_NTILES_B + par;
         a.defer_list = ctx->defer_list;
-        a.defer_count = ctx->words + W_DEFER;
+        a.defer_count = ctx->words + W_DEFER + par;
+        a.next_b = ctx->words + W_NTILES_B + (par ^ 1);
+        a.next_defer = ctx->words + W_DEFER + (par ^ 1);
     }
 
     const int tiles = ctx->cfg.mode == LAG_COMM ? ctx->cap_tiles : ctx->n_tiles;
@@ -524,24 +532,24 @@ static lag_status advect_enqueue(lag_ctx_s* ctx, float* d0, float* d1, double dt
         a1.pass = 1;
         const int nb1 = std::max(blocks, kXchgCtas + 1);
         if (ev) cudaEventRecord(ev[1], ctx->stream);
-        if (D == 3) {
-            if (a.frozen) advect_xchg_kernel<3, true><<<nb1, kThreads, 0, ctx->stream>>>(a1, xf);
-            else advect_xchg_kernel<3, false><<<nb1, kThreads, 0, ctx->stream>>>(a1, xf);
-        } else {
-            if (a.frozen) advect_xchg_kernel<2, true><<<nb1, kThreads, 0, ctx->stream>>>(a1, xf);
-            else advect_xchg_kernel<2, false><<<nb1, kThreads, 0, ctx->stream>>>(a1, xf);
-        }
+        // both passes are programmatic dependents of the kernel before them
+        cudaLaunchConfig_t l1{};
+        l1.gridDim = dim3(nb1); l1.blockDim = dim3(kThreads); l1.stream = ctx->stream;
+        l1.attrs = &pdl; l1.numAttrs = 1;
+        if (D == 3) CK(a.frozen ? cudaLaunchKernelEx(&l1, advect_xchg_kernel<3, true>, a1, xf)
+                                : cudaLaunchKernelEx(&l1, advect_xchg_kernel<3, false>, a1, xf));
+        else CK(a.frozen ? cudaLaunchKernelEx(&l1, advect_xchg_kernel<2, true>, a1, xf)
+                         : cudaLaunchKernelEx(&l1, advect_xchg_kernel<2, false>, a1, xf));
         ++ctx->launches;
         if (ev) cudaEventRecord(ev[2], ctx->stream);
         AdvectArgs a2 = a;
         a2.pass = 2;
-        if (D == 3) {
-            if (a2.frozen) advect_kernel<3, false, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a2);
-            else advect_kernel<3, false, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a2);
-        } else {
-            if (a2.frozen) advect_kernel<2, false, true, true><<<blocks, kThreads, 0, ctx->stream>>>(a2);
-            else advect_kernel<2, false, false, true><<<blocks, kThreads, 0, ctx->stream>>>(a2);
-        }
+        cudaLaunchConfig_t l2 = l1;
+        l2.gridDim = dim3(blocks);
+        if (D == 3) CK(a2.frozen ? cudaLaunchKernelEx(&l2, advect_kernel<3, false, true, true>, a2)
+                                 : cudaLaunchKernelEx(&l2, advect_kernel<3, false, false, true>, a2));
+        else CK(a2.frozen ? cudaLaunchKernelEx(&l2, advect_kernel<2, false, true, true>, a2)
+                          : cudaLaunchKernelEx(&l2, advect_kernel<2, false, false, true>, a2));
     } else {
         CK(launch(a, blocks));
     }

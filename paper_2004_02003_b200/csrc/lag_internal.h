@@ -7,7 +7,8 @@
 #include <string>
 
 namespace lag {
-enum : int { W_DEAD = 0, W_ERR = 1, W_NTILES = 2, W_APPEND_DONE = 3, W_NTILES_B = 4, W_DEFER = 5, kWords = 8 };
+// W_NTILES_B / W_DEFER: overlap transport, two words each (cycle parity)
+enum : int { W_DEAD = 0, W_ERR = 1, W_NTILES = 2, W_APPEND_DONE = 3, W_NTILES_B = 4, W_DEFER = 6, kWords = 8 };
 struct Comm;         // lag_comm.cu
 struct LocalGroup;   // lag_comm.cu (LAG_XCHG_LOCAL)
 }

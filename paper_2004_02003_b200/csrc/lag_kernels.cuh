@@ -69,6 +69,8 @@ struct AdvectArgs {
     // this cycle's exchange.  pass 0: every tile.
     int32_t pass;
     const uint32_t* n_tiles_b;      // tile count before this cycle's append
+    uint32_t* next_b;               // pass 2 sets the next cycle's n_tiles_b / defer_count
+    uint32_t* next_defer;           // (the other parity's words)
     uint32_t* defer_list;
     uint32_t* defer_count;
     int32_t smin[3], sspan[3];      // ghost-free cells (gather offsets): samples stay off ghost nodes
@@ -448,12 +450,22 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         } else if (a.pass == 2) {
             n_def = (int)*a.defer_count;
             n_b = (int)*a.n_tiles_b;
+            // the tile count is final for this cycle: the next cycle's pass 1
+            // starts from it with an empty deferral list
+            if (cta == 0 && threadIdx.x == 0) { *a.next_b = (uint32_t)n_tiles; *a.next_defer = 0u; }
             n_tiles = n_def + (n_tiles - n_b);
         }
     }
     auto real_tile = [&](int v) -> int {
         if constexpr (!BTO && PASSES) {
             if (a.pass == 2) return v < n_def ? (int)a.defer_list[v] : n_b + (v - n_def);
+            // pass 1: the tiles next to a face come in runs (one x-run of a
+            // brick: 16 consecutive tiles in 64), and the grid's warp count is
+            // a multiple of 64, so a plain stride hands some warps only tiles
+            // that are deferred; rotating each full chunk of 64 tiles by its
+            // chunk index spreads them over all warps (a bijection; locality
+            // stays within the chunk)
+            if ((v | 63) < n_tiles) return (v & ~63) | (((v & 63) + (v >> 6)) & 63);
         }
         return v;
     };
@@ -635,6 +647,8 @@ struct SeedArgs {
     float4* state;
     uint8_t* tile_count;
     uint32_t* n_tiles_word;         // COMM: device-side tile count to initialise (or nullptr)
+    uint32_t* snap_b;               // COMM: the overlap transport's two tile-count snapshots
+    uint32_t* snap_defer;           //       and two deferral counts (cycle parity)
     int64_t n_tiles;                // tiles of the brick layout (>= ceil(n / 32))
     int32_t first[3], stride, ns[3];
     int32_t by, bz;                 // brick rows (y, z) of 32-seed tiles
@@ -662,6 +676,10 @@ static __global__ void seed_kernel(const SeedArgs a) {
     // 32-bit index math: tiles * 32 < 2^31 (lag_init bounds the slice)
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0 && a.n_tiles_word) *a.n_tiles_word = (uint32_t)a.n_tiles;
+    if (i == 0 && a.snap_b) {                  // overlap transport: either parity may come first
+        a.snap_b[0] = a.snap_b[1] = (uint32_t)a.n_tiles;
+        a.snap_defer[0] = a.snap_defer[1] = 0u;
+    }
     if (i >= (int)a.n_tiles * kTile) return;
     const int t = i >> 5, lane = i & 31;
     const int tb = a.by * a.bz;
