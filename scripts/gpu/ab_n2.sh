@@ -14,8 +14,8 @@ v = sys.argv[1]
 t = open(f"gpurun_out/ab_{v}.json").read(); d = json.loads(t[t.index("{"):])
 p = d["max_over_ranks"]["comm_peer"]
 t = open(f"gpurun_out/ab_bench_{v}.json").read(); b = json.loads(t[t.index("{"):].splitlines()[0])
-c = b["comm"]["peer"]
-print(f"{v:14s} phases: cycle {p['us_per_cycle_event']:.1f} pre {p['pre_exchange_us']:.1f} adv {p['advect_us']:.1f} | bench: bto {1e3*b['config']['ms_per_cycle']:.1f} peer {1e3*c['ms_per_cycle']:.1f} us/cycle ratio {c['bto_speedup']:.3f}")
+c = b["comm"]["peer"]; o = b["comm"]["peer_overlap"]
+print(f"{v:14s} phases: cycle {p['us_per_cycle_event']:.1f} pre {p['pre_exchange_us']:.1f} adv {p['advect_us']:.1f} | bench: bto {1e3*b['config']['ms_per_cycle']:.1f} peer {1e3*c['ms_per_cycle']:.1f} us/cycle ratio {c['bto_speedup']:.3f} | overlap {1e3*o['ms_per_cycle']:.1f} ratio {o['bto_speedup']:.3f}")
 PY
 done
 done

@@ -37,14 +37,16 @@ def main():
         for c in range(1, arm.interval):
             r = t[c]
             p1 = max(r[1], r[2])
-            rows.append([(r[1] - r[0]) / 1e3, (r[2] - r[0]) / 1e3, (r[3] - p1) / 1e3, (r[4] - r[3]) / 1e3])
-        med = np.median(np.array(rows), axis=0).tolist()
+            nxt = t[c + 1][0] if c + 1 < arm.interval else 0
+            rows.append([(r[1] - r[0]) / 1e3, (r[5] - r[0]) / 1e3, (r[2] - r[0]) / 1e3, (r[3] - p1) / 1e3,
+                         (r[4] - r[3]) / 1e3, ((nxt - r[4]) / 1e3) if nxt else float("nan")])
+        med = np.nanmedian(np.array(rows), axis=0).tolist()
         allr = [None] * world
         dist.all_gather_object(allr, med)
         res[fl] = allr
     arm.ctx.close()
     if rank == 0:
-        print("median us per cycle [exchange CTAs end, pass-1 advect end, gap to pass 2, pass 2] per rank")
+        print("median us per cycle [exchange CTAs end, pass-1 advect start, pass-1 advect end, gap to pass 2, pass 2, gap to next pass 1] per rank (from pass-1 entry)")
         print(json.dumps(res, indent=1))
     dist.destroy_process_group()
 
