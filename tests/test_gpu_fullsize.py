@@ -105,7 +105,7 @@ def test_c4_full_size_block_sampled(interval):
     assert n == 64 ** 3
     assert res["exit"] > 0                    # seeds on the global faces leave the domain
     # (at this CFL a stride-4 seed needs > 50 cycles to cross the 4 nodes to
-    # an internal face; the termination path is covered by the C3/C5/C2 cases)
+    # an internal face; the interval-100 case below asserts terminations)
 
 
 @pytest.mark.parametrize("rank", [0, 7])
@@ -134,6 +134,9 @@ def test_c4_full_size_interval_100_twin_criterion():
     orc, tw, start, end, status, st, n = _lockstep(cfg, b, cfg["stride"], 100, near=12, twin=1e-6, raw=True)
     h = np.array(cfg["grid"].spacing[:3])
     assert n == 64 ** 3 and st["particle_steps"] > 0
+    # over 100 cycles the seeds near the internal faces reach them: BTO
+    # terminations at an internal face at stride 4, full size
+    assert int((orc.status == oracle.TERM_BOUNDARY).sum()) > 0 and int((status == oracle.TERM_BOUNDARY).sum()) > 0
     np.testing.assert_allclose(start, orc.start, rtol=0, atol=1e-12 * np.abs(orc.start).max())
     flag_bad = (status != orc.status) & (orc.min_face >= EXCUSE_CELLS) & (tw.status == orc.status)
     assert not flag_bad.any(), ("flag mismatch the twin does not share", int(flag_bad.sum()))
@@ -145,4 +148,5 @@ def test_c4_full_size_interval_100_twin_criterion():
         "GPU deviation beyond 1e-4 cells larger than the twin's",
         int((beyond & (twin_dev < err)).sum()), float(err.max()))
     print({"n_sample": int(status.size), "valid_both": int(both.sum()), "max_err_cells": float(err.max()),
+           "term_gpu": int((status == oracle.TERM_BOUNDARY).sum()),
            "beyond_1e-4": int(beyond.sum()), "twin_dev_median": float(np.median(twin_dev))})
