@@ -526,7 +526,7 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
                 }
             }
         }
-        const int idx1 = live ? vindex<DIM>(a, v1c) : 0;     // stage-1 cell origin (node index)
+        int idx1 = live ? vindex<DIM>(a, v1c) : 0;           // stage-1 cell origin (node index)
         LAG_CHECK_GATHER(a, idx1, live);
         int cur = idx1;                                      // cell held by the corner cache
         float k1[3];
@@ -544,6 +544,22 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
 #pragma unroll
             for (int ax = 0; ax < DIM; ++ax) k1[ax] = __ldg(pv + ax);
             if constexpr (DIM == 2) k1[2] = 0.f;
+            // the stage samples move along k1: on an axis where it is
+            // negative they fall into the cell below the node, so take that
+            // cell as the frame (f = 1, the same point) when it is a gather
+            // cell; the samples then stay in one cell and no lane relocates.
+            // Not in overlap pass 1, whose ghost-free test holds for samples
+            // within one cell of the unshifted frame.
+            bool moved = false;
+            const bool shift = !PASSES || a.pass != 1;
+#pragma unroll
+            for (int ax = 0; ax < DIM; ++ax) {
+                const bool down = shift & (f1[ax] == 0.f) & (k1[ax] < 0.f) & (v1c[ax] > 0);
+                v1c[ax] -= down ? 1 : 0;
+                f1[ax] = down ? 1.f : f1[ax];
+                moved |= down;
+            }
+            if (moved && live) idx1 = vindex<DIM>(a, v1c);
             cur = -1;
         } else {
             gather_pairs<DIM>(a.v0, idx1, a.sx, a.sxy, S);
