@@ -4,6 +4,7 @@ mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/c0_tests.log 2>&1; tail -2 gpurun_out/c0_tests.log
 timeout 300 python scripts/time_advect.py C5 1 2>&1 | tail -2
 timeout 300 python scripts/time_advect.py C4 0 2>&1 | tail -2
+timeout 300 python scripts/time_advect.py C3 0 2>&1 | tail -2
 timeout 900 python bench.py --no-cpu --no-e2e > gpurun_out/c0_bench.json 2> gpurun_out/c0_bench.err
 python - <<'PY'
 import json
