@@ -253,7 +253,8 @@ __device__ __forceinline__ bool in_unit_cell(const float fs[3]) {
 // Latches non-finite samples (non-finite velocity reached the particle).
 template <int DIM, bool BTO, bool PASSES>
 __device__ __forceinline__ int stage_moved(const AdvectArgs& a, const int v1[3], const float fs[3],
-                                        uint8_t& st, bool& ghost_bad, uint32_t& errbits, float f[3]) {
+                                        uint8_t& st, bool& ghost_bad, uint32_t& errbits, float f[3],
+                                        int shifted = 0) {
     int v[3] = {0, 0, 0};
     bool ok = true, finite = true;
 #pragma unroll
@@ -278,8 +279,10 @@ __device__ __forceinline__ int stage_moved(const AdvectArgs& a, const int v1[3],
         // within one cell of them (CFL < 1); a farther sample may read ghost
         // nodes the exchange CTAs are writing: latched as a ghost error
         if (a.pass == 1) {
+            // within one cell of the stage-1 cell the tile was judged by (the
+            // frame is one cell below it on the axes of `shifted`, first cycle)
 #pragma unroll
-            for (int ax = 0; ax < DIM; ++ax) ghost_bad |= (unsigned)(v[ax] - v1[ax] + 1) > 2u;
+            for (int ax = 0; ax < DIM; ++ax) ghost_bad |= (unsigned)(v[ax] - v1[ax] + 1 - ((shifted >> ax) & 1)) > 2u;
         }
     }
     return vindex<DIM>(a, v);
@@ -294,7 +297,8 @@ __device__ __forceinline__ int stage_moved(const AdvectArgs& a, const int v1[3],
 template <int DIM, bool BTO, bool FROZEN, bool PASSES, int SLICES>
 __device__ __forceinline__ void stage_locate(const AdvectArgs& a, bool active, const int v1[3], int idx1,
                                              const float fs[3], int& cur, uint8_t& st, bool& ghost_bad,
-                                             uint32_t& errbits, float f[3], f2_t* S, f2_t* B) {
+                                             uint32_t& errbits, float f[3], f2_t* S, f2_t* B,
+                                             int shifted = 0) {
     constexpr int NP = Pairs<DIM>::n;
     const bool same = in_unit_cell<DIM>(fs);
 #pragma unroll
@@ -303,7 +307,7 @@ __device__ __forceinline__ void stage_locate(const AdvectArgs& a, bool active, c
     if (__any_sync(0xffffffffu, need)) {
         if (need) {
             int idx = idx1;
-            if (!same) idx = stage_moved<DIM, BTO, PASSES>(a, v1, fs, st, ghost_bad, errbits, f);
+            if (!same) idx = stage_moved<DIM, BTO, PASSES>(a, v1, fs, st, ghost_bad, errbits, f, shifted);
             LAG_CHECK_GATHER(a, idx, st == ST_VALID);
             if (st == ST_VALID && idx != cur) {
                 if constexpr (SLICES == 2) {
@@ -529,6 +533,7 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         int idx1 = live ? vindex<DIM>(a, v1c) : 0;           // stage-1 cell origin (node index)
         LAG_CHECK_GATHER(a, idx1, live);
         int cur = idx1;                                      // cell held by the corner cache
+        int shifted = 0;                                     // first cycle: axes framed one cell below
         float k1[3];
         if (a.cycle == 0 && __all_sync(0xffffffffu, !live || ((d[0] == 0.f) & (d[1] == 0.f) & (d[2] == 0.f)))) {
             // every particle sits on its seed node (first cycle of an interval;
@@ -547,17 +552,16 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
             // the stage samples move along k1: on an axis where it is
             // negative they fall into the cell below the node, so take that
             // cell as the frame (f = 1, the same point) when it is a gather
-            // cell; the samples then stay in one cell and no lane relocates.
-            // Not in overlap pass 1, whose ghost-free test holds for samples
-            // within one cell of the unshifted frame.
+            // cell; the samples then stay in one cell and no lane relocates
+            // (overlap pass 1 still judges them against the unshifted cell)
             bool moved = false;
-            const bool shift = !PASSES || a.pass != 1;
 #pragma unroll
             for (int ax = 0; ax < DIM; ++ax) {
-                const bool down = shift & (f1[ax] == 0.f) & (k1[ax] < 0.f) & (v1c[ax] > 0);
+                const bool down = (f1[ax] == 0.f) & (k1[ax] < 0.f) & (v1c[ax] > 0);
                 v1c[ax] -= down ? 1 : 0;
                 f1[ax] = down ? 1.f : f1[ax];
                 moved |= down;
+                shifted |= (down ? 1 : 0) << ax;
             }
             if (moved && live) idx1 = vindex<DIM>(a, v1c);
             cur = -1;
@@ -578,21 +582,21 @@ __device__ __forceinline__ void advect_body(const AdvectArgs& a, const int cta, 
         // ---- stage 2: q2 = x + dt/2 k1, alpha = 1/2 ----
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) e[ax] = ax < DIM ? fmaf(a.hdth[ax], k1[ax], f1[ax]) : 0.f;
-        stage_locate<DIM, BTO, FROZEN, PASSES, 2>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
+        stage_locate<DIM, BTO, FROZEN, PASSES, 2>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B, shifted);
         float T2[3];
         interp_pairs<DIM>(S, f, T2);                          // T2 = 2 k2
 
         // ---- stage 3: q3 = x + dt/2 k2 = x + dt/4 T2, alpha = 1/2 ----
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) e[ax] = ax < DIM ? fmaf(a.qdth[ax], T2[ax], f1[ax]) : 0.f;
-        stage_locate<DIM, BTO, FROZEN, PASSES, 2>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
+        stage_locate<DIM, BTO, FROZEN, PASSES, 2>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B, shifted);
         float T3[3];
         interp_pairs<DIM>(S, f, T3);                          // T3 = 2 k3
 
         // ---- stage 4: q4 = x + dt k3 = x + dt/2 T3, alpha = 1 ----
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) e[ax] = ax < DIM ? fmaf(a.hdth[ax], T3[ax], f1[ax]) : 0.f;
-        stage_locate<DIM, BTO, FROZEN, PASSES, 1>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B);
+        stage_locate<DIM, BTO, FROZEN, PASSES, 1>(a, live, v1c, idx1, e, cur, st, ghost_bad, errbits, f, S, B, shifted);
         float k4[3];
         interp_pairs<DIM>(B, f, k4);
 
