@@ -30,7 +30,7 @@ import paper_2004_02003_b200 as P  # noqa: E402
 
 
 def run_block(cfg, block, layout, rank, world, mode, slices, stride, nccl_id=None, exchange=0,
-              reseed_mid=None):
+              reseed_mid=None, second=False):
     g = cfg["grid"]
     ghost = 1 if mode == P.LAG_COMM else 0
     lo = [block.lo[a] - ghost if a < g.dim else 0 for a in range(3)]
@@ -61,6 +61,15 @@ def run_block(cfg, block, layout, rank, world, mode, slices, stride, nccl_id=Non
         # in flight must be dropped, so the interval that follows is a fresh one
         for k in range(reseed_mid):
             ctx.advect(dev[k], dev[k + 1], cfg["dt"])
+        n = ctx.seed(stride)
+    if second:
+        # a whole interval with its write cycle first (the last cycle's
+        # hand-offs flushed, particles returned to their origin): the
+        # interval that follows must equal a fresh context's
+        for k in range(len(dev) - 1):
+            ctx.advect(dev[k], dev[k + 1], cfg["dt"])
+        o = [torch.empty((n, g.dim), dtype=torch.float64, device="cuda") for _ in range(2)]
+        ctx.extract(o[0], o[1], torch.empty((n,), dtype=torch.uint8, device="cuda"), flags=P.LAG_NO_RESEED)
         n = ctx.seed(stride)
     for k in range(len(dev) - 1):
         ctx.advect(dev[k], dev[k + 1], cfg["dt"])
@@ -110,7 +119,18 @@ def main():
     dist.broadcast_object_list(obj4, src=0)
     rsd = run_block(cfg, me, layout, rank, world, P.LAG_COMM, slices, stride, nccl_id=obj4[0],
                     exchange=P.LAG_XCHG_PEER, reseed_mid=5)
+    sec = []
+    for xch in (P.LAG_XCHG_PEER, P.LAG_XCHG_PEER_OVERLAP):
+        o5 = [P.lag_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(o5, src=0)
+        sec.append(run_block(cfg, me, layout, rank, world, P.LAG_COMM, slices, stride, nccl_id=o5[0],
+                             exchange=xch, second=True))
     bto = run_block(cfg, me, layout, rank, world, P.LAG_BTO, slices, stride)
+    sec_all = []
+    for x in sec:
+        xa = [None] * world
+        dist.all_gather_object(xa, x)
+        sec_all.append(xa)
     comm_all = [None] * world
     bto_all = [None] * world
     peer_all = [None] * world
@@ -153,6 +173,11 @@ def main():
         rm = sum(int(not np.array_equal(x, y)) for c, rz in zip(peer_all, rsd_all) for x, y in zip(c[:3], rz[:3]))
         report["peer_mid_reseed_vs_fresh_mismatching_arrays"] = rm
         ok &= rm == 0
+        # second interval after a write cycle == the first interval of a fresh context
+        sm = [sum(int(not np.array_equal(x, y)) for c, z in zip(peer_all, xa) for x, y in zip(c[:3], z[:3]))
+              for xa in sec_all]
+        report["second_interval_vs_fresh_mismatching_arrays"] = {"peer": sm[0], "peer_overlap": sm[1]}
+        ok &= sum(sm) == 0
         report["sent"] = sent
         report["received"] = recv
         ok &= mism == 0 and sent == recv and sent > 0

@@ -40,3 +40,5 @@ def test_mgpu_comm_and_bto(nproc, config, scale):
     assert rep["overlap_vs_nccl_bitwise_mismatching_arrays"] == 0 and rep["overlap_sent"] == rep["sent"]
     # a reseed in the middle of an interval drops the hand-offs in flight
     assert rep["peer_mid_reseed_vs_fresh_mismatching_arrays"] == 0
+    # the interval after a write cycle starts clean on both peer transports
+    assert rep["second_interval_vs_fresh_mismatching_arrays"] == {"peer": 0, "peer_overlap": 0}
