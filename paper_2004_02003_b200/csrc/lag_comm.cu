@@ -38,7 +38,6 @@ lag_status lag_peer_init(lag_ctx_s* ctx, ncclComm_t nccl, const std::vector<int>
 void lag_peer_destroy(PeerState* ps);
 float4* lag_peer_remote_slot(PeerState* ps, int i, int prank, int pback, int q);
 float4* lag_peer_my_slot(PeerState* ps, int q, int poff);
-float* lag_peer_outbox(PeerState* ps, int q);
 unsigned long long& lag_peer_seq(PeerState* ps);
 unsigned long long* lag_peer_remote_flag(PeerState* ps, int i, int kind, int pback);
 const unsigned long long* lag_peer_my_count(PeerState* ps, int par, int poff);

@@ -219,7 +219,6 @@ float4* lag_peer_remote_slot(PeerState* ps, int i, int prank, int pback, int q) 
            t[T_SLOT + pback];
 }
 
-float* lag_peer_outbox(PeerState* ps, int q) { return ps->outbox + (size_t)q * 2 * ps->halo_send_floats; }
 
 unsigned long long& lag_peer_seq(PeerState* ps) { return ps->seq; }
 
