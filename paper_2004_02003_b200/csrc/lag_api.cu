@@ -336,8 +336,13 @@ extern "C" lag_status lag_seed(lag_ctx ctx, int32_t stride, int64_t* n_seeds_out
     for (int a = 0; a < 3; ++a) { sa.first[a] = ctx->first[a]; sa.ns[a] = ctx->ns[a]; }
     sa.by = ctx->brick[0]; sa.bz = ctx->brick[1];
     sa.bx = ctx->bits[0]; sa.by_bits = ctx->bits[1];
-    const int64_t total = (int64_t)ctx->n_tiles * kTile;
-    seed_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(sa);
+    const dim3 bricks((unsigned)((ctx->ns[0] + kTile - 1) / kTile), (unsigned)((ctx->ns[1] + sa.by - 1) / sa.by),
+                      (unsigned)((ctx->ns[2] + sa.bz - 1) / sa.bz));
+    if (bricks.y > 65535u || bricks.z > 65535u) {
+        lag_set_error(ctx, "seed lattice too tall for the brick grid (%u x %u bricks in y, z)", bricks.y, bricks.z);
+        return LAG_EINVAL;
+    }
+    seed_kernel<<<bricks, dim3(kTile, sa.by, sa.bz), 0, ctx->stream>>>(sa);
     ++ctx->launches;
     CK(cudaGetLastError());
     ctx->seeded = true;

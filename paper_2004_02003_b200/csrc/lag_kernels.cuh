@@ -692,24 +692,23 @@ __host__ __device__ inline int64_t brick_tiles(const int32_t ns[3], int by, int 
     return nbx * nby * nbz * by * bz;
 }
 
+// One CTA per brick: grid (bricks in x, y, z), block (32 lanes, by rows,
+// bz rows), so the tile and its lattice row follow from the indices without
+// a division.
 static __global__ void seed_kernel(const SeedArgs a) {
-    // 32-bit index math: tiles * 32 < 2^31 (lag_init bounds the slice)
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x, ry = threadIdx.y, rz = threadIdx.z;
+    const int nbx = gridDim.x, nby = gridDim.y;
+    const int brick = blockIdx.x + nbx * (blockIdx.y + nby * blockIdx.z);
+    const int t = brick * (a.by * a.bz) + ry + a.by * rz;
+    const int i = t * kTile + lane;              // 32-bit: tiles * 32 < 2^31 (lag_init bounds the slice)
     if (i == 0 && a.n_tiles_word) *a.n_tiles_word = (uint32_t)a.n_tiles;
     if (i == 0 && a.snap_b) {                  // overlap transport: either parity may come first
         a.snap_b[0] = a.snap_b[1] = (uint32_t)a.n_tiles;
         a.snap_defer[0] = a.snap_defer[1] = 0u;
     }
-    if (i >= (int)a.n_tiles * kTile) return;
-    const int t = i >> 5, lane = i & 31;
-    const int tb = a.by * a.bz;
-    const int brick = t / tb, j = t - brick * tb;
-    const int nbx = (a.ns[0] + kTile - 1) / kTile, nby = (a.ns[1] + a.by - 1) / a.by;
-    const int bq = brick / nbx;
-    const int ix0 = (brick - bq * nbx) * kTile;
-    const int jz = j / a.by;
-    const int iy = (bq % nby) * a.by + (j - jz * a.by);
-    const int iz = (bq / nby) * a.bz + jz;
+    const int ix0 = blockIdx.x * kTile;
+    const int iy = blockIdx.y * a.by + ry;
+    const int iz = blockIdx.z * a.bz + rz;
     const bool row = iy < a.ns[1] && iz < a.ns[2];
     const int cnt = row ? min(a.ns[0] - ix0, kTile) : 0;
     if (lane < cnt) {
