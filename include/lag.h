@@ -110,9 +110,10 @@ typedef enum {
 /* lag_extract flags */
 #define LAG_NO_RESEED 1u    /* do not reseed after extracting */
 #define LAG_ASYNC     2u    /* do not synchronise: outputs must be device pointers of the
-                               ctx's device (or NULL), complete when ctx->stream passes
-                               this call's work; latched errors are reported by the next
-                               synchronous lag_extract (or seen in lag_stats) */
+                               ctx's device, page-locked host memory, or NULL; complete
+                               when ctx->stream passes this call's work; latched errors
+                               are reported by the next synchronous lag_extract (or seen
+                               in lag_stats) */
 
 typedef struct {
     int32_t dim;                 /* 2 or 3                                                */
@@ -224,10 +225,11 @@ LAG_API lag_status lag_advect_cycle(lag_ctx ctx, void* v_t, void* v_t1, double d
  * writing the outputs; a reported error is cleared.  Then reseeds with the
  * same stride unless flags & LAG_NO_RESEED.  With flags & LAG_ASYNC the call
  * only enqueues (no host synchronisation, for a simulation that must not
- * stall on the write cycle): BTO only needs device outputs; errors stay
- * latched across the reseed until a synchronous lag_extract reports them.
+ * stall on the write cycle): outputs in device or page-locked host memory;
+ * errors stay latched across the reseed until a synchronous lag_extract
+ * reports them.
  * Errors: LAG_ESTATE (no lag_seed; interval_index out of order),
- * LAG_EINVAL (capacity < n; LAG_ASYNC with a host output pointer), LAG_ENCCL
+ * LAG_EINVAL (capacity < n; LAG_ASYNC with a pageable host output), LAG_ENCCL
  * (NCCL failure or asynchronous communicator error).
  */
 LAG_API lag_status lag_extract(lag_ctx ctx, int64_t interval_index, double* start, double* end,

@@ -710,11 +710,22 @@ extern "C" lag_status lag_extract_ex(lag_ctx ctx, int64_t interval_index, double
     e.status = out_target(ctx, status, ctx->out_status);
     e.term_cycle = term_cycle ? out_target(ctx, term_cycle, ctx->out_cycle) : nullptr;
     const bool async = (flags & LAG_ASYNC) != 0;
-    if (async && ((start && (void*)e.start != (void*)start) || (end && (void*)e.end != (void*)end) ||
-                  (status && (void*)e.status != (void*)status) ||
-                  (term_cycle && (void*)e.term_cycle != (void*)term_cycle))) {
-        lag_set_error(ctx, "LAG_ASYNC needs device output pointers on device %d", ctx->cfg.device);
-        return LAG_EINVAL;
+    if (async) {
+        // device outputs of this device, or page-locked host outputs (copied
+        // from the staging buffers by stream-ordered asynchronous copies)
+        for (const void* p : {(const void*)start, (const void*)end, (const void*)status, (const void*)term_cycle}) {
+            if (!p) continue;
+            cudaPointerAttributes at{};
+            const bool ok = cudaPointerGetAttributes(&at, p) == cudaSuccess &&
+                            ((at.type == cudaMemoryTypeDevice && at.device == ctx->cfg.device) ||
+                             at.type == cudaMemoryTypeHost);
+            if (!ok) {
+                cudaGetLastError();
+                lag_set_error(ctx, "LAG_ASYNC needs device outputs on device %d or page-locked host outputs",
+                              ctx->cfg.device);
+                return LAG_EINVAL;
+            }
+        }
     }
     e.write_start = ctx->cfg.mode == LAG_BTO ? 1 : 0;
     const unsigned nb_seed = (unsigned)((ctx->n_seeds + 255) / 256);

@@ -345,9 +345,9 @@ def test_termination_cycles_match_oracle():
 
 def test_async_extract_matches_sync_and_keeps_errors_latched():
     """LAG_ASYNC enqueues the write cycle without a host sync: same bits as the
-    synchronous extract; a latched device error survives the asynchronous
-    write cycle and its reseed and is reported by the next synchronous one;
-    host outputs are refused."""
+    synchronous extract (device and page-locked host outputs); a latched
+    device error survives the asynchronous write cycle and its reseed and is
+    reported by the next synchronous one; pageable host outputs are refused."""
     import torch
     import paper_2004_02003_b200 as P
     cfg = L.make_config("C2", scale=21)
@@ -366,8 +366,14 @@ def test_async_extract_matches_sync_and_keeps_errors_latched():
     good = torch.zeros_like(bad)
     end = torch.empty((n, 3), dtype=torch.float64, device="cuda")
     with pytest.raises(P.LagError) as e:
-        ctx.extract(end=torch.empty((n, 3), dtype=torch.float64).pin_memory(), flags=P.LAG_ASYNC)
+        ctx.extract(end=torch.empty((n, 3), dtype=torch.float64), flags=P.LAG_ASYNC)   # pageable
     assert e.value.status == P.LAG_EINVAL
+    pinned = torch.full((n, 3), -1.0, dtype=torch.float64).pin_memory()
+    ctx.extract(end=pinned, flags=P.LAG_ASYNC | P.LAG_NO_RESEED)                     # enqueued copy
+    torch.cuda.synchronize()
+    ctx.extract(end=end, flags=P.LAG_NO_RESEED)
+    assert np.array_equal(pinned.numpy(), end.cpu().numpy())
+    n = ctx.seed(1)
     ctx.advect(bad, bad, 0.1)
     ctx.extract(end=end, flags=P.LAG_ASYNC)                  # enqueued, reseeded, error kept
     ctx.advect(good, good, 0.1)
