@@ -631,6 +631,9 @@ def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # rank 0 alone runs it: on all host cores (torchrun sets OMP_NUM_THREADS=1
+    # per process; the OpenMP runtime reads it when the oracle library loads)
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     import lag_inputs as L
     cfg = L.make_config(args.config, nranks=1)
     vals = []
